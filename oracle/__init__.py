@@ -1,0 +1,165 @@
+"""CPU oracle for the BinSketch hot path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package. The
+product path (``paper_1910_04658_b200``) must never import it, and shares no
+code with it (tests/test_independence.py checks this).
+
+``liboracle.so`` is built from ``oracle.cpp`` (plain C++17, fp64, no FMA
+contraction, OpenMP over rows). ``definitional.py`` is the per-bit
+pure-Python oracle for tiny inputs that pins it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+IP, HAM, JS, COS = 1, 2, 4, 8
+MEASURES = {"ip": IP, "ham": HAM, "js": JS, "cos": COS}
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle.cpp")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fopenmp", "-fPIC", "-shared",
+                               "-ffp-contract=off", src, "-o", _SO])
+    return _SO
+
+
+def _lib_():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        u64, u32, i32, vp, dbl, i64 = (ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32,
+                                       ctypes.c_void_p, ctypes.c_double, ctypes.c_int64)
+        L.orc_mix64.argtypes = [u64]; L.orc_mix64.restype = u64
+        L.orc_make_pi.argtypes = [u64, u64, u32, vp]; L.orc_make_pi.restype = None
+        L.orc_recommended_N.argtypes = [u32, dbl]; L.orc_recommended_N.restype = u32
+        L.orc_sketch.argtypes = [vp, u64, u32, vp, vp, u64, vp]; L.orc_sketch.restype = ctypes.c_int
+        L.orc_popcount.argtypes = [vp, u64, u32, vp]; L.orc_popcount.restype = None
+        L.orc_andpopc.argtypes = [vp, u64, vp, u64, u32, vp]; L.orc_andpopc.restype = None
+        L.orc_card_table.argtypes = [u32, u64, vp]; L.orc_card_table.restype = None
+        L.orc_estimate_pair.argtypes = [i32, i32, i32, u32, vp, vp]; L.orc_estimate_pair.restype = None
+        L.orc_estimate_literal.argtypes = [i32, i32, i32, u32, u64, vp]
+        L.orc_estimate_literal.restype = None
+        L.orc_estimate.argtypes = [vp, u64, vp, u64, u32, u64, u32, vp]; L.orc_estimate.restype = None
+        L.orc_topk.argtypes = [vp, u64, vp, u64, u32, u64, u32, u32, u32, vp, vp, ctypes.c_int]
+        L.orc_topk.restype = None
+        L.orc_exact.argtypes = [vp, i64, vp, i64, vp]; L.orc_exact.restype = None
+        L.orc_enumerate.argtypes = [u32, u32, vp, i64, vp, i64, vp, vp]
+        L.orc_enumerate.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data
+
+
+def words(N: int) -> int:
+    return (N + 31) // 32
+
+
+def mix64(z: int) -> int:
+    return int(_lib_().orc_mix64(z))
+
+
+def make_pi(seed: int, d: int, N: int) -> np.ndarray:
+    pi = np.empty(d, dtype=np.uint32)
+    _lib_().orc_make_pi(seed, d, N, _p(pi))
+    return pi
+
+
+def recommended_N(psi: int, rho: float) -> int:
+    return int(_lib_().orc_recommended_N(psi, rho))
+
+
+def sketch(pi: np.ndarray, d: int, N: int, indptr: np.ndarray, indices: np.ndarray):
+    """Returns (uint32[n][W], status)."""
+    n = len(indptr) - 1
+    out = np.empty((n, words(N)), dtype=np.uint32)
+    st = _lib_().orc_sketch(_p(np.ascontiguousarray(pi, dtype=np.uint32)), d, N,
+                            _p(np.ascontiguousarray(indptr, dtype=np.int64)),
+                            _p(np.ascontiguousarray(indices, dtype=np.int32)), n, _p(out))
+    return out, int(st)
+
+
+def popcount(sk: np.ndarray, N: int) -> np.ndarray:
+    sk = np.ascontiguousarray(sk, dtype=np.uint32)
+    out = np.empty(sk.shape[0], dtype=np.int32)
+    _lib_().orc_popcount(_p(sk), sk.shape[0], N, _p(out))
+    return out
+
+
+def andpopc(A: np.ndarray, B: np.ndarray, N: int) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.uint32)
+    B = np.ascontiguousarray(B, dtype=np.uint32)
+    out = np.empty((A.shape[0], B.shape[0]), dtype=np.int32)
+    _lib_().orc_andpopc(_p(A), A.shape[0], _p(B), B.shape[0], N, _p(out))
+    return out
+
+
+def card_table(N: int, d: int) -> np.ndarray:
+    L = np.empty(N + 1, dtype=np.float64)
+    _lib_().orc_card_table(N, d, _p(L))
+    return L
+
+
+def estimate_pair(pa: int, pb: int, pab: int, N: int, L: np.ndarray) -> np.ndarray:
+    out = np.empty(4, dtype=np.float64)
+    _lib_().orc_estimate_pair(pa, pb, pab, N, _p(L), _p(out))
+    return out
+
+
+def estimate_literal(pa: int, pb: int, pab: int, N: int, d: int) -> np.ndarray:
+    tr = np.empty(9, dtype=np.float64)
+    _lib_().orc_estimate_literal(pa, pb, pab, N, d, _p(tr))
+    return tr
+
+
+def estimate(A: np.ndarray, B: np.ndarray, N: int, d: int, measure: int) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.uint32)
+    B = np.ascontiguousarray(B, dtype=np.uint32)
+    planes = bin(measure & 15).count("1")
+    out = np.empty((planes, A.shape[0], B.shape[0]), dtype=np.float32)
+    _lib_().orc_estimate(_p(A), A.shape[0], _p(B), B.shape[0], N, d, measure, _p(out))
+    return out
+
+
+def topk(Q: np.ndarray, D: np.ndarray, N: int, d: int, measure: int, k: int,
+         exclude_self: bool = False, nthreads: int = 0):
+    Q = np.ascontiguousarray(Q, dtype=np.uint32)
+    D = np.ascontiguousarray(D, dtype=np.uint32)
+    idx = np.empty((Q.shape[0], k), dtype=np.int32)
+    sc = np.empty((Q.shape[0], k), dtype=np.float32)
+    _lib_().orc_topk(_p(Q), Q.shape[0], _p(D), D.shape[0], N, d, measure, k,
+                     1 if exclude_self else 0, _p(idx), _p(sc), nthreads)
+    return idx, sc
+
+
+def exact(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    b = np.ascontiguousarray(b, dtype=np.int32)
+    out = np.empty(4, dtype=np.float64)
+    _lib_().orc_exact(_p(a), len(a), _p(b), len(b), _p(out))
+    return out
+
+
+def enumerate_expectations(d: int, N: int, a, b):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.int32))
+    m1 = ctypes.c_double()
+    m2 = ctypes.c_double()
+    rc = _lib_().orc_enumerate(d, N, _p(a), len(a), _p(b), len(b), ctypes.byref(m1), ctypes.byref(m2))
+    if rc != 0:
+        raise ValueError("instance too large to enumerate")
+    return m1.value, m2.value
