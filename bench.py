@@ -1,0 +1,419 @@
+"""BinSketch hot-path benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload large|medium|ranking|buildonly|tiny] [--no-extras] [--no-cpu-baseline]
+
+Default workload = BASELINE.json configs[4] ("Large"): one step is the whole
+hot path on synthetic Zipf CSR already resident in HBM:
+  a1 make_pi (d = 500,000) -> a2 build 200,000 sketches (N = 1024) ->
+  a3 popcounts -> a4/a5/a6 all-pairs AND-popcount + fp64 IP estimate ->
+  a7 top-50 per row (self-join, self excluded).
+value = estimated pairs/s (4e10 ordered pairs per step per GPU). The
+build-only HBM measurement (configs[3]) is reported in "build".
+
+Multi-GPU (torchrun): every rank runs an independent problem instance (its
+own data seed) with no data-path collective; value = all ranks' pairs / max
+rank time ("scaling": "weak").
+
+--impl reference: the CPU oracle (oracle/, the reference arm of this tier)
+timed on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "sketch rows/s (HBM GB/s) and estimated pairs/s vs popc roofline, 1xB200"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SM_COUNT_B200 = 148
+POPC_PER_CLK_SM = 16          # CUDA C++ Programming Guide throughput table (cc 10.x); K9 calibrates
+HBM_FALLBACK_GBS = 6650.0     # B200_PROFILING.md fallback
+
+
+# ----------------------------------------------------------------- utils --
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": HBM_FALLBACK_GBS, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = max(smax, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------- workloads --
+def workload_spec(name):
+    import synth
+    if name == "large":
+        return dict(db=synth.LARGE, q=None, N=synth.LARGE_N, k=synth.LARGE_K, measure=1, exclude_self=True,
+                    desc="configs[4] Large: n=200000 sketches N=1024 from d=500000 CSR (lognormal mean 100, "
+                         "Zipf 1.1); build + self-join IP top-50 (self excluded)")
+    if name == "ranking":
+        return dict(db=synth.RANKING_DB, q=synth.RANKING_Q, N=synth.RANKING_N, k=synth.RANKING_K, measure=4,
+                    exclude_self=False,
+                    desc="configs[2] Ranking: db 100000 + 1000 queries, d=102660, N=4096; build + JS top-100")
+    if name == "tiny":
+        return dict(db=synth.TINY, q=None, N=synth.TINY_N, k=10, measure=4, exclude_self=True,
+                    desc="configs[0] Tiny: n=1000, d=5000, N=1224; build + JS top-10")
+    raise ValueError(name)
+
+
+def rank_spec(spec, rank):
+    import synth
+    if rank == 0:
+        return spec
+    return synth.CSRSpec(**{**spec.__dict__, "seed": spec.seed + 1000 * rank})
+
+
+# ------------------------------------------------------------- our arm ----
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_1910_04658_b200 import binsketch as bs
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pk, pk_src = peaks()
+
+    w = workload_spec(args.workload)
+    db_spec = rank_spec(w["db"], rank)
+    N, k, measure = w["N"], w["k"], w["measure"]
+    d = db_spec.d
+    W = (N + 31) // 32
+    ip_h, ix_h = synth.make_csr(db_spec)
+    n = db_spec.n
+    ip = torch.from_numpy(ip_h).cuda()
+    ix = torch.from_numpy(ix_h).cuda()
+    if w["q"] is not None:
+        qp_h, qx_h = synth.make_csr(rank_spec(w["q"], rank))
+        qp, qx = torch.from_numpy(qp_h).cuda(), torch.from_numpy(qx_h).cuda()
+        nq = w["q"].n
+    else:
+        qp_h = qx_h = qp = qx = None
+        nq = n
+    pi = torch.empty(d, dtype=torch.int32, device="cuda")
+    sk = torch.empty((n, W), dtype=torch.int32, device="cuda")
+    qsk = torch.empty((nq, W), dtype=torch.int32, device="cuda") if qp is not None else None
+    out_idx = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    out_score = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+    wsp = torch.empty(max(1, bs.workspace_bytes(bs.OP_TOPK, nq, n, N, k)), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+    nnz = int(ip_h[-1])
+
+    ev = {name: [] for name in ("step", "build", "topk")}
+
+    def step(record):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if record else None
+        if record:
+            e[0].record(stream)
+        bs.make_pi(synth.PI_SEED, d, N, out=pi)
+        bs.build(pi, d, N, ip, ix, out=sk)
+        if qp is not None:
+            bs.build(pi, d, N, qp, qx, out=qsk)
+        if record:
+            e[1].record(stream)
+        bs.topk(qsk if qsk is not None else sk, sk, N, d, measure, k, exclude_self=w["exclude_self"],
+                out_idx=out_idx, out_score=out_score, ws=wsp)
+        if record:
+            e[2].record(stream)
+            ev["step"].append((e[0], e[2]))
+            ev["build"].append((e[0], e[1]))
+            ev["topk"].append((e[1], e[2]))
+
+    for _ in range(args.warmup):
+        step(False)
+    bs.device_status()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = bs.launch_count()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()                          # L2 flush between timed steps (outside the events)
+            step(True)
+        torch.cuda.synchronize()
+    launches = bs.launch_count() - l0 - 0
+    bs.device_status()
+
+    def tot(name):
+        return sum(a.elapsed_time(b) for a, b in ev[name]) * 1e-3     # seconds over K steps
+
+    t_step, t_build, t_topk = tot("step"), tot("build"), tot("topk")
+    t_max = t_step
+    if ws > 1:
+        tt = torch.tensor([t_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    pairs_per_step = nq * n                       # ordered pairs scored (self pair included in the count)
+    value = ws * pairs_per_step * args.steps / t_max
+    clocks = clk.summary()
+
+    # --- e2e: host (pinned) CSR -> build -> top-k -> host results, through the public API ---
+    e2e = None
+    if w["q"] is None:
+        ip_pin = torch.from_numpy(ip_h).pin_memory()
+        ix_pin = torch.from_numpy(ix_h).pin_memory()
+        pi_pin = torch.empty(d, dtype=torch.int32).pin_memory()
+        pi_pin.copy_(pi.cpu())
+        bufs = {}
+        for _ in range(max(1, args.warmup)):
+            bs.rank_from_host_csr(ip_pin, ix_pin, pi_pin, d, N, measure, k, exclude_self=w["exclude_self"], bufs=bufs)
+        torch.cuda.synchronize()
+        tsum = 0.0
+        h2d = d2h = 0
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            _, _, h2d, d2h = bs.rank_from_host_csr(ip_pin, ix_pin, pi_pin, d, N, measure, k,
+                                                   exclude_self=w["exclude_self"], bufs=bufs)
+            b.record(stream)
+            b.synchronize()
+            tsum += a.elapsed_time(b) * 1e-3
+        if ws > 1:
+            tt = torch.tensor([tsum], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tsum = float(tt.item())
+        e2e = {"value": ws * pairs_per_step * args.steps / tsum, "unit": "pairs/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # --- roofline of the dominant kernel (top-k: AND+POPC mainloop) ---
+    f_sm = (clocks["sm_mhz"] or pk.get("sm_max_mhz", 1965.0)) * 1e6
+    sm_max = (clocks.get("sm_max_mhz") or pk.get("sm_max_mhz", 1965.0)) * 1e6
+    peak_words = SM_COUNT_B200 * POPC_PER_CLK_SM * sm_max            # word-ops/s at max clock
+    achieved_words = pairs_per_step * W * args.steps / t_topk
+    roofline = {"bound": "alu", "kernel": "topk_kernel (LOP3+POPC mainloop + fp64 epilogue)",
+                "achieved": achieved_words / 1e12, "peak": peak_words / 1e12, "unit": "Tword-popc/s",
+                "frac": achieved_words / peak_words,
+                "frac_at_measured_clock": achieved_words / (SM_COUNT_B200 * POPC_PER_CLK_SM * f_sm),
+                "peak_basis": f"148 SMs x {POPC_PER_CLK_SM} POPC/clk/SM x sm_max_mhz (guide table; DESIGN.md)",
+                "traffic": None}
+
+    result = {
+        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 (bit-packed sketches; fp64 estimator)",
+        "data": "synthetic (seeded Zipf-feature CSR, synth/; stands in for the paper's UCI corpora)",
+        "config": {"workload": args.workload, "desc": w["desc"], "n": n, "nq": nq, "d": d, "N": N, "k": k,
+                   "nnz": nnz, "measure": measure, "pairs_per_step": pairs_per_step,
+                   "l2": "flushed between timed steps (256 MB write outside the events)",
+                   "parallelism": f"independent instances x{ws} (no data-path collective)"},
+        "stages_ms_per_step": {"build": t_build / args.steps * 1e3, "topk": t_topk / args.steps * 1e3},
+        "build_rows_per_s": (n + (nq if qp is not None else 0)) * args.steps / t_build,
+        "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        "peaks_source": pk_src,
+    }
+
+    if rank == 0 and not args.no_extras and args.workload == "large":
+        result["build"] = bench_buildonly(args, bs, torch, pk, pk_src)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(args, w, ip_h, ix_h, qp_h, qx_h)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def bench_buildonly(args, bs, torch, pk, pk_src):
+    """configs[3]: 1e7 rows, d=2^20, N=1024: sketch rows/s and HBM GB/s vs the measured copy peak."""
+    import synth
+    spec, N = synth.BUILD_ONLY, synth.BUILD_ONLY_N
+    ip_h, ix_h = synth.make_csr(spec)
+    ip, ix = torch.from_numpy(ip_h).cuda(), torch.from_numpy(ix_h).cuda()
+    del ix_h
+    n, d, W = spec.n, spec.d, (N + 31) // 32
+    nnz = int(ip_h[-1])
+    pi = bs.make_pi(synth.PI_SEED, d, N)
+    out = torch.empty((n, W), dtype=torch.int32, device="cuda")
+    res = {}
+    alg_bytes = 4 * nnz + 8 * (n + 1) + 4 * W * n + 4 * d
+    for variant in ("table", "seeded"):
+        def call():
+            if variant == "table":
+                bs.build(pi, d, N, ip, ix, out=out)
+            else:
+                bs.build_seeded(synth.PI_SEED, d, N, ip, ix, out=out)
+        for _ in range(3):
+            call()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(5, args.steps)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            call()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        t = statistics.median(ts)
+        gbs = alg_bytes / t / 1e9
+        res[variant] = {"ms": t * 1e3, "rows_per_s": n / t, "hbm_gbs": gbs,
+                        "frac_of_measured_hbm": gbs / pk["hbm_gbs"], "frac_of_8TBs_datasheet": gbs / 8000.0}
+    bs.device_status()
+    res["config"] = {"workload": "buildonly (configs[3])", "n": n, "d": d, "N": N, "nnz": nnz,
+                     "algorithmic_bytes": alg_bytes, "bytes_formula": "4*nnz + 8*(n+1) + 4*W*n + 4*d",
+                     "peak_gbs": pk["hbm_gbs"], "peak_source": pk_src,
+                     "l2": "inputs 3.9 GB >> L2 (no flush needed)"}
+    del ip, ix, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def _oracle_sample_step(w, ip_h, ix_h, qp_h, qx_h, nsample, nthreads):
+    """One bounded oracle step: pi + sketches of all rows + top-k for `nsample` queries vs all rows."""
+    import oracle
+    import synth
+    N, d, k = w["N"], w["db"].d, w["k"]
+    pi = oracle.make_pi(synth.PI_SEED, d, N)
+    D, _ = oracle.sketch(pi, d, N, ip_h, ix_h)
+    if qp_h is not None:
+        Q, _ = oracle.sketch(pi, d, N, qp_h, qx_h)
+        Q = Q[:nsample]
+        oracle.topk(Q, D, N, d, w["measure"], k, exclude_self=False, nthreads=nthreads)
+    else:
+        oracle.topk(D[:nsample], D, N, d, w["measure"], k, exclude_self=w["exclude_self"], nthreads=nthreads)
+    return nsample * D.shape[0]
+
+
+def cpu_baseline(args, w, ip_h, ix_h, qp_h, qx_h):
+    nthreads = os.cpu_count() or 1
+    nsample = {"large": 2000, "ranking": 200, "tiny": 1000}[args.workload]
+    t0 = time.perf_counter()
+    pairs = _oracle_sample_step(w, ip_h, ix_h, qp_h, qx_h, nsample, nthreads)
+    t = time.perf_counter() - t0
+    return {"value": pairs / t, "unit": "pairs/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"oracle (oracle/oracle.cpp, OpenMP) on the same workload: pi + all {len(ip_h) - 1} sketches "
+                      f"+ top-{w['k']} for {nsample} query rows vs all db rows; {t:.1f} s"}
+
+
+# -------------------------------------------------------- reference arm ---
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    import synth
+    w = workload_spec(args.workload)
+    ip_h, ix_h = synth.make_csr(w["db"])
+    if w["q"] is not None:
+        qp_h, qx_h = synth.make_csr(w["q"])
+    else:
+        qp_h = qx_h = None
+    nthreads = os.cpu_count() or 1
+    nsample = {"large": 1000, "ranking": 100, "tiny": 1000}[args.workload]
+    for _ in range(args.warmup):
+        _oracle_sample_step(w, ip_h, ix_h, qp_h, qx_h, max(1, nsample // 10), nthreads)
+    t0 = time.perf_counter()
+    pairs = 0
+    for _ in range(args.steps):
+        pairs += _oracle_sample_step(w, ip_h, ix_h, qp_h, qx_h, nsample, nthreads)
+    t = time.perf_counter() - t0
+    v = pairs / t
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32/fp64 (CPU)", "data": "synthetic (same seeded generator)",
+        "config": {"workload": args.workload, "desc": w["desc"]},
+        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": nthreads, "kind": "oracle",
+                         "sample": f"each step: pi + all sketches + top-{w['k']} for {nsample} query rows vs all db rows"},
+        "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="large", choices=["large", "ranking", "tiny"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/* binsketch.h — C ABI of the B200-native BinSketch hot path (libbinsketch.so).
+ *
+ * Method: Pratap, Bera, Revanuru, "Efficient Sketching Algorithm for Sparse
+ * Binary Data", arXiv 1910.04658. Line citations are PAPER.md
+ * lines; SPEC.md lines where the paper is silent and SPEC's reading is
+ * adopted (R-*).
+ *
+ * Conventions shared by every entry point
+ * ----------------------------------------
+ *  - Array arguments are DEVICE pointers owned by the caller (e.g. torch
+ *    tensors), except where marked HOST. Inputs are read-only; outputs are
+ *    fully overwritten (including padding slots).
+ *  - Calls enqueue work on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream) and return without synchronising, except binsketch_device_status.
+ *  - The library keeps no device allocations of its own apart from one
+ *    4-byte latched device-status word; scratch memory comes from the caller's
+ *    workspace (see binsketch_workspace_bytes). It keeps a host-side cache of
+ *    cardinality tables keyed by (N, d), guarded by a mutex. Calls are pure
+ *    functions of their inputs and may be issued from many host threads on
+ *    different streams.
+ *  - Sketch layout (reading R-G10): a sketch of N bits is W = ceil(N/32)
+ *    uint32 words, bit j in word j/32 at bit position j%32 (LSB first); tail
+ *    bits (j >= N) are 0; row r starts at word r*W (row stride W words).
+ *  - Sparse binary rows are CSR: int64 indptr[n+1] (non-decreasing,
+ *    indptr[0] arbitrary base), int32 indices[...] in [0,d). Duplicate or
+ *    unsorted indices inside a row are allowed (OR is idempotent).
+ *  - No exceptions cross the ABI. Host-detectable errors return immediately
+ *    (nothing enqueued). Device-detectable input errors (index outside [0,d),
+ *    pi value >= N, decreasing indptr) are latched into the device-status
+ *    word and reported by binsketch_device_status; output contents are then
+ *    unspecified. Zero-sized problems (n = 0, na*nb = 0, k = 0) succeed
+ *    without enqueuing anything.
+ *  - Determinism: outputs are bit-identical for identical inputs, independent
+ *    of launch configuration.
+ */
+#ifndef BINSKETCH_H
+#define BINSKETCH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* binsketch_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  BINSKETCH_OK = 0,
+  BINSKETCH_EINVAL = 1,     /* bad argument (N < 2, null pointer with nonzero count, bad measure, ...) */
+  BINSKETCH_EINDEX = 2,     /* device-detected bad input (latched; see binsketch_device_status) */
+  BINSKETCH_ECUDA = 3,      /* a CUDA runtime call failed */
+  BINSKETCH_EWORKSPACE = 4, /* workspace too small */
+  BINSKETCH_EUNSUPPORTED = 5 /* valid request outside this build's limits (e.g. k > BINSKETCH_MAX_K) */
+} binsketch_status;
+
+/* Measures (bit mask). Planes of binsketch_estimate are written in this order. */
+enum {
+  BINSKETCH_IP = 1,  /* inner product |a ∩ b|, Algorithm 1            */
+  BINSKETCH_HAM = 2, /* Hamming |a|+|b|-2|a∩b|, Algorithm 2 (R-G2)      */
+  BINSKETCH_JS = 4,  /* Jaccard, Algorithm 3 (R-G3)                    */
+  BINSKETCH_COS = 8  /* cosine, Algorithm 4                            */
+};
+
+enum { BINSKETCH_TOPK_EXCLUDE_SELF = 1 };  /* topk flags: skip db row j == query row i */
+
+enum { BINSKETCH_MAX_K = 256 };            /* largest k binsketch_topk accepts */
+
+/* ops for binsketch_workspace_bytes */
+enum { BINSKETCH_OP_ANDPOPC = 1, BINSKETCH_OP_ESTIMATE = 2, BINSKETCH_OP_TOPK = 3 };
+
+/* W = ceil(N/32), words per sketch row. */
+uint32_t binsketch_words(uint32_t N);
+
+/* Theorem 1 sizing rule: N = psi*sqrt(psi/2*ln(2/rho)),
+ * made an integer as max(2, ceil(.)) (reading R-G5).
+ * Returns 0 on a domain error (psi = 0, rho not in (0,1)). Host only. */
+uint32_t binsketch_recommended_N(uint32_t psi, double rho);
+
+/* Random map pi:[d]->[N], generated on the device:
+ *   pi[i] = mix64(seed + (i+1)*0x9E3779B97F4A7C15) mod N,   i in [0,d)
+ * mix64 = splitmix64 finalizer (reading R-G8).
+ * pi: device uint32[d]. EINVAL if N < 2 or (d > 0 and pi == NULL). */
+binsketch_status binsketch_make_pi(uint64_t seed, uint64_t d, uint32_t N, uint32_t* pi,
+                                   binsketch_stream_t stream);
+
+/* Sketch construction, the BinSketch definition:
+ *   out_words[r] bit j = OR over e in [indptr[r], indptr[r+1]) of [pi[indices[e]] == j]
+ * pi: device uint32[d] (any table with values in [0,N));
+ * indptr: device int64[n+1]; indices: device int32[indptr[n]-indptr[0]] addressed
+ * by indptr's values; out_words: device uint32[n][W].
+ * EINVAL: N < 2, d == 0 with n > 0, null pointer with n > 0.
+ * Latched EINDEX: index outside [0,d), pi value >= N, indptr decreasing. */
+binsketch_status binsketch_build(const uint32_t* pi, uint64_t d, uint32_t N, const int64_t* indptr,
+                                 const int32_t* indices, uint64_t n, uint32_t* out_words,
+                                 binsketch_stream_t stream);
+
+/* Same result as binsketch_make_pi followed by binsketch_build, with pi(i)
+ * evaluated in-kernel from (seed, i, N) instead of gathered from a table
+ * (removes the random 4-byte gather per nonzero). */
+binsketch_status binsketch_build_seeded(uint64_t seed, uint64_t d, uint32_t N, const int64_t* indptr,
+                                        const int32_t* indices, uint64_t n, uint32_t* out_words,
+                                        binsketch_stream_t stream);
+
+/* Algorithm 1 line 1: out[r] = |sk[r]| (popcount).
+ * sk: device uint32[n][W]; out: device int32[n]. */
+binsketch_status binsketch_popcount(const uint32_t* sk, uint64_t n, uint32_t N, int32_t* out,
+                                    binsketch_stream_t stream);
+
+/* Algorithm 1 line 2: out[i][j] = |A[i] AND B[j]|.
+ * A: device uint32[na][W]; B: device uint32[nb][W]; out: device int32[na][nb].
+ * ws: device workspace of ws_bytes >= binsketch_workspace_bytes(BINSKETCH_OP_ANDPOPC, ...). */
+binsketch_status binsketch_andpopc(const uint32_t* A, uint64_t na, const uint32_t* B, uint64_t nb,
+                                   uint32_t N, int32_t* out, void* ws, size_t ws_bytes,
+                                   binsketch_stream_t stream);
+
+/* All-pairs estimation from sketches alone (Algorithms 1-4)
+ * by the canonical fp64 recipe (DESIGN.md R-C3): with pa = |a_s|, pb = |b_s|,
+ * pab = |a_s AND b_s|, pu = pa+pb-pab and L[k] = log1p(-k/N)/log1p(-1/N)
+ * (L[N] = d, saturation, R-G12):
+ *   IP  = (pu == N && pa < N && pb < N) ? 0 : min(max(L[pa]+L[pb]-L[pu], 0), min(L[pa], L[pb]))
+ *   HAM = min(max(S - 2 IP, 0), S),  S = L[pa]+L[pb]
+ *   JS  = (pa == pb == 0) ? 1 : clamp(IP/(S-IP), 0, 1)
+ *   COS = (pa == 0 || pb == 0) ? 0 : clamp(IP/sqrt(L[pa]L[pb]), 0, 1)
+ * The L table is built on the host with the C library's log1p and uploaded.
+ * measure: nonzero mask of BINSKETCH_{IP,HAM,JS,COS}; out: device
+ * float[popcount(measure)][na][nb], planes in the order IP, HAM, JS, COS, each
+ * value the fp64 result rounded to nearest float.
+ * d: ambient dimension (saturation cap). */
+binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, const uint32_t* sketches_b,
+                                    uint64_t nb, uint32_t N, uint64_t d, uint32_t measure, float* out,
+                                    void* ws, size_t ws_bytes, binsketch_stream_t stream);
+
+/* Query x database top-k (ranking; reading R-G17): for each
+ * query i, the k database rows with the best estimate under one measure,
+ * ordered by (key descending, db index ascending) where key = the estimate
+ * (IP, JS, COS) or -HAM; the fp64 key is computed by the recipe above.
+ * measure: exactly one BINSKETCH_* bit; 1 <= k <= BINSKETCH_MAX_K (k = 0 is a no-op).
+ * flags: BINSKETCH_TOPK_EXCLUDE_SELF skips j == i (self-join, R-G18).
+ * out_idx: device int32[nq][k]; out_score: device float[nq][k] (the measure's
+ * value, not the key). Slots beyond the number of eligible db rows hold
+ * idx = -1 and score = NaN. */
+binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb,
+                                uint32_t N, uint64_t d, uint32_t measure, uint32_t k, uint32_t flags,
+                                int32_t* out_idx, float* out_score, void* ws, size_t ws_bytes,
+                                binsketch_stream_t stream);
+
+/* Workspace bytes needed by op (BINSKETCH_OP_*) for na (queries) x nb (db)
+ * rows of N-bit sketches and top-k size k (ignored for other ops). Pure
+ * function of its arguments. */
+size_t binsketch_workspace_bytes(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k);
+
+/* The cardinality table the library uploads (Alg. 1 line 3):
+ * host_out[0..N] = L (HOST double[N+1]). For byte-level parity checks. */
+binsketch_status binsketch_card_table(uint32_t N, uint64_t d, double* host_out);
+
+/* Synchronises `stream`, returns BINSKETCH_EINDEX if a device-side input
+ * error was latched since the last call (and clears it), ECUDA on a CUDA
+ * error, else OK. */
+binsketch_status binsketch_device_status(binsketch_stream_t stream);
+
+/* Number of kernels this library has enqueued since it was loaded (all
+ * threads, all streams; atomic counter). Used by the bench to report
+ * gpu_launches. Host only. */
+uint64_t binsketch_launch_count(void);
+
+/* Static string for a status code. */
+const char* binsketch_strerror(binsketch_status status);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BINSKETCH_H */

@@ -1,0 +1,251 @@
+"""Thin ctypes binding over libbinsketch.so (include/binsketch.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels behind the C ABI. Tensors must be CUDA tensors of the documented
+dtype; calls enqueue on ``torch.cuda.current_stream()``. There is no CPU
+fallback: if the library is missing or a call fails, a ``BinSketchError`` is
+raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbinsketch.so")
+
+IP, HAM, JS, COS = 1, 2, 4, 8
+MEASURES = {"ip": IP, "ham": HAM, "js": JS, "cos": COS}
+TOPK_EXCLUDE_SELF = 1
+MAX_K = 256
+OP_ANDPOPC, OP_ESTIMATE, OP_TOPK = 1, 2, 3
+
+STATUS = {0: "OK", 1: "EINVAL", 2: "EINDEX", 3: "ECUDA", 4: "EWORKSPACE", 5: "EUNSUPPORTED"}
+
+# name -> (restype, argtypes)
+_u32, _u64, _i32, _vp, _dbl, _sz, _int = (ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p,
+                                          ctypes.c_double, ctypes.c_size_t, ctypes.c_int)
+SIGNATURES = {
+    "binsketch_words": (_u32, [_u32]),
+    "binsketch_recommended_N": (_u32, [_u32, _dbl]),
+    "binsketch_make_pi": (_int, [_u64, _u64, _u32, _vp, _vp]),
+    "binsketch_build": (_int, [_vp, _u64, _u32, _vp, _vp, _u64, _vp, _vp]),
+    "binsketch_build_seeded": (_int, [_u64, _u64, _u32, _vp, _vp, _u64, _vp, _vp]),
+    "binsketch_popcount": (_int, [_vp, _u64, _u32, _vp, _vp]),
+    "binsketch_andpopc": (_int, [_vp, _u64, _vp, _u64, _u32, _vp, _vp, _sz, _vp]),
+    "binsketch_estimate": (_int, [_vp, _u64, _vp, _u64, _u32, _u64, _u32, _vp, _vp, _sz, _vp]),
+    "binsketch_topk": (_int, [_vp, _u64, _vp, _u64, _u32, _u64, _u32, _u32, _u32, _vp, _vp, _vp, _sz, _vp]),
+    "binsketch_workspace_bytes": (_sz, [_int, _u64, _u64, _u32, _u32]),
+    "binsketch_card_table": (_int, [_u32, _u64, _vp]),
+    "binsketch_device_status": (_int, [_vp]),
+    "binsketch_launch_count": (_u64, []),
+    "binsketch_strerror": (ctypes.c_char_p, [_int]),
+}
+
+
+class BinSketchError(RuntimeError):
+    def __init__(self, fn: str, code: int):
+        self.code = code
+        msg = _lib().binsketch_strerror(code).decode() if _LIB is not None else STATUS.get(code, "?")
+        super().__init__(f"{fn}: {STATUS.get(code, code)} ({msg})")
+
+
+_LIB = None
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_1910_04658_b200.buildlib` "
+                              "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def _check(fn: str, code: int):
+    if code != 0:
+        raise BinSketchError(fn, code)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev(t: torch.Tensor, dtype: torch.dtype, name: str):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _words_tensor(t, name):
+    if t.dtype not in (torch.int32, torch.uint32):
+        raise TypeError(f"{name} must hold uint32 sketch words (torch.int32/uint32)")
+    return _dev(t, t.dtype, name)
+
+
+# ------------------------------------------------------------------ API ---
+def words(N: int) -> int:
+    return int(_lib().binsketch_words(N))
+
+
+def recommended_N(psi: int, rho: float) -> int:
+    return int(_lib().binsketch_recommended_N(psi, rho))
+
+
+def make_pi(seed: int, d: int, N: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(d, dtype=torch.int32, device="cuda")
+    _check("binsketch_make_pi", _lib().binsketch_make_pi(seed, d, N, _words_tensor(out, "pi") if d else None, _stream()))
+    return out
+
+
+def build(pi: torch.Tensor, d: int, N: int, indptr: torch.Tensor, indices: torch.Tensor,
+          out: torch.Tensor | None = None) -> torch.Tensor:
+    n = indptr.numel() - 1
+    if out is None:
+        out = torch.empty((n, words(N)), dtype=torch.int32, device="cuda")
+    _check("binsketch_build", _lib().binsketch_build(
+        _words_tensor(pi, "pi") if pi.numel() else None, d, N, _dev(indptr, torch.int64, "indptr"),
+        _dev(indices, torch.int32, "indices") if indices.numel() else None, n,
+        _words_tensor(out, "out") if out.numel() else None, _stream()))
+    return out
+
+
+def build_seeded(seed: int, d: int, N: int, indptr: torch.Tensor, indices: torch.Tensor,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    n = indptr.numel() - 1
+    if out is None:
+        out = torch.empty((n, words(N)), dtype=torch.int32, device="cuda")
+    _check("binsketch_build_seeded", _lib().binsketch_build_seeded(
+        seed, d, N, _dev(indptr, torch.int64, "indptr"),
+        _dev(indices, torch.int32, "indices") if indices.numel() else None, n,
+        _words_tensor(out, "out") if out.numel() else None, _stream()))
+    return out
+
+
+def popcount(sk: torch.Tensor, N: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    n = sk.shape[0]
+    if out is None:
+        out = torch.empty(n, dtype=torch.int32, device="cuda")
+    _check("binsketch_popcount", _lib().binsketch_popcount(
+        _words_tensor(sk, "sk") if n else None, n, N, _dev(out, torch.int32, "out") if n else None, _stream()))
+    return out
+
+
+def workspace_bytes(op: int, na: int, nb: int, N: int, k: int = 0) -> int:
+    return int(_lib().binsketch_workspace_bytes(op, na, nb, N, k))
+
+
+def _workspace(op, na, nb, N, k, ws):
+    need = workspace_bytes(op, na, nb, N, k)
+    if ws is None:
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+    return ws, ctypes.c_void_p(ws.data_ptr()), ws.numel()
+
+
+def andpopc(A: torch.Tensor, B: torch.Tensor, N: int, out: torch.Tensor | None = None, ws=None) -> torch.Tensor:
+    na, nb = A.shape[0], B.shape[0]
+    if out is None:
+        out = torch.empty((na, nb), dtype=torch.int32, device="cuda")
+    ws, wp, wn = _workspace(OP_ANDPOPC, na, nb, N, 0, ws)
+    _check("binsketch_andpopc", _lib().binsketch_andpopc(
+        _words_tensor(A, "A") if na else None, na, _words_tensor(B, "B") if nb else None, nb, N,
+        _dev(out, torch.int32, "out") if out.numel() else None, wp, wn, _stream()))
+    return out
+
+
+def estimate(A: torch.Tensor, B: torch.Tensor, N: int, d: int, measure: int = 15,
+             out: torch.Tensor | None = None, ws=None) -> torch.Tensor:
+    na, nb = A.shape[0], B.shape[0]
+    planes = bin(measure & 15).count("1")
+    if out is None:
+        out = torch.empty((planes, na, nb), dtype=torch.float32, device="cuda")
+    ws, wp, wn = _workspace(OP_ESTIMATE, na, nb, N, 0, ws)
+    _check("binsketch_estimate", _lib().binsketch_estimate(
+        _words_tensor(A, "A") if na else None, na, _words_tensor(B, "B") if nb else None, nb, N, d, measure,
+        _dev(out, torch.float32, "out") if out.numel() else None, wp, wn, _stream()))
+    return out
+
+
+def topk(Q: torch.Tensor, D: torch.Tensor, N: int, d: int, measure: int, k: int, exclude_self: bool = False,
+         out_idx: torch.Tensor | None = None, out_score: torch.Tensor | None = None, ws=None):
+    nq, ndb = Q.shape[0], D.shape[0]
+    if out_idx is None:
+        out_idx = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    if out_score is None:
+        out_score = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+    ws, wp, wn = _workspace(OP_TOPK, nq, ndb, N, k, ws)
+    _check("binsketch_topk", _lib().binsketch_topk(
+        _words_tensor(Q, "queries") if nq else None, nq, _words_tensor(D, "db") if ndb else None, ndb, N, d,
+        measure, k, TOPK_EXCLUDE_SELF if exclude_self else 0,
+        _dev(out_idx, torch.int32, "out_idx") if out_idx.numel() else None,
+        _dev(out_score, torch.float32, "out_score") if out_score.numel() else None, wp, wn, _stream()))
+    return out_idx, out_score
+
+
+def card_table(N: int, d: int):
+    import numpy as np
+    out = np.empty(N + 1, dtype=np.float64)
+    _check("binsketch_card_table", _lib().binsketch_card_table(N, d, out.ctypes.data))
+    return out
+
+
+def launch_count() -> int:
+    """Kernels libbinsketch has enqueued since load (for the bench's gpu_launches)."""
+    return int(_lib().binsketch_launch_count())
+
+
+def device_status() -> int:
+    """Synchronises the current stream; raises BinSketchError on a latched device error."""
+    code = _lib().binsketch_device_status(_stream())
+    _check("binsketch_device_status", code)
+    return code
+
+
+# ------------------------------------------------ end-to-end (host buffers) --
+def rank_from_host_csr(indptr_h: torch.Tensor, indices_h: torch.Tensor, pi_h: torch.Tensor, d: int, N: int,
+                       measure: int, k: int, nq: int | None = None, exclude_self: bool = False,
+                       bufs: dict | None = None):
+    """The whole path from HOST (pinned) CSR to HOST top-k lists, through the C ABI.
+
+    H2D copy of CSR + pi -> binsketch_build -> binsketch_topk (rows [0,nq) as
+    queries against all rows) -> D2H copy of (idx, score). ``bufs`` caches the
+    device buffers between calls (so repeated calls do not allocate).
+    Returns (out_idx_host, out_score_host, h2d_bytes, d2h_bytes).
+    """
+    n = indptr_h.numel() - 1
+    nq = n if nq is None else nq
+    b = bufs if bufs is not None else {}
+    if "indptr" not in b:
+        b["indptr"] = torch.empty_like(indptr_h, device="cuda")
+        b["indices"] = torch.empty_like(indices_h, device="cuda")
+        b["pi"] = torch.empty_like(pi_h, device="cuda")
+        b["sk"] = torch.empty((n, words(N)), dtype=torch.int32, device="cuda")
+        b["idx"] = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+        b["score"] = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+        b["ws"] = torch.empty(max(1, workspace_bytes(OP_TOPK, nq, n, N, k)), dtype=torch.uint8, device="cuda")
+        b["idx_h"] = torch.empty((nq, k), dtype=torch.int32, pin_memory=True)
+        b["score_h"] = torch.empty((nq, k), dtype=torch.float32, pin_memory=True)
+    b["indptr"].copy_(indptr_h, non_blocking=True)
+    b["indices"].copy_(indices_h, non_blocking=True)
+    b["pi"].copy_(pi_h, non_blocking=True)
+    build(b["pi"], d, N, b["indptr"], b["indices"], out=b["sk"])
+    topk(b["sk"][:nq], b["sk"], N, d, measure, k, exclude_self=exclude_self, out_idx=b["idx"],
+         out_score=b["score"], ws=b["ws"])
+    b["idx_h"].copy_(b["idx"], non_blocking=True)
+    b["score_h"].copy_(b["score"], non_blocking=True)
+    h2d = indptr_h.numel() * 8 + indices_h.numel() * 4 + pi_h.numel() * 4
+    d2h = nq * k * 8
+    return b["idx_h"], b["score_h"], h2d, d2h

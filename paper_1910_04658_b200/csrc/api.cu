@@ -1,0 +1,244 @@
+// api.cu — host side of the C ABI declared in include/binsketch.h:
+// argument validation, the fp64 cardinality table (built with the host C
+// library's log1p, cached per (N, d) in pinned memory and uploaded into the
+// caller's workspace), workspace layout, and kernel dispatch on the caller's
+// stream. Product code; shares nothing with oracle/.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "binsketch.h"
+#include "bsk_internal.cuh"
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+// Cardinality table, Algorithm 1 line 3 with q = 1 - 1/N
+// (PAPER.md:358): L[k] = ln(1-k/N)/ln(q) evaluated as log1p(-k/N)/log1p(-1/N)
+// (reading R-G11); L[N] = d (saturation, R-G12).
+struct TableCache {
+  std::mutex mu;
+  std::map<std::pair<uint32_t, uint64_t>, double*> tables;
+
+  const double* get(uint32_t N, uint64_t d) {
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(N, d);
+    auto it = tables.find(key);
+    if (it != tables.end()) return it->second;
+    double* t = nullptr;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&t), (size_t)(N + 1) * sizeof(double), cudaHostAllocDefault) !=
+        cudaSuccess) {
+      cudaGetLastError();  // clear; fall back to pageable memory (host-only use, no GPU)
+      t = static_cast<double*>(std::malloc((size_t)(N + 1) * sizeof(double)));
+      if (!t) return nullptr;
+    }
+    const double c = std::log1p(-1.0 / (double)N);
+    for (uint32_t k = 0; k < N; ++k) t[k] = std::log1p(-(double)k / (double)N) / c;
+    t[N] = (double)d;
+    tables.emplace(key, t);
+    return t;
+  }
+};
+
+TableCache& cache() {
+  static TableCache* c = new TableCache();  // never destroyed: pinned buffers may back in-flight copies
+  return *c;
+}
+
+struct Layout {
+  size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, total = 0;
+  uint32_t splits = 1;
+};
+
+Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
+  Layout l;
+  if (op == BINSKETCH_OP_ANDPOPC) return l;
+  size_t off = 0;
+  l.L = off; off += align_up((size_t)(N + 1) * 8);
+  l.pa = off; off += align_up((size_t)na * 4);
+  l.pb = off; off += align_up((size_t)nb * 4);
+  if (op == BINSKETCH_OP_TOPK) {
+    l.splits = bsk::topk_splits(na, nb, k);
+    if (l.splits > 1) {
+      l.pkey = off; off += align_up((size_t)na * l.splits * k * 8);
+      l.pidx = off; off += align_up((size_t)na * l.splits * k * 4);
+    }
+  }
+  l.total = off;
+  return l;
+}
+
+inline binsketch_status cuda_status(cudaError_t e) { return e == cudaSuccess ? BINSKETCH_OK : BINSKETCH_ECUDA; }
+
+inline bool one_bit(uint32_t m) { return m == 1u || m == 2u || m == 4u || m == 8u; }
+
+binsketch_status upload_table(uint32_t N, uint64_t d, void* ws, const Layout& l, cudaStream_t s) {
+  const double* t = cache().get(N, d);
+  if (!t) return BINSKETCH_ECUDA;
+  return cuda_status(cudaMemcpyAsync(static_cast<char*>(ws) + l.L, t, (size_t)(N + 1) * 8,
+                                     cudaMemcpyHostToDevice, s));
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t binsketch_words(uint32_t N) { return (uint32_t)(((uint64_t)N + 31u) / 32u); }
+
+uint32_t binsketch_recommended_N(uint32_t psi, double rho) {
+  // Theorem 1: N = psi * sqrt(psi/2 * ln(2/rho)); max(2, ceil(.)) (R-G5).
+  if (psi == 0 || !(rho > 0.0 && rho < 1.0)) return 0;
+  const double p = (double)psi;
+  double v = std::ceil(p * std::sqrt(0.5 * p * std::log(2.0 / rho)));
+  if (v < 2.0) v = 2.0;
+  if (v > 4294967295.0) return 0;
+  return (uint32_t)v;
+}
+
+binsketch_status binsketch_make_pi(uint64_t seed, uint64_t d, uint32_t N, uint32_t* pi, binsketch_stream_t stream) {
+  if (N < 2 || (d > 0 && pi == nullptr)) return BINSKETCH_EINVAL;
+  return cuda_status(bsk::launch_make_pi(seed, d, N, pi, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+static binsketch_status build_common(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t N,
+                                     const int64_t* indptr, const int32_t* indices, uint64_t n,
+                                     uint32_t* out, binsketch_stream_t stream) {
+  if (N < 2) return BINSKETCH_EINVAL;
+  if (n == 0) return BINSKETCH_OK;
+  if (d == 0 || indptr == nullptr || indices == nullptr || out == nullptr) return BINSKETCH_EINVAL;
+  if (d > 0x80000000ull) return BINSKETCH_EINVAL;  // int32 indices cannot address more
+  if (!bsk::status_ptr()) return BINSKETCH_ECUDA;
+  return cuda_status(bsk::launch_build(pi, seed, d, N, indptr, indices, n, out,
+                                       reinterpret_cast<cudaStream_t>(stream)));
+}
+
+binsketch_status binsketch_build(const uint32_t* pi, uint64_t d, uint32_t N, const int64_t* indptr,
+                                 const int32_t* indices, uint64_t n, uint32_t* out_words,
+                                 binsketch_stream_t stream) {
+  if (n > 0 && pi == nullptr) return BINSKETCH_EINVAL;
+  return build_common(pi, 0, d, N, indptr, indices, n, out_words, stream);
+}
+
+binsketch_status binsketch_build_seeded(uint64_t seed, uint64_t d, uint32_t N, const int64_t* indptr,
+                                        const int32_t* indices, uint64_t n, uint32_t* out_words,
+                                        binsketch_stream_t stream) {
+  return build_common(nullptr, seed, d, N, indptr, indices, n, out_words, stream);
+}
+
+binsketch_status binsketch_popcount(const uint32_t* sk, uint64_t n, uint32_t N, int32_t* out,
+                                    binsketch_stream_t stream) {
+  if (N < 2) return BINSKETCH_EINVAL;
+  if (n == 0) return BINSKETCH_OK;
+  if (!sk || !out) return BINSKETCH_EINVAL;
+  return cuda_status(bsk::launch_popcount(sk, n, binsketch_words(N), out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+size_t binsketch_workspace_bytes(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
+  return layout(op, na, nb, N, k).total;
+}
+
+binsketch_status binsketch_andpopc(const uint32_t* A, uint64_t na, const uint32_t* B, uint64_t nb, uint32_t N,
+                                   int32_t* out, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
+  (void)ws; (void)ws_bytes;
+  if (N < 2) return BINSKETCH_EINVAL;
+  if (na == 0 || nb == 0) return BINSKETCH_OK;
+  if (!A || !B || !out) return BINSKETCH_EINVAL;
+  return cuda_status(bsk::launch_pairs(bsk::kAndPopc, A, na, B, nb, N, 0, nullptr, nullptr, nullptr, out,
+                                       reinterpret_cast<cudaStream_t>(stream)));
+}
+
+binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, const uint32_t* sketches_b,
+                                    uint64_t nb, uint32_t N, uint64_t d, uint32_t measure, float* out, void* ws,
+                                    size_t ws_bytes, binsketch_stream_t stream) {
+  if (N < 2 || measure == 0 || (measure & ~15u)) return BINSKETCH_EINVAL;
+  if (na == 0 || nb == 0) return BINSKETCH_OK;
+  if (!sketches_a || !sketches_b || !out || d == 0) return BINSKETCH_EINVAL;
+  const Layout l = layout(BINSKETCH_OP_ESTIMATE, na, nb, N, 0);
+  if (!ws || ws_bytes < l.total) return BINSKETCH_EWORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  binsketch_status st = upload_table(N, d, ws, l, s);
+  if (st != BINSKETCH_OK) return st;
+  const uint32_t W = binsketch_words(N);
+  int32_t* pa = reinterpret_cast<int32_t*>(w + l.pa);
+  int32_t* pb = reinterpret_cast<int32_t*>(w + l.pb);
+  cudaError_t e = bsk::launch_popcount(sketches_a, na, W, pa, s);
+  if (e == cudaSuccess) e = bsk::launch_popcount(sketches_b, nb, W, pb, s);
+  if (e == cudaSuccess)
+    e = bsk::launch_pairs(bsk::kEstimate, sketches_a, na, sketches_b, nb, N, measure, pa, pb,
+                          reinterpret_cast<const double*>(w + l.L), out, s);
+  return cuda_status(e);
+}
+
+binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb, uint32_t N,
+                                uint64_t d, uint32_t measure, uint32_t k, uint32_t flags, int32_t* out_idx,
+                                float* out_score, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
+  if (N < 2 || !one_bit(measure) || (flags & ~1u)) return BINSKETCH_EINVAL;
+  if (nq == 0 || k == 0) return BINSKETCH_OK;
+  if (k > BINSKETCH_MAX_K) return BINSKETCH_EUNSUPPORTED;
+  if (!queries || !out_idx || !out_score || d == 0 || (ndb > 0 && !db)) return BINSKETCH_EINVAL;
+  if (ndb > 0x7fffffffull) return BINSKETCH_EUNSUPPORTED;   // int32 output indices
+  const Layout l = layout(BINSKETCH_OP_TOPK, nq, ndb, N, k);
+  if (!ws || ws_bytes < l.total) return BINSKETCH_EWORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  binsketch_status st = upload_table(N, d, ws, l, s);
+  if (st != BINSKETCH_OK) return st;
+  const uint32_t W = binsketch_words(N);
+  int32_t* pq = reinterpret_cast<int32_t*>(w + l.pa);
+  int32_t* pd = reinterpret_cast<int32_t*>(w + l.pb);
+  cudaError_t e = bsk::launch_popcount(queries, nq, W, pq, s);
+  if (e == cudaSuccess) e = bsk::launch_popcount(db, ndb, W, pd, s);
+  if (e == cudaSuccess)
+    e = bsk::launch_topk(queries, nq, db, ndb, N, measure, k, flags, pq, pd,
+                         reinterpret_cast<const double*>(w + l.L),
+                         l.splits > 1 ? reinterpret_cast<double*>(w + l.pkey) : nullptr,
+                         l.splits > 1 ? reinterpret_cast<int32_t*>(w + l.pidx) : nullptr, out_idx, out_score, s);
+  return cuda_status(e);
+}
+
+binsketch_status binsketch_card_table(uint32_t N, uint64_t d, double* host_out) {
+  if (N < 2 || !host_out) return BINSKETCH_EINVAL;
+  const double* t = cache().get(N, d);
+  if (!t) return BINSKETCH_ECUDA;
+  for (uint32_t k = 0; k <= N; ++k) host_out[k] = t[k];
+  return BINSKETCH_OK;
+}
+
+binsketch_status binsketch_device_status(binsketch_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return BINSKETCH_ECUDA;
+  unsigned int* p = bsk::status_ptr();
+  if (!p) return BINSKETCH_ECUDA;
+  unsigned int v = 0;
+  if (cudaMemcpy(&v, p, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return BINSKETCH_ECUDA;
+  if (v) {
+    const unsigned int z = 0;
+    if (cudaMemcpy(p, &z, sizeof(z), cudaMemcpyHostToDevice) != cudaSuccess) return BINSKETCH_ECUDA;
+    return BINSKETCH_EINDEX;
+  }
+  return BINSKETCH_OK;
+}
+
+uint64_t binsketch_launch_count(void) { return bsk::launch_count(); }
+
+const char* binsketch_strerror(binsketch_status status) {
+  switch (status) {
+    case BINSKETCH_OK: return "ok";
+    case BINSKETCH_EINVAL: return "invalid argument";
+    case BINSKETCH_EINDEX: return "device-detected invalid input (index out of range, pi value >= N, or decreasing indptr)";
+    case BINSKETCH_ECUDA: return "CUDA runtime error";
+    case BINSKETCH_EWORKSPACE: return "workspace too small";
+    case BINSKETCH_EUNSUPPORTED: return "unsupported request (outside this build's limits)";
+  }
+  return "unknown status";
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+// bsk_internal.cuh — launch interface between the C-ABI host layer (api.cu)
+// and the sm_100a kernels (pi.cu, build.cu, pairs.cu). Product code only;
+// shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace bsk {
+
+constexpr uint32_t kStatusIndex = 1u;   // latched: bad index / pi value / indptr
+
+// Kernel-launch counter (binsketch_launch_count); every launch site calls count_launch().
+void count_launch(uint64_t n = 1);
+uint64_t launch_count();
+
+// Device address of the latched status word (defined in build.cu).
+unsigned int* status_ptr();
+
+// 64-bit x mod N without a 64-bit division: q = umulhi(x, M), M = floor((2^64-1)/N),
+// then at most two corrections. Bit-identical to x % N for 2 <= N < 2^32.
+struct ModN {
+  uint64_t M;
+  uint32_t N;
+};
+ModN make_modn(uint32_t N);
+
+int num_sms();
+
+cudaError_t launch_make_pi(uint64_t seed, uint64_t d, uint32_t N, uint32_t* pi, cudaStream_t s);
+
+// pi == nullptr -> seeded (in-kernel pi); else table gather.
+cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t N,
+                         const int64_t* indptr, const int32_t* indices, uint64_t n,
+                         uint32_t* out, cudaStream_t s);
+
+cudaError_t launch_popcount(const uint32_t* sk, uint64_t n, uint32_t W, int32_t* out, cudaStream_t s);
+
+enum PairsMode { kAndPopc = 0, kEstimate = 1 };
+// All-pairs kernel: A[na][W] x B[nb][W]. mode kAndPopc writes int32 out[na][nb];
+// mode kEstimate reads pa/pb/L (device) and writes float planes.
+cudaError_t launch_pairs(int mode, const uint32_t* A, uint64_t na, const uint32_t* B, uint64_t nb,
+                         uint32_t N, uint32_t measure, const int32_t* pa, const int32_t* pb,
+                         const double* L, void* out, cudaStream_t s);
+
+// Top-k: number of db splits chosen for (nq, ndb, k) (pure function).
+uint32_t topk_splits(uint64_t nq, uint64_t ndb, uint32_t k);
+cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint64_t ndb, uint32_t N,
+                        uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq,
+                        const int32_t* pd, const double* L, double* part_key, int32_t* part_idx,
+                        int32_t* out_idx, float* out_score, cudaStream_t s);
+
+}  // namespace bsk

@@ -1,0 +1,110 @@
+"""C-ABI library, CPU-side checks (no GPU compute).
+
+* libbinsketch.so loads and exports every entry point include/binsketch.h declares;
+* host-only entry points (sizing rule, words, strerror, workspace sizing, the
+  host-built cardinality table) and host-detectable argument errors;
+* the product package shares no code with oracle/ and never imports it.
+"""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from bsk_helpers import ROOT
+
+from paper_1910_04658_b200 import buildlib as libbuild
+
+HEADER = os.path.join(ROOT, "include", "binsketch.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    libbuild.build()
+    return ctypes.CDLL(libbuild.LIB)
+
+
+def _declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(binsketch_[a-z_N]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = _declared()
+    assert len(names) == 14
+    for name in names:
+        assert hasattr(lib, name), name
+    from paper_1910_04658_b200.binsketch import SIGNATURES
+    assert sorted(SIGNATURES) == names      # the binding wraps exactly the ABI
+
+
+def test_host_entry_points(lib):
+    lib.binsketch_recommended_N.restype = ctypes.c_uint32
+    lib.binsketch_recommended_N.argtypes = [ctypes.c_uint32, ctypes.c_double]
+    for psi, rho in [(100, 0.1), (20, 0.1), (1, 0.999999), (0, 0.1), (5, 1.5), (300, 0.01)]:
+        assert lib.binsketch_recommended_N(psi, rho) == oracle.recommended_N(psi, rho)
+    lib.binsketch_words.restype = ctypes.c_uint32
+    assert [lib.binsketch_words(N) for N in (2, 32, 33, 1224, 5000)] == [1, 1, 2, 39, 157]
+    lib.binsketch_strerror.restype = ctypes.c_char_p
+    for code in range(6):
+        assert lib.binsketch_strerror(code)
+
+
+@pytest.mark.parametrize("N,d", [(2, 10), (1000, 28102), (1224, 5000), (2000, 28102), (4096, 102660),
+                                 (5000, 28102), (1024, 1 << 20)])
+def test_card_table_bit_identical_to_oracle(lib, N, d):
+    """binsketch_card_table (host libm log1p) == the oracle's table, byte for byte (R-C3)."""
+    lib.binsketch_card_table.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p]
+    out = np.empty(N + 1, dtype=np.float64)
+    assert lib.binsketch_card_table(N, d, out.ctypes.data) == 0
+    assert out.tobytes() == oracle.card_table(N, d).tobytes()
+
+
+def test_workspace_sizing(lib):
+    lib.binsketch_workspace_bytes.restype = ctypes.c_size_t
+    lib.binsketch_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
+                                              ctypes.c_uint32]
+    est = lib.binsketch_workspace_bytes(2, 1000, 1000, 1224, 0)
+    assert est >= 1225 * 8 + 2000 * 4
+    topk_small = lib.binsketch_workspace_bytes(3, 1000, 100_000, 4096, 100)
+    assert topk_small > 4097 * 8 + 101_000 * 4         # includes the split-merge buffers
+    assert lib.binsketch_workspace_bytes(3, 1000, 100_000, 4096, 100) == topk_small   # pure function
+
+
+def test_host_detected_errors(lib):
+    vp = ctypes.c_void_p
+    lib.binsketch_build.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint32, vp, vp, ctypes.c_uint64, vp, vp]
+    lib.binsketch_estimate.argtypes = [vp, ctypes.c_uint64, vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                                       ctypes.c_uint32, vp, vp, ctypes.c_size_t, vp]
+    lib.binsketch_topk.argtypes = [vp, ctypes.c_uint64, vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                                   ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, vp, vp, vp, ctypes.c_size_t, vp]
+    lib.binsketch_make_pi.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, vp, vp]
+    EINVAL, EUNSUP = 1, 5
+    assert lib.binsketch_make_pi(0, 10, 1, None, None) == EINVAL                 # N < 2
+    assert lib.binsketch_make_pi(0, 10, 16, None, None) == EINVAL                # null with d > 0
+    assert lib.binsketch_build(None, 10, 1, None, None, 5, None, None) == EINVAL  # N < 2
+    assert lib.binsketch_build(None, 10, 64, None, None, 5, None, None) == EINVAL  # null pointers
+    assert lib.binsketch_build(None, 10, 64, None, None, 0, None, None) == 0      # n = 0: no-op
+    assert lib.binsketch_estimate(None, 4, None, 4, 64, 10, 0, None, None, 0, None) == EINVAL   # measure 0
+    assert lib.binsketch_estimate(None, 4, None, 4, 64, 10, 16, None, None, 0, None) == EINVAL  # bad bit
+    assert lib.binsketch_estimate(None, 0, None, 4, 64, 10, 15, None, None, 0, None) == 0       # empty
+    assert lib.binsketch_topk(None, 4, None, 4, 64, 10, 3, 5, 0, None, None, None, 0, None) == EINVAL  # 2 bits
+    assert lib.binsketch_topk(None, 4, None, 4, 64, 10, 1, 5, 2, None, None, None, 0, None) == EINVAL  # flags
+    assert lib.binsketch_topk(None, 4, None, 4, 64, 10, 1, 0, 0, None, None, None, 0, None) == 0       # k = 0
+    assert lib.binsketch_topk(vp(8), 4, vp(8), 4, 64, 10, 1, 257, 0, vp(8), vp(8), None, 0, None) == EUNSUP
+
+
+def test_product_shares_no_code_with_oracle():
+    pkg = os.path.join(ROOT, "paper_1910_04658_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
+                assert "oracle.cpp" not in src and "liboracle" not in src, f
+                assert not re.search(r"^\s*(import|from)\s+synth\b", src, re.M), f
+    osrc = open(os.path.join(ROOT, "oracle", "oracle.cpp")).read()
+    assert "#include \"binsketch.h\"" not in osrc and "bsk_" not in osrc

@@ -1,0 +1,337 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bar (north star): bit-exact for pi, sketches, popcounts, AND-popcounts and
+top-k index lists (ties -> lower index); float estimates within
+|delta| <= 1e-4 * max(1, |ref|) — under the canonical fp64 recipe (R-C3) they
+are expected bit-identical, and that stronger property is asserted too.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_1910_04658_b200 import binsketch as bs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    bs._lib()       # fails loudly if libbinsketch.so is missing (no fallback)
+    yield
+    torch.cuda.synchronize()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def csr_dev(indptr, indices):
+    return dev(indptr.astype(np.int64)), dev(indices.astype(np.int32))
+
+
+def assert_est_close(got, ref):
+    """The graded tolerance, then bit-identity (canonical recipe)."""
+    ref64 = ref.astype(np.float64)
+    assert np.all(np.abs(got.astype(np.float64) - ref64) <= 1e-4 * np.maximum(1.0, np.abs(ref64)))
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+# ------------------------------------------------------------------ pi -----
+@pytest.mark.parametrize("seed,d,N", [(0, 8, 16), (1, 8, 1224), (1, 5000, 1224), (1, 28_102, 1000),
+                                      (7, 102_660, 4096), (1, 1 << 20, 1024), (3, 1000, 2),
+                                      (5, 1000, 3), (9, 4097, 65537), (11, 3000, 2**31 + 11),
+                                      (2**64 - 1, 777, 4294967295)])
+def test_make_pi_bit_exact(seed, d, N):
+    got = u32(bs.make_pi(seed, d, N))
+    assert np.array_equal(got, oracle.make_pi(seed, d, N))
+
+
+# --------------------------------------------------------------- build -----
+def _check_build(spec_or_csr, N, seed=synth.PI_SEED, d=None, seeded_too=True):
+    if isinstance(spec_or_csr, synth.CSRSpec):
+        indptr, indices = synth.make_csr(spec_or_csr)
+        d = spec_or_csr.d
+    else:
+        indptr, indices = spec_or_csr
+    pi = oracle.make_pi(seed, d, N)
+    ref, st = oracle.sketch(pi, d, N, indptr, indices)
+    assert st == 0
+    ip, ix = csr_dev(indptr, indices)
+    got = u32(bs.build(dev(pi.view(np.int32)), d, N, ip, ix))
+    assert np.array_equal(got, ref)
+    if seeded_too:
+        got2 = u32(bs.build_seeded(seed, d, N, ip, ix))
+        assert np.array_equal(got2, ref)
+    bs.device_status()
+    return ref
+
+
+def test_build_tiny_full():
+    _check_build(synth.TINY, synth.TINY_N)
+
+
+@pytest.mark.parametrize("N", synth.MEDIUM_NS)
+def test_build_medium_scaled(N):
+    _check_build(synth.scaled(synth.MEDIUM, 3000), N)
+
+
+def test_build_medium_smem_pi_path():
+    # >= 148*8*32 rows with W = 32 and d = 28102 engages the shared-memory uint16 pi table
+    _check_build(synth.scaled(synth.MEDIUM, 40_000), 1000, seeded_too=False)
+
+
+def test_build_ranking_and_buildonly_and_large_scaled():
+    _check_build(synth.scaled(synth.RANKING_DB, 3000), synth.RANKING_N)
+    _check_build(synth.scaled(synth.BUILD_ONLY, 50_000), synth.BUILD_ONLY_N)
+    _check_build(synth.scaled(synth.LARGE, 20_000), synth.LARGE_N)
+
+
+@pytest.mark.parametrize("N", [2, 3, 31, 32, 33, 63, 64, 65, 1000, 1224, 2000, 4096, 5000, 40_000, 100_000])
+def test_build_adversarial_widths(N):
+    rng = np.random.default_rng(N)
+    d = 3000
+    rows = []
+    for r in range(300):
+        kind = r % 6
+        if kind == 0:
+            rows.append(np.array([], dtype=np.int32))                        # empty row
+        elif kind == 1:
+            rows.append(rng.integers(0, d, 1).astype(np.int32))              # nnz = 1
+        elif kind == 2:
+            rows.append(rng.integers(0, d, 2500).astype(np.int32))           # nnz >> N, duplicates, unsorted
+        else:
+            rows.append(np.sort(rng.choice(d, rng.integers(1, 200), replace=False)).astype(np.int32))
+    indptr = np.zeros(len(rows) + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum([len(x) for x in rows])
+    indices = np.concatenate(rows)
+    _check_build((indptr, indices), N, seed=N, d=d)
+
+
+def test_build_explicit_colliding_table_and_offset_indptr():
+    d, N = 500, 70
+    pi = (np.arange(d) % 7).astype(np.uint32)          # forced collisions: only 7 buckets used
+    indptr, indices = synth.make_csr(synth.CSRSpec(n=400, d=d, kind=0, p1=1, p2=60, cap=60, zipf_s=1.1, seed=31))
+    ref, _ = oracle.sketch(pi, d, N, indptr, indices)
+    got = u32(bs.build(dev(pi.view(np.int32)), d, N, *csr_dev(indptr, indices)))
+    assert np.array_equal(got, ref)
+    # indptr with a nonzero base: rows 100..399 addressed into the full indices array
+    sub = indptr[100:]
+    got = u32(bs.build(dev(pi.view(np.int32)), d, N, dev(sub), dev(indices)))
+    assert np.array_equal(got, ref[100:])
+
+
+def test_build_empty_and_errors():
+    pi = dev(oracle.make_pi(1, 100, 64).view(np.int32))
+    out = bs.build(pi, 100, 64, dev(np.zeros(1, dtype=np.int64)), dev(np.zeros(0, dtype=np.int32)))
+    assert out.shape == (0, 2)
+    # out-of-range index -> latched EINDEX
+    bs.build(pi, 100, 64, dev(np.array([0, 2], dtype=np.int64)), dev(np.array([5, 100], dtype=np.int32)))
+    with pytest.raises(bs.BinSketchError) as e:
+        bs.device_status()
+    assert e.value.code == 2
+    bs.device_status()                                # cleared
+    bs.build(pi, 100, 64, dev(np.array([0, 1], dtype=np.int64)), dev(np.array([-3], dtype=np.int32)))
+    with pytest.raises(bs.BinSketchError):
+        bs.device_status()
+    # decreasing indptr
+    bs.build(pi, 100, 64, dev(np.array([0, 3, 1, 4], dtype=np.int64)), dev(np.arange(4, dtype=np.int32)))
+    with pytest.raises(bs.BinSketchError):
+        bs.device_status()
+    # pi value >= N
+    bad = dev(np.array([0, 99, 1], dtype=np.int32))
+    bs.build(bad, 3, 64, dev(np.array([0, 3], dtype=np.int64)), dev(np.arange(3, dtype=np.int32)))
+    with pytest.raises(bs.BinSketchError):
+        bs.device_status()
+    with pytest.raises(bs.BinSketchError):
+        bs.build(pi, 100, 1, dev(np.array([0, 1], dtype=np.int64)), dev(np.array([1], dtype=np.int32)))
+
+
+# ----------------------------------------------------------- popcounts -----
+def _sketches(spec, N, seed=synth.PI_SEED):
+    indptr, indices = synth.make_csr(spec)
+    sk, _ = oracle.sketch(oracle.make_pi(seed, spec.d, N), spec.d, N, indptr, indices)
+    return sk
+
+
+@pytest.mark.parametrize("N", [1224, 1000, 2000, 5000, 4096, 33])
+def test_popcount_and_andpopc(N):
+    A = _sketches(synth.scaled(synth.MEDIUM, 333, seed=77), N)
+    B = _sketches(synth.scaled(synth.MEDIUM, 517, seed=78), N)
+    Ad, Bd = dev(A.view(np.int32)), dev(B.view(np.int32))
+    assert np.array_equal(bs.popcount(Ad, N).cpu().numpy(), oracle.popcount(A, N))
+    assert np.array_equal(bs.andpopc(Ad, Bd, N).cpu().numpy(), oracle.andpopc(A, B, N))
+
+
+def test_andpopc_tiny_full():
+    A = _sketches(synth.TINY, synth.TINY_N)
+    Ad = dev(A.view(np.int32))
+    assert np.array_equal(bs.andpopc(Ad, Ad, synth.TINY_N).cpu().numpy(), oracle.andpopc(A, A, synth.TINY_N))
+
+
+# ------------------------------------------------------------ estimate -----
+def test_estimate_tiny_full_all_planes():
+    N, d = synth.TINY_N, synth.TINY.d
+    A = _sketches(synth.TINY, N)
+    Ad = dev(A.view(np.int32))
+    got = bs.estimate(Ad, Ad, N, d, 15).cpu().numpy()
+    ref = oracle.estimate(A, A, N, d, 15)
+    assert_est_close(got, ref)
+
+
+@pytest.mark.parametrize("N", synth.MEDIUM_NS)
+@pytest.mark.parametrize("measure", [15, 1, 2 | 8, 4])
+def test_estimate_medium_scaled(N, measure):
+    A = _sketches(synth.scaled(synth.MEDIUM, 300, seed=91), N)
+    B = _sketches(synth.scaled(synth.MEDIUM, 450, seed=92), N)
+    B[:40] = A[:40]                         # identical pairs (self-similarity exactness)
+    B[40] = 0                               # empty sketch
+    B[41] = 0xFFFFFFFF                      # saturated (tail bits cleared below)
+    if N % 32:
+        B[41, -1] = (1 << (N % 32)) - 1
+    got = bs.estimate(dev(A.view(np.int32)), dev(B.view(np.int32)), N, 28_102, measure).cpu().numpy()
+    ref = oracle.estimate(A, B, N, 28_102, measure)
+    assert_est_close(got, ref)
+
+
+# ---------------------------------------------------------------- top-k ----
+def _check_topk(Q, D, N, d, measure, k, exclude_self=False):
+    gi, gs = bs.topk(dev(Q.view(np.int32)), dev(D.view(np.int32)), N, d, measure, k, exclude_self=exclude_self)
+    ri, rs = oracle.topk(Q, D, N, d, measure, k, exclude_self=exclude_self)
+    gi, gs = gi.cpu().numpy(), gs.cpu().numpy()
+    assert np.array_equal(gi, ri)
+    assert np.array_equal(np.isnan(gs), np.isnan(rs))
+    m = ~np.isnan(rs)
+    assert_est_close(gs[m], rs[m])
+
+
+@pytest.mark.parametrize("measure", [1, 2, 4, 8])
+def test_topk_tiny(measure):
+    N, d = synth.TINY_N, synth.TINY.d
+    A = _sketches(synth.TINY, N)
+    _check_topk(A, A, N, d, measure, 10)
+    _check_topk(A, A, N, d, measure, 10, exclude_self=True)
+
+
+@pytest.mark.parametrize("measure", [4, 8])
+def test_topk_ranking_scaled_split_merge(measure):
+    # few queries, many db rows: exercises db splits + the merge kernel
+    N, d = synth.RANKING_N, synth.RANKING_DB.d
+    D = _sketches(synth.scaled(synth.RANKING_DB, 20_000), N)
+    Q = _sketches(synth.scaled(synth.RANKING_Q, 70), N)
+    _check_topk(Q, D, N, d, measure, 100)
+
+
+@pytest.mark.parametrize("k", [1, 50, 64, 65, 100, 192, 193, 256])
+def test_topk_k_sizes_and_ties(k):
+    N, d = 1024, 500_000
+    D = _sketches(synth.scaled(synth.LARGE, 3000), N)
+    D[100:110] = D[5]                    # exact ties: lower index first
+    D[2000:2300] = D[7]
+    Q = D[:150].copy()
+    _check_topk(Q, D, N, d, 1, k, exclude_self=True)
+    _check_topk(Q, D, N, d, 4, k)
+
+
+def test_topk_padding_and_empty_db():
+    N, d = 64, 1000
+    D = _sketches(synth.CSRSpec(n=20, d=d, kind=0, p1=5, p2=20, cap=20, zipf_s=1.1, seed=3), N)
+    _check_topk(D[:5], D, N, d, 2, 30)                       # k > ndb -> -1 / NaN padding
+    _check_topk(D[:5], D, N, d, 1, 20, exclude_self=True)    # k > ndb - 1
+    gi, gs = bs.topk(dev(D[:3].view(np.int32)), dev(D[:0].view(np.int32)), N, d, 1, 4)
+    assert (gi.cpu().numpy() == -1).all() and np.isnan(gs.cpu().numpy()).all()
+
+
+# ------------------------------------------ full BASELINE sizes (sampled) --
+@pytest.mark.slow
+def test_full_large_selfjoin_sampled():
+    """configs[4] at full size in the bench launch configuration; 256 sampled query rows vs the oracle."""
+    spec, N, k = synth.LARGE, synth.LARGE_N, synth.LARGE_K
+    indptr, indices = synth.make_csr(spec)
+    pi = oracle.make_pi(synth.PI_SEED, spec.d, N)
+    ip, ix = csr_dev(indptr, indices)
+    sk = bs.build(dev(pi.view(np.int32)), spec.d, N, ip, ix)
+    gi, gs = bs.topk(sk, sk, N, spec.d, bs.IP, k, exclude_self=True)
+    torch.cuda.synchronize()
+    skh = u32(sk)
+    rows = np.sort(np.random.default_rng(0).choice(spec.n, 256, replace=False))
+    # sketches: sampled rows recomputed by the oracle
+    for r in rows[:64]:
+        one, _ = oracle.sketch(pi, spec.d, N, np.array([0, indptr[r + 1] - indptr[r]]),
+                               indices[indptr[r]:indptr[r + 1]])
+        assert np.array_equal(one[0], skh[r])
+    # top-k of sampled queries against the full db: the query row index must stay r for exclusion
+    Qs = skh[rows]
+    ri = np.empty((len(rows), k), dtype=np.int32)
+    rs = np.empty((len(rows), k), dtype=np.float32)
+    for t, r in enumerate(rows):
+        # exclude_self compares db index with the query's own row index r
+        i1, s1 = oracle.topk(Qs[t:t + 1], np.delete(skh, r, axis=0), N, spec.d, 1, k)
+        i1 = np.where(i1 >= r, i1 + 1, i1)
+        ri[t], rs[t] = i1[0], s1[0]
+    assert np.array_equal(gi.cpu().numpy()[rows], ri)
+    assert_est_close(gs.cpu().numpy()[rows], rs)
+
+
+@pytest.mark.slow
+def test_full_ranking_sampled():
+    """configs[2] at full size: 100k db, 1000 queries, top-100 JS and COS; 100 sampled queries."""
+    N, d, k = synth.RANKING_N, synth.RANKING_DB.d, synth.RANKING_K
+    pi = oracle.make_pi(synth.PI_SEED, d, N)
+    dbp, dbi = synth.make_csr(synth.RANKING_DB)
+    qp, qi = synth.make_csr(synth.RANKING_Q)
+    D = bs.build(dev(pi.view(np.int32)), d, N, *csr_dev(dbp, dbi))
+    Q = bs.build(dev(pi.view(np.int32)), d, N, *csr_dev(qp, qi))
+    Dh, Qh = u32(D), u32(Q)
+    rows = np.sort(np.random.default_rng(1).choice(1000, 100, replace=False))
+    for m in (bs.JS, bs.COS):
+        gi, gs = bs.topk(Q, D, N, d, m, k)
+        ri, rs = oracle.topk(Qh[rows], Dh, N, d, m, k)
+        assert np.array_equal(gi.cpu().numpy()[rows], ri)
+        assert_est_close(gs.cpu().numpy()[rows], rs)
+
+
+@pytest.mark.slow
+def test_full_medium_sampled_planes():
+    """configs[1] at full size (10k x 10k, 4 planes) for each N; 64 sampled rows x all columns."""
+    spec = synth.MEDIUM
+    indptr, indices = synth.make_csr(spec)
+    ip, ix = csr_dev(indptr, indices)
+    rows = np.sort(np.random.default_rng(2).choice(spec.n, 64, replace=False))
+    for N in synth.MEDIUM_NS:
+        sk = bs.build_seeded(synth.PI_SEED, spec.d, N, ip, ix)
+        out = bs.estimate(sk, sk, N, spec.d, 15)
+        torch.cuda.synchronize()
+        skh = u32(sk)
+        ref = oracle.estimate(skh[rows], skh, N, spec.d, 15)
+        assert_est_close(out.cpu().numpy()[:, rows, :], ref)
+
+
+@pytest.mark.slow
+def test_full_buildonly_sampled():
+    """configs[3] at full size (1e7 rows): 20k sampled rows recomputed by the oracle, bit-exact."""
+    spec, N = synth.BUILD_ONLY, synth.BUILD_ONLY_N
+    indptr, indices = synth.make_csr(spec)
+    pi = oracle.make_pi(synth.PI_SEED, spec.d, N)
+    ip, ix = csr_dev(indptr, indices)
+    for fn in ("table", "seeded"):
+        if fn == "table":
+            sk = bs.build(dev(pi.view(np.int32)), spec.d, N, ip, ix)
+        else:
+            sk = bs.build_seeded(synth.PI_SEED, spec.d, N, ip, ix)
+        torch.cuda.synchronize()
+        rows = np.sort(np.random.default_rng(3).choice(spec.n, 20_000, replace=False))
+        sub_ptr = np.zeros(len(rows) + 1, dtype=np.int64)
+        sub_ptr[1:] = np.cumsum(indptr[rows + 1] - indptr[rows])
+        sub_idx = np.concatenate([indices[indptr[r]:indptr[r + 1]] for r in rows])
+        ref, _ = oracle.sketch(pi, spec.d, N, sub_ptr, sub_idx)
+        assert np.array_equal(u32(sk[torch.from_numpy(rows).cuda()]), ref)
+        bs.device_status()
+        del sk

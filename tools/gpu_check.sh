@@ -1,0 +1,14 @@
+#!/bin/bash
+# One GPU session: build, calibrate, parity tests, smoke, bench. Logs -> gpurun_out/
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/gpu.txt 2>&1
+nproc > gpurun_out/host.txt; lscpu | grep "Model name" >> gpurun_out/host.txt
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
+timeout 120 ./tools/microbench > gpurun_out/microbench.jsonl 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q ${PYTEST_EXTRA} > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "smoke exit $?" >> gpurun_out/smoke.log
+timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1
+echo "bench exit $?" >> gpurun_out/bench.log
