@@ -72,79 +72,122 @@ cudaError_t launch_make_pi(uint64_t seed, uint64_t d, uint32_t N, uint32_t* pi, 
 }
 
 // ------------------------------------------------------------------ K1 ----
-enum PiMode { kPiGlobal = 0, kPiSmem16 = 1, kPiSmem32 = 2, kPiSeeded = 3 };
+enum PiMode { kPiGlobal = 0, kPiSmem16 = 1, kPiCache = 2, kPiSeeded = 3 };
 
-constexpr int kBuildThreads = 256;
-constexpr int kBuildWarps = kBuildThreads / 32;
-constexpr uint32_t kTileWords = 1024;     // RW * W <= 1024 words (4 KB) per warp
+constexpr uint32_t kTileWordsMax = 1024;     // RW * W <= 1024 words (4 KB) per warp
+constexpr uint32_t kCacheSlots = 32768;      // shared-memory pi cache: 32K x 4 B = 128 KB
+constexpr uint32_t kCacheEmpty = 0xFFFFFFFFu;
+
+// pi(idx) for the kernel's pi mode.
+//  kPiGlobal: read-only L1/L2 gather.   kPiSmem16: whole table in shared memory (uint16).
+//  kPiSeeded: splitmix64 evaluated in-kernel (no table).
+//  kPiCache:  direct-mapped software cache in shared memory, slot = idx mod 32K holding
+//             (idx >> 15) << 16 | pi(idx); a miss gathers from global and fills the slot.
+//             Zipf-skewed features make most lookups hits; every (tag, value) ever written
+//             is correct because pi is read-only, so races between lanes are benign.
+template <int MODE>
+__device__ __forceinline__ uint32_t pi_lookup(uint32_t idx, const uint32_t* __restrict__ pi, uint64_t seed,
+                                              const ModN& mn, unsigned char* smem_pi) {
+  if (MODE == kPiGlobal) return __ldg(pi + idx);
+  if (MODE == kPiSmem16) return reinterpret_cast<const uint16_t*>(smem_pi)[idx];
+  if (MODE == kPiSeeded) return pi_seeded(seed, idx, mn);
+  uint32_t* cache = reinterpret_cast<uint32_t*>(smem_pi);
+  const uint32_t slot = idx & (kCacheSlots - 1), tag = idx >> 15;
+  const uint32_t c = cache[slot];
+  if ((c >> 16) == tag) return c & 0xFFFFu;
+  const uint32_t j = __ldg(pi + idx);
+  if (j < 65536u) cache[slot] = (tag << 16) | j;
+  return j;
+}
 
 template <int MODE>
-__global__ void __launch_bounds__(kBuildThreads)
+__global__ void __launch_bounds__(1024)
 build_kernel(const uint32_t* __restrict__ pi, uint64_t seed, uint64_t d, ModN mn,
              const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, uint64_t n,
-             uint32_t* __restrict__ out, uint32_t W, uint32_t RW, unsigned int* status) {
+             uint32_t* __restrict__ out, uint32_t W, uint32_t RW, size_t pi_bytes, unsigned int* status) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
   const uint32_t N = mn.N;
 
-  size_t pi_bytes = 0;
-  if (MODE == kPiSmem16) pi_bytes = ((d * 2 + 15) / 16) * 16;
-  if (MODE == kPiSmem32) pi_bytes = ((d * 4 + 15) / 16) * 16;
   // per-warp: indptr slice (RW+1 int64), then the RW x W sketch tile (16-B aligned)
   const size_t ip_bytes = (((size_t)(RW + 1) * 8 + 15) / 16) * 16;
-  const size_t tile_bytes = (size_t)RW * W * 4;
-  unsigned char* wbase = smem + pi_bytes + (size_t)warp * (ip_bytes + ((tile_bytes + 15) / 16) * 16);
+  const size_t tile_bytes = (((size_t)RW * W * 4 + 15) / 16) * 16;
+  unsigned char* wbase = smem + pi_bytes + (size_t)warp * (ip_bytes + tile_bytes);
   int64_t* ip_s = reinterpret_cast<int64_t*>(wbase);
   uint32_t* tile = reinterpret_cast<uint32_t*>(wbase + ip_bytes);
 
   unsigned bad_bits = 0;
-  if (MODE == kPiSmem16 || MODE == kPiSmem32) {
+  if (MODE == kPiSmem16) {
     for (uint64_t i = threadIdx.x; i < d; i += blockDim.x) {
       uint32_t v = __ldg(pi + i);
       if (v >= N) { bad_bits = kStatusIndex; v = 0; }
-      if (MODE == kPiSmem16) reinterpret_cast<uint16_t*>(smem)[i] = (uint16_t)v;
-      else reinterpret_cast<uint32_t*>(smem)[i] = v;
+      reinterpret_cast<uint16_t*>(smem)[i] = (uint16_t)v;
     }
-    __syncthreads();
   }
+  if (MODE == kPiCache) {
+    for (uint32_t i = threadIdx.x; i < kCacheSlots; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = kCacheEmpty;
+  }
+  if (MODE == kPiSmem16 || MODE == kPiCache) __syncthreads();
 
+  const bool vec = (reinterpret_cast<uintptr_t>(indices) & 15u) == 0;
   const uint64_t ntiles = (n + RW - 1) / RW;
-  for (uint64_t t = (uint64_t)blockIdx.x * kBuildWarps + warp; t < ntiles;
-       t += (uint64_t)gridDim.x * kBuildWarps) {
+  for (uint64_t t = (uint64_t)blockIdx.x * nwarps + warp; t < ntiles; t += (uint64_t)gridDim.x * nwarps) {
     const uint64_t r0 = t * RW;
     const uint32_t rows = (uint32_t)((n - r0) < RW ? (n - r0) : RW);
     const uint32_t nw = rows * W;
     for (uint32_t i = lane; i <= rows; i += 32) ip_s[i] = __ldg(indptr + r0 + i);
-    if ((nw & 3u) == 0) {
-      uint4 z = make_uint4(0, 0, 0, 0);
-      for (uint32_t w = lane * 4; w < nw; w += 128) *reinterpret_cast<uint4*>(tile + w) = z;
-    } else {
-      for (uint32_t w = lane; w < nw; w += 32) tile[w] = 0u;
+    {
+      const uint4 z = make_uint4(0, 0, 0, 0);
+      for (uint32_t w = lane * 4; w < nw; w += 128) *reinterpret_cast<uint4*>(tile + w) = z;  // tile_bytes padded
     }
     __syncwarp();
-    bool mono = true;
-    for (uint32_t i = lane; i < rows; i += 32) mono &= ip_s[i + 1] >= ip_s[i];
-    if (__all_sync(0xffffffffu, mono)) {
-      const int64_t e1 = ip_s[rows];
+    bool ok = ip_s[0] >= 0;
+    for (uint32_t i = lane; i < rows; i += 32) ok &= ip_s[i + 1] >= ip_s[i];
+    if (__all_sync(0xffffffffu, ok)) {
+      const int64_t e0 = ip_s[0], e1 = ip_s[rows];
       uint32_t cr = 0;
-      for (int64_t e = ip_s[0] + lane; e < e1; e += 32) {
-        while (e >= ip_s[cr + 1]) ++cr;
-        const int32_t idx = __ldcs(indices + e);
-        if ((uint64_t)(uint32_t)idx >= d || idx < 0) { bad_bits = kStatusIndex; continue; }
-        uint32_t j;
-        if (MODE == kPiGlobal) j = __ldg(pi + idx);
-        else if (MODE == kPiSmem16) j = reinterpret_cast<const uint16_t*>(smem)[idx];
-        else if (MODE == kPiSmem32) j = reinterpret_cast<const uint32_t*>(smem)[idx];
-        else j = pi_seeded(seed, (uint64_t)idx, mn);
-        if (MODE == kPiGlobal && j >= N) { bad_bits = kStatusIndex; continue; }
-        atomicOr(tile + cr * W + (j >> 5), 1u << (j & 31u));
+      int64_t nxt = ip_s[1];
+      // Each lane handles 2 quads (8 consecutive-in-pairs elements) per iteration: quads at
+      // p and p + 128, with p = base + 4*lane + 256*it; 16-byte streaming loads when aligned.
+      const int64_t base = vec ? (e0 & ~(int64_t)3) : e0;
+      for (int64_t p = base + 4 * lane; p < e1; p += 256) {
+        int v[8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t q = p + 128 * h;
+          if (vec && q + 4 <= e1) {
+            const int4 t4 = __ldcs(reinterpret_cast<const int4*>(indices + q));
+            v[4 * h + 0] = t4.x; v[4 * h + 1] = t4.y; v[4 * h + 2] = t4.z; v[4 * h + 3] = t4.w;
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[4 * h + u] = (q + u >= e0 && q + u < e1) ? __ldcs(indices + q + u) : 0;
+          }
+        }
+        uint32_t j[8];
+        bool valid[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t e = p + 128 * (u >> 2) + (u & 3);
+          valid[u] = e >= e0 && e < e1;
+          if (valid[u] && (v[u] < 0 || (uint64_t)v[u] >= d)) { bad_bits = kStatusIndex; valid[u] = false; }
+          j[u] = valid[u] ? pi_lookup<MODE>((uint32_t)v[u], pi, seed, mn, smem) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (!valid[u]) continue;
+          if (MODE != kPiSeeded && MODE != kPiSmem16 && j[u] >= N) { bad_bits = kStatusIndex; continue; }
+          const int64_t e = p + 128 * (u >> 2) + (u & 3);
+          while (e >= nxt) { ++cr; nxt = ip_s[cr + 1]; }
+          atomicOr(tile + cr * W + (j[u] >> 5), 1u << (j[u] & 31u));
+        }
       }
     } else {
-      bad_bits = kStatusIndex;  // decreasing indptr: rows of this tile stay zero
+      bad_bits = kStatusIndex;  // decreasing / negative indptr: rows of this tile stay zero
     }
     __syncwarp();
     uint32_t* dst = out + r0 * W;
-    if ((nw & 3u) == 0 && ((r0 * W) & 3u) == 0) {
+    if ((nw & 3u) == 0 && ((r0 * W) & 3u) == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
       for (uint32_t w = lane * 4; w < nw; w += 128)
         __stcs(reinterpret_cast<uint4*>(dst + w), *reinterpret_cast<const uint4*>(tile + w));
     } else {
@@ -179,6 +222,17 @@ __global__ void build_wide_kernel(const uint32_t* __restrict__ pi, uint64_t seed
   if (bad) latch(status, bad);
 }
 
+// Largest RW (rows per warp tile, <= 32, RW*W <= kTileWordsMax) whose per-warp shared
+// memory fits `per_warp` bytes; 0 if even one row does not fit.
+static uint32_t pick_rw(uint32_t W, size_t per_warp) {
+  uint32_t rw = std::max<uint32_t>(1, std::min<uint32_t>(32, kTileWordsMax / W));
+  for (; rw >= 1; --rw) {
+    const size_t need = (((size_t)(rw + 1) * 8 + 15) / 16) * 16 + (((size_t)rw * W * 4 + 15) / 16) * 16;
+    if (need <= per_warp) return rw;
+  }
+  return 0;
+}
+
 cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t N,
                          const int64_t* indptr, const int32_t* indices, uint64_t n,
                          uint32_t* out, cudaStream_t s) {
@@ -190,51 +244,49 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
   int dev = 0, smem_optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t optin = (size_t)smem_optin;
 
-  uint32_t RW = std::max<uint32_t>(1, std::min<uint32_t>(32, kTileWords / W));
-  const size_t ip_bytes = (((size_t)(RW + 1) * 8 + 15) / 16) * 16;
-  const size_t tile_bytes = (((size_t)RW * W * 4 + 15) / 16) * 16;
-  const size_t per_cta = kBuildWarps * (ip_bytes + tile_bytes);
-  if (per_cta > (size_t)smem_optin) {
+  int mode = kPiGlobal, threads = 256;
+  size_t pi_bytes = 0;
+  const size_t smem16_bytes = ((d * 2 + 15) / 16) * 16;
+  if (pi == nullptr) {
+    mode = kPiSeeded;
+  } else if (N <= 65536 && smem16_bytes <= 96 * 1024) {
+    mode = kPiSmem16; threads = 1024; pi_bytes = smem16_bytes;
+  } else if (N <= 65536 && d < 0x80000000ull - 32768ull) {
+    mode = kPiCache; threads = 1024; pi_bytes = (size_t)kCacheSlots * 4;
+  }
+  uint32_t RW = pick_rw(W, (optin - pi_bytes) / (threads / 32));
+  if (RW == 0 && mode != kPiSeeded && mode != kPiGlobal) {   // wide sketches: drop the smem table
+    mode = kPiGlobal; threads = 256; pi_bytes = 0;
+    RW = pick_rw(W, optin / (threads / 32));
+  }
+  if (RW == 0 || (mode == kPiSeeded && RW == 0)) RW = pick_rw(W, optin / (threads / 32));
+  if (RW == 0) {
     cudaError_t e = cudaMemsetAsync(out, 0, n * (size_t)W * 4, s);
     if (e != cudaSuccess) return e;
     build_wide_kernel<<<sms * 8, 256, 0, s>>>(pi, seed, d, mn, pi == nullptr, indptr, indices, n, out, W, st);
     count_launch();
     return cudaGetLastError();
   }
+  const size_t per_warp = (((size_t)(RW + 1) * 8 + 15) / 16) * 16 + (((size_t)RW * W * 4 + 15) / 16) * 16;
+  const size_t smem = pi_bytes + per_warp * (threads / 32);
   const uint64_t ntiles = (n + RW - 1) / RW;
-  const uint64_t want_blocks = (ntiles + kBuildWarps - 1) / kBuildWarps;
-
-  int mode;
-  size_t pi_bytes = 0;
-  if (pi == nullptr) {
-    mode = kPiSeeded;
-  } else if (N <= 65536 && ((d * 2 + 15) / 16) * 16 + per_cta <= (size_t)smem_optin && d * 2 <= 160 * 1024 &&
-             want_blocks >= (uint64_t)sms) {
-    mode = kPiSmem16;
-    pi_bytes = ((d * 2 + 15) / 16) * 16;
-  } else {
-    mode = kPiGlobal;
-  }
-  const size_t smem = pi_bytes + per_cta;
-  uint64_t blocks;
-  if (mode == kPiSmem16) {
-    blocks = std::min<uint64_t>(want_blocks, (uint64_t)sms);  // persistent: table loaded once per CTA
-  } else {
-    int per_sm = std::max<int>(1, (int)std::min<size_t>(8, (size_t)(smem_optin) / std::max<size_t>(smem, 1)));
-    blocks = std::min<uint64_t>(want_blocks, (uint64_t)sms * per_sm);
-  }
+  const uint64_t want_blocks = (ntiles + (threads / 32) - 1) / (threads / 32);
+  const int per_sm = std::max<int>(1, std::min<int>(2048 / threads, (int)(optin / std::max<size_t>(smem, 1))));
+  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(want_blocks, (uint64_t)sms * per_sm));
   cudaError_t e = cudaSuccess;
 #define BSK_LAUNCH_BUILD(M)                                                                            \
   do {                                                                                                 \
     e = cudaFuncSetAttribute(build_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                                    \
-    build_kernel<M><<<(unsigned)blocks, kBuildThreads, smem, s>>>(pi, seed, d, mn, indptr, indices, n, \
-                                                                  out, W, RW, st);                    \
+    build_kernel<M><<<(unsigned)blocks, threads, smem, s>>>(pi, seed, d, mn, indptr, indices, n, out,  \
+                                                            W, RW, pi_bytes, st);                      \
     count_launch();                                                                                    \
   } while (0)
   switch (mode) {
     case kPiSmem16: BSK_LAUNCH_BUILD(kPiSmem16); break;
+    case kPiCache: BSK_LAUNCH_BUILD(kPiCache); break;
     case kPiSeeded: BSK_LAUNCH_BUILD(kPiSeeded); break;
     default: BSK_LAUNCH_BUILD(kPiGlobal); break;
   }
