@@ -17,6 +17,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 }
 
 __device__ __forceinline__ uint32_t mod_n(uint64_t x, const ModN& m) {
+  if (m.mask) return (uint32_t)x & m.mask;
   uint64_t q = __umul64hi(x, m.M);
   uint64_t r = x - q * (uint64_t)m.N;
   if (r >= m.N) r -= m.N;

@@ -22,6 +22,7 @@ unsigned int* status_ptr();
 struct ModN {
   uint64_t M;
   uint32_t N;
+  uint32_t mask;   // N-1 when N is a power of two (x mod N = x & mask), else 0
 };
 ModN make_modn(uint32_t N);
 

@@ -20,6 +20,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
+#include <cstring>
 #include <cstdint>
 
 #include "bsk_device.cuh"
@@ -46,6 +48,7 @@ ModN make_modn(uint32_t N) {
   ModN m;
   m.N = N;
   m.M = (N > 1) ? (~0ULL) / (uint64_t)N : 0ULL;
+  m.mask = (N > 1 && (N & (N - 1)) == 0) ? N - 1 : 0u;
   return m;
 }
 
@@ -78,28 +81,44 @@ constexpr uint32_t kTileWordsMax = 1024;     // RW * W <= 1024 words (4 KB) per 
 constexpr uint32_t kCacheSlots = 32768;      // shared-memory pi cache: 32K x 4 B = 128 KB
 constexpr uint32_t kCacheEmpty = 0xFFFFFFFFu;
 
-// pi(idx) for the kernel's pi mode.
+// 32-bit shared-memory accessors (keep shared addresses in one register; no generic
+// address conversion per access).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_or_shared(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// K1. Modes of obtaining pi(idx):
 //  kPiGlobal: read-only L1/L2 gather.   kPiSmem16: whole table in shared memory (uint16).
 //  kPiSeeded: splitmix64 evaluated in-kernel (no table).
 //  kPiCache:  direct-mapped software cache in shared memory, slot = idx mod 32K holding
 //             (idx >> 15) << 16 | pi(idx); a miss gathers from global and fills the slot.
 //             Zipf-skewed features make most lookups hits; every (tag, value) ever written
 //             is correct because pi is read-only, so races between lanes are benign.
-template <int MODE>
-__device__ __forceinline__ uint32_t pi_lookup(uint32_t idx, const uint32_t* __restrict__ pi, uint64_t seed,
-                                              const ModN& mn, unsigned char* smem_pi) {
-  if (MODE == kPiGlobal) return __ldg(pi + idx);
-  if (MODE == kPiSmem16) return reinterpret_cast<const uint16_t*>(smem_pi)[idx];
-  if (MODE == kPiSeeded) return pi_seeded(seed, idx, mn);
-  uint32_t* cache = reinterpret_cast<uint32_t*>(smem_pi);
-  const uint32_t slot = idx & (kCacheSlots - 1), tag = idx >> 15;
-  const uint32_t c = cache[slot];
-  if ((c >> 16) == tag) return c & 0xFFFFu;
-  const uint32_t j = __ldg(pi + idx);
-  if (j < 65536u) cache[slot] = (tag << 16) | j;
-  return j;
-}
-
+// Per lane and iteration, 8 nonzeros (two 16-B quads) are looked up branch-free (all
+// loads independent), then OR-ed into the warp's shared tile with RED.OR; the next two
+// quads are already in flight. Invalid indices / pi values are clamped (so no access
+// leaves its array) and latched as EINDEX.
 template <int MODE>
 __global__ void __launch_bounds__(1024)
 build_kernel(const uint32_t* __restrict__ pi, uint64_t seed, uint64_t d, ModN mn,
@@ -109,13 +128,18 @@ build_kernel(const uint32_t* __restrict__ pi, uint64_t seed, uint64_t d, ModN mn
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const uint32_t N = mn.N;
+  const uint32_t d32 = (uint32_t)d;   // d <= 2^31 (checked on the host)
 
-  // per-warp: indptr slice (RW+1 int64), then the RW x W sketch tile (16-B aligned)
-  const size_t ip_bytes = (((size_t)(RW + 1) * 8 + 15) / 16) * 16;
+  // per-warp: indptr slice (RW+1 int64), window-relative int32 copy, then the RW x W tile
+  const size_t ip_bytes = (((size_t)(RW + 1) * 12 + 15) / 16) * 16;
   const size_t tile_bytes = (((size_t)RW * W * 4 + 15) / 16) * 16;
   unsigned char* wbase = smem + pi_bytes + (size_t)warp * (ip_bytes + tile_bytes);
   int64_t* ip_s = reinterpret_cast<int64_t*>(wbase);
+  const uint32_t rel_a = smem_u32(wbase + (size_t)(RW + 1) * 8);
+  int* rel_p = reinterpret_cast<int*>(wbase + (size_t)(RW + 1) * 8);
   uint32_t* tile = reinterpret_cast<uint32_t*>(wbase + ip_bytes);
+  const uint32_t tile_a = smem_u32(tile);
+  const uint32_t pi_a = smem_u32(smem);
 
   unsigned bad_bits = 0;
   if (MODE == kPiSmem16) {
@@ -130,6 +154,7 @@ build_kernel(const uint32_t* __restrict__ pi, uint64_t seed, uint64_t d, ModN mn
   }
   if (MODE == kPiSmem16 || MODE == kPiCache) __syncthreads();
 
+  uint32_t max_idx = 0, max_j = 0;   // validity, checked once at the end
   const bool vec = (reinterpret_cast<uintptr_t>(indices) & 15u) == 0;
   const uint64_t ntiles = (n + RW - 1) / RW;
   for (uint64_t t = (uint64_t)blockIdx.x * nwarps + warp; t < ntiles; t += (uint64_t)gridDim.x * nwarps) {
@@ -147,40 +172,88 @@ build_kernel(const uint32_t* __restrict__ pi, uint64_t seed, uint64_t d, ModN mn
     if (__all_sync(0xffffffffu, ok)) {
       const int64_t e0 = ip_s[0], e1 = ip_s[rows];
       uint32_t cr = 0;
-      int64_t nxt = ip_s[1];
-      // Each lane handles 2 quads (8 consecutive-in-pairs elements) per iteration: quads at
-      // p and p + 128, with p = base + 4*lane + 256*it; 16-byte streaming loads when aligned.
-      const int64_t base = vec ? (e0 & ~(int64_t)3) : e0;
-      for (int64_t p = base + 4 * lane; p < e1; p += 256) {
-        int v[8];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t q = p + 128 * h;
-          if (vec && q + 4 <= e1) {
-            const int4 t4 = __ldcs(reinterpret_cast<const int4*>(indices + q));
-            v[4 * h + 0] = t4.x; v[4 * h + 1] = t4.y; v[4 * h + 2] = t4.z; v[4 * h + 3] = t4.w;
+      // The tile's nonzeros [e0, e1) are walked in windows of 2^30 elements with 32-bit
+      // window-relative offsets (one window unless a tile holds > 1e9 nonzeros). Lane l
+      // owns the quads at 4l + 256 it and 4l + 128 + 256 it.
+      const int64_t first = vec ? (e0 & ~(int64_t)3) : e0;
+      for (int64_t wb = first; wb < e1; wb += (int64_t)1 << 30) {
+        const int n_el = (int)min((int64_t)1 << 30, e1 - wb);
+        const int lo = (int)max((int64_t)0, e0 - wb);
+        for (uint32_t i = lane; i <= rows; i += 32) {
+          const int64_t x = ip_s[i] - wb;
+          rel_p[i] = x > 0x7fffffff ? 0x7fffffff : (x < 0 ? 0 : (int)x);
+        }
+        __syncwarp();
+        const int* __restrict__ src = indices + wb;
+        int nxt = lds_s32(rel_a + 4 * (cr + 1));
+        auto load_quad = [&](int q, int (&v)[4]) {
+          if (vec && q + 4 <= n_el) {
+            const int4 t4 = __ldcs(reinterpret_cast<const int4*>(src + q));
+            v[0] = t4.x; v[1] = t4.y; v[2] = t4.z; v[3] = t4.w;
           } else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[4 * h + u] = (q + u >= e0 && q + u < e1) ? __ldcs(indices + q + u) : 0;
+            for (int u = 0; u < 4; ++u) v[u] = (q + u >= lo && q + u < n_el) ? __ldcs(src + q + u) : 0;
           }
-        }
-        uint32_t j[8];
-        bool valid[8];
+        };
+        int cur[2][4], nx[2][4];
+        int p = 4 * lane;
+        if (p < n_el) { load_quad(p, cur[0]); load_quad(p + 128, cur[1]); }
+        for (; p < n_el; p += 256) {
+          if (p + 256 < n_el) { load_quad(p + 256, nx[0]); load_quad(p + 384, nx[1]); }
+          uint32_t idx[8], j[8];
+          bool in[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int64_t e = p + 128 * (u >> 2) + (u & 3);
-          valid[u] = e >= e0 && e < e1;
-          if (valid[u] && (v[u] < 0 || (uint64_t)v[u] >= d)) { bad_bits = kStatusIndex; valid[u] = false; }
-          j[u] = valid[u] ? pi_lookup<MODE>((uint32_t)v[u], pi, seed, mn, smem) : 0u;
-        }
+          for (int u = 0; u < 8; ++u) {
+            const int e = p + 128 * (u >> 2) + (u & 3);
+            in[u] = (unsigned)(e - lo) < (unsigned)(n_el - lo);
+            const uint32_t x = (uint32_t)cur[u >> 2][u & 3];
+            max_idx = in[u] ? max(max_idx, x) : max_idx;    // negative -> huge -> flagged
+            idx[u] = min(x, d32 - 1);
+          }
+          if (MODE == kPiGlobal) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (!valid[u]) continue;
-          if (MODE != kPiSeeded && MODE != kPiSmem16 && j[u] >= N) { bad_bits = kStatusIndex; continue; }
-          const int64_t e = p + 128 * (u >> 2) + (u & 3);
-          while (e >= nxt) { ++cr; nxt = ip_s[cr + 1]; }
-          atomicOr(tile + cr * W + (j[u] >> 5), 1u << (j[u] & 31u));
+            for (int u = 0; u < 8; ++u) j[u] = __ldg(pi + idx[u]);
+          } else if (MODE == kPiSmem16) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) j[u] = lds_u16(pi_a + 2 * idx[u]);
+          } else if (MODE == kPiSeeded) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) j[u] = pi_seeded(seed, idx[u], mn);
+          } else {
+            uint32_t c[8], g[8];
+            bool miss[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c[u] = lds_u32(pi_a + 4 * (idx[u] & (kCacheSlots - 1)));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              miss[u] = (c[u] >> 16) != (idx[u] >> 15);
+              g[u] = __ldg(pi + (miss[u] ? idx[u] : 0u));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              j[u] = miss[u] ? g[u] : (c[u] & 0xFFFFu);
+              if (miss[u] && in[u] && g[u] < 65536u)
+                sts_u32(pi_a + 4 * (idx[u] & (kCacheSlots - 1)), ((idx[u] >> 15) << 16) | g[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (MODE == kPiGlobal || MODE == kPiCache) {
+              max_j = in[u] ? max(max_j, j[u]) : max_j;
+              j[u] = min(j[u], N - 1);
+            }
+            if (in[u]) {
+              const int e = p + 128 * (u >> 2) + (u & 3);
+              while (e >= nxt) { ++cr; nxt = lds_s32(rel_a + 4 * (cr + 1)); }
+              red_or_shared(tile_a + 4 * (cr * W + (j[u] >> 5)), 1u << (j[u] & 31u));
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cur[h][u] = nx[h][u];
         }
+        __syncwarp();
       }
     } else {
       bad_bits = kStatusIndex;  // decreasing / negative indptr: rows of this tile stay zero
@@ -195,6 +268,7 @@ build_kernel(const uint32_t* __restrict__ pi, uint64_t seed, uint64_t d, ModN mn
     }
     __syncwarp();
   }
+  if (max_idx >= d32 || ((MODE == kPiGlobal || MODE == kPiCache) && max_j >= N)) bad_bits = kStatusIndex;
   if (__any_sync(0xffffffffu, bad_bits != 0) && lane == 0) latch(status, kStatusIndex);
 }
 
@@ -227,7 +301,7 @@ __global__ void build_wide_kernel(const uint32_t* __restrict__ pi, uint64_t seed
 static uint32_t pick_rw(uint32_t W, size_t per_warp) {
   uint32_t rw = std::max<uint32_t>(1, std::min<uint32_t>(32, kTileWordsMax / W));
   for (; rw >= 1; --rw) {
-    const size_t need = (((size_t)(rw + 1) * 8 + 15) / 16) * 16 + (((size_t)rw * W * 4 + 15) / 16) * 16;
+    const size_t need = (((size_t)(rw + 1) * 12 + 15) / 16) * 16 + (((size_t)rw * W * 4 + 15) / 16) * 16;
     if (need <= per_warp) return rw;
   }
   return 0;
@@ -256,6 +330,17 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
   } else if (N <= 65536 && d < 0x80000000ull - 32768ull) {
     mode = kPiCache; threads = 1024; pi_bytes = (size_t)kCacheSlots * 4;
   }
+  // Experiment knob (ncu A/B of the pi source): BINSKETCH_BUILD_MODE=global|cache|smem16.
+  const char* force = std::getenv("BINSKETCH_BUILD_MODE");
+  if (force && pi != nullptr && N <= 65536) {
+    if (!std::strcmp(force, "global")) { mode = kPiGlobal; threads = 256; pi_bytes = 0; }
+    if (!std::strcmp(force, "cache") && d < 0x80000000ull - 32768ull) {
+      mode = kPiCache; threads = 1024; pi_bytes = (size_t)kCacheSlots * 4;
+    }
+    if (!std::strcmp(force, "smem16") && smem16_bytes + 32 * 1024 <= optin) {
+      mode = kPiSmem16; threads = 1024; pi_bytes = smem16_bytes;
+    }
+  }
   uint32_t RW = pick_rw(W, (optin - pi_bytes) / (threads / 32));
   if (RW == 0 && mode != kPiSeeded && mode != kPiGlobal) {   // wide sketches: drop the smem table
     mode = kPiGlobal; threads = 256; pi_bytes = 0;
@@ -269,7 +354,7 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
     count_launch();
     return cudaGetLastError();
   }
-  const size_t per_warp = (((size_t)(RW + 1) * 8 + 15) / 16) * 16 + (((size_t)RW * W * 4 + 15) / 16) * 16;
+  const size_t per_warp = (((size_t)(RW + 1) * 12 + 15) / 16) * 16 + (((size_t)RW * W * 4 + 15) / 16) * 16;
   const size_t smem = pi_bytes + per_warp * (threads / 32);
   const uint64_t ntiles = (n + RW - 1) / RW;
   const uint64_t want_blocks = (ntiles + (threads / 32) - 1) / (threads / 32);
