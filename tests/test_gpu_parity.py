@@ -115,6 +115,38 @@ def test_build_adversarial_widths(N):
     _check_build((indptr, indices), N, seed=N, d=d)
 
 
+@pytest.mark.parametrize("mode", ["global", "cache", "cache32", "smem16"])
+def test_build_forced_pi_source(mode, monkeypatch):
+    """Every pi source of K1 (shared-memory table, shared-memory caches, L1/L2 gather) gives
+    the same bit-exact sketches, on Zipf data and on adversarial rows."""
+    monkeypatch.setenv("BINSKETCH_BUILD_MODE", mode)
+    _check_build(synth.scaled(synth.BUILD_ONLY, 20_000), synth.BUILD_ONLY_N, seeded_too=False)
+    _check_build(synth.scaled(synth.RANKING_DB, 2000), synth.RANKING_N, seeded_too=False)
+    rng = np.random.default_rng(7)
+    d, N = 70_000, 1224
+    rows = [np.array([], dtype=np.int32) if r % 5 == 0 else
+            rng.integers(0, d, int(rng.integers(1, 3000))).astype(np.int32) for r in range(400)]
+    indptr = np.zeros(len(rows) + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum([len(x) for x in rows])
+    _check_build((indptr, np.concatenate(rows)), N, seed=3, d=d, seeded_too=False)
+
+
+def test_build_unaligned_indices_view():
+    """indices not 16-B aligned (a view at offset 1): the scalar-load path."""
+    indptr, indices = synth.make_csr(synth.scaled(synth.LARGE, 3000))
+    N, d = synth.LARGE_N, synth.LARGE.d
+    pi = oracle.make_pi(synth.PI_SEED, d, N)
+    ref, _ = oracle.sketch(pi, d, N, indptr, indices)
+    buf = torch.zeros(len(indices) + 1, dtype=torch.int32, device="cuda")
+    buf[1:] = dev(indices)
+    view = buf[1:]
+    assert view.data_ptr() % 16 != 0
+    got = u32(bs.build(dev(pi.view(np.int32)), d, N, dev(indptr), view))
+    assert np.array_equal(got, ref)
+    got = u32(bs.build_seeded(synth.PI_SEED, d, N, dev(indptr), view))
+    assert np.array_equal(got, ref)
+
+
 def test_build_explicit_colliding_table_and_offset_indptr():
     d, N = 500, 70
     pi = (np.arange(d) % 7).astype(np.uint32)          # forced collisions: only 7 buckets used
