@@ -27,6 +27,7 @@ UNITS = {
     "api.cu": [],
     "build.cu": [],
     "pairs.cu": ["-fmad=false"],
+    "tc.cu": ["-fmad=false"],
 }
 HEADERS = ["bsk_internal.cuh", "bsk_device.cuh"]
 

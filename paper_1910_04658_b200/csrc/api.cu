@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -53,14 +54,27 @@ TableCache& cache() {
 }
 
 struct Layout {
-  size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, total = 0;
+  size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, total = 0;
   uint32_t splits = 1;
 };
 
+// Pair engine: tensor cores (tcgen05 kind::i8 on {0,1}-byte operands, tc.cu) or CUDA
+// cores (LOP3 + POPC, pairs.cu). BINSKETCH_ENGINE=cuda|tc overrides (A/B measurement).
+bool use_tc(int op) {
+  const char* e = std::getenv("BINSKETCH_ENGINE");
+  if (e && !std::strcmp(e, "cuda")) return false;
+  return op == BINSKETCH_OP_ANDPOPC;
+}
+
 Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
   Layout l;
-  if (op == BINSKETCH_OP_ANDPOPC) return l;
   size_t off = 0;
+  if (op == BINSKETCH_OP_ANDPOPC) {   // only the tensor-core engine needs scratch: expanded operands
+    l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
+    l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
+    l.total = off;
+    return l;
+  }
   l.L = off; off += align_up((size_t)(N + 1) * 8);
   l.pa = off; off += align_up((size_t)na * 4);
   l.pb = off; off += align_up((size_t)nb * 4);
@@ -146,12 +160,20 @@ size_t binsketch_workspace_bytes(int op, uint64_t na, uint64_t nb, uint32_t N, u
 
 binsketch_status binsketch_andpopc(const uint32_t* A, uint64_t na, const uint32_t* B, uint64_t nb, uint32_t N,
                                    int32_t* out, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
-  (void)ws; (void)ws_bytes;
   if (N < 2) return BINSKETCH_EINVAL;
   if (na == 0 || nb == 0) return BINSKETCH_OK;
   if (!A || !B || !out) return BINSKETCH_EINVAL;
-  return cuda_status(bsk::launch_pairs(bsk::kAndPopc, A, na, B, nb, N, 0, nullptr, nullptr, nullptr, out,
-                                       reinterpret_cast<cudaStream_t>(stream)));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!use_tc(BINSKETCH_OP_ANDPOPC))
+    return cuda_status(bsk::launch_pairs(bsk::kAndPopc, A, na, B, nb, N, 0, nullptr, nullptr, nullptr, out, s));
+  const Layout l = layout(BINSKETCH_OP_ANDPOPC, na, nb, N, 0);
+  if (!ws || ws_bytes < l.total) return BINSKETCH_EWORKSPACE;
+  uint8_t* a8 = static_cast<uint8_t*>(ws) + l.a8;
+  uint8_t* b8 = static_cast<uint8_t*>(ws) + l.b8;
+  cudaError_t e = bsk::launch_expand(A, na, N, a8, s);
+  if (e == cudaSuccess) e = bsk::launch_expand(B, nb, N, b8, s);
+  if (e == cudaSuccess) e = bsk::launch_tc_andpopc(a8, na, b8, nb, N, out, s);
+  return cuda_status(e);
 }
 
 binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, const uint32_t* sketches_b,

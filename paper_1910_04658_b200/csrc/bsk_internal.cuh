@@ -51,4 +51,11 @@ cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint6
                         const int32_t* pd, const double* L, double* part_key, int32_t* part_idx,
                         int32_t* out_idx, float* out_score, cudaStream_t s);
 
+// Tensor-core pair engine (tc.cu): sketches widened to {0,1} bytes, rows padded to
+// tc_kpad(N) bytes (multiple of 128), then tcgen05 kind::i8 all-pairs.
+uint32_t tc_kpad(uint32_t N);
+cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* out, cudaStream_t s);
+cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
+                              int32_t* out, cudaStream_t s);
+
 }  // namespace bsk

@@ -208,6 +208,31 @@ def test_andpopc_tiny_full():
     assert np.array_equal(bs.andpopc(Ad, Ad, synth.TINY_N).cpu().numpy(), oracle.andpopc(A, A, synth.TINY_N))
 
 
+@pytest.mark.parametrize("engine", ["tc", "cuda"])
+@pytest.mark.parametrize("N,na,nb", [(1024, 1100, 1300), (1224, 700, 2049), (4096, 257, 513),
+                                     (5000, 130, 300), (33, 129, 257), (2, 5, 7)])
+def test_andpopc_engines_tiles_and_tails(engine, N, na, nb, monkeypatch):
+    """Both pair engines bit-exact vs the oracle, at sizes spanning several 128 x 256
+    tensor-core tiles with ragged row tails and K padding (N not a multiple of 128)."""
+    monkeypatch.setenv("BINSKETCH_ENGINE", engine)
+    A = _sketches(synth.scaled(synth.LARGE, na, seed=91), N)
+    B = _sketches(synth.scaled(synth.LARGE, nb, seed=92), N)
+    got = bs.andpopc(dev(A.view(np.int32)), dev(B.view(np.int32)), N).cpu().numpy()
+    assert np.array_equal(got, oracle.andpopc(A, B, N))
+
+
+def test_andpopc_tc_saturated_and_empty_rows():
+    """All-ones and all-zero sketches: counts 0 and N exactly (no int8 saturation)."""
+    N = 1224
+    W = (N + 31) // 32
+    A = np.zeros((300, W), dtype=np.uint32)
+    A[::2] = 0xFFFFFFFF
+    A[::2, -1] = (1 << (N % 32)) - 1 if N % 32 else 0xFFFFFFFF
+    got = bs.andpopc(dev(A.view(np.int32)), dev(A.view(np.int32)), N).cpu().numpy()
+    assert np.array_equal(got, oracle.andpopc(A, A, N))
+    assert got.max() == N
+
+
 # ------------------------------------------------------------ estimate -----
 def test_estimate_tiny_full_all_planes():
     N, d = synth.TINY_N, synth.TINY.d
