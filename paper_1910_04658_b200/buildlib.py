@@ -29,7 +29,7 @@ UNITS = {
     "pairs.cu": ["-fmad=false"],
     "tc.cu": ["-fmad=false"],
 }
-HEADERS = ["bsk_internal.cuh", "bsk_device.cuh"]
+HEADERS = ["bsk_internal.cuh", "bsk_device.cuh", "bsk_estimator.cuh"]
 
 
 def _stale(target, deps):

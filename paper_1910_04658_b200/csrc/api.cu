@@ -27,6 +27,29 @@ inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 struct TableCache {
   std::mutex mu;
   std::map<std::pair<uint32_t, uint64_t>, double*> tables;
+  std::map<std::pair<uint32_t, uint64_t>, bool> convex_;
+
+  // L non-decreasing with non-decreasing increments (to 1e-9 relative): the condition
+  // under which the tensor-core top-k prefilter bound holds (K10). False e.g.
+  // when the saturation value L[N] = d is below L[N-1].
+  bool convex(uint32_t N, uint64_t d) {
+    const double* t = get(N, d);
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(N, d);
+    auto it = convex_.find(key);
+    if (it != convex_.end()) return it->second;
+    bool ok = t != nullptr;
+    for (uint32_t k = 0; ok && k < N; ++k) {
+      const double inc = t[k + 1] - t[k];
+      if (inc < 0.0) ok = false;
+      if (k > 0) {
+        const double prev = t[k] - t[k - 1];
+        if (inc < prev - 1e-9 * std::fabs(prev)) ok = false;
+      }
+    }
+    convex_.emplace(key, ok);
+    return ok;
+  }
 
   const double* get(uint32_t N, uint64_t d) {
     std::lock_guard<std::mutex> lock(mu);
@@ -54,16 +77,17 @@ TableCache& cache() {
 }
 
 struct Layout {
-  size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, total = 0;
+  size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, total = 0;
   uint32_t splits = 1;
 };
 
 // Pair engine: tensor cores (tcgen05 kind::i8 on {0,1}-byte operands, tc.cu) or CUDA
 // cores (LOP3 + POPC, pairs.cu). BINSKETCH_ENGINE=cuda|tc overrides (A/B measurement).
-bool use_tc(int op) {
+bool use_tc(int op, uint32_t N, uint32_t k = 0) {
   const char* e = std::getenv("BINSKETCH_ENGINE");
   if (e && !std::strcmp(e, "cuda")) return false;
-  return op == BINSKETCH_OP_ANDPOPC;
+  if (op == BINSKETCH_OP_TOPK) return k <= bsk::tc_topk_max_k() && N <= bsk::tc_topk_max_n();
+  return true;
 }
 
 Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
@@ -78,9 +102,19 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
   l.L = off; off += align_up((size_t)(N + 1) * 8);
   l.pa = off; off += align_up((size_t)na * 4);
   l.pb = off; off += align_up((size_t)nb * 4);
+  const bool tc = use_tc(op, N, k);
+  if (tc) {
+    l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
+    l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
+  }
+  if (op == BINSKETCH_OP_TOPK && tc && bsk::tc_sortable(N)) {
+    l.bins = off; off += align_up((size_t)(N + 1) * 4);
+    l.perm = off; off += align_up((size_t)nb * 4);
+    l.spb = off; off += align_up((size_t)nb * 4);
+  }
   if (op == BINSKETCH_OP_TOPK) {
-    l.splits = bsk::topk_splits(na, nb, k);
-    if (l.splits > 1) {
+    l.splits = tc ? bsk::tc_topk_splits(na, nb, k) : bsk::topk_splits(na, nb, k);
+    if (l.splits > 1 || tc) {
       l.pkey = off; off += align_up((size_t)na * l.splits * k * 8);
       l.pidx = off; off += align_up((size_t)na * l.splits * k * 4);
     }
@@ -164,7 +198,7 @@ binsketch_status binsketch_andpopc(const uint32_t* A, uint64_t na, const uint32_
   if (na == 0 || nb == 0) return BINSKETCH_OK;
   if (!A || !B || !out) return BINSKETCH_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (!use_tc(BINSKETCH_OP_ANDPOPC))
+  if (!use_tc(BINSKETCH_OP_ANDPOPC, N))
     return cuda_status(bsk::launch_pairs(bsk::kAndPopc, A, na, B, nb, N, 0, nullptr, nullptr, nullptr, out, s));
   const Layout l = layout(BINSKETCH_OP_ANDPOPC, na, nb, N, 0);
   if (!ws || ws_bytes < l.total) return BINSKETCH_EWORKSPACE;
@@ -192,10 +226,21 @@ binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, con
   int32_t* pa = reinterpret_cast<int32_t*>(w + l.pa);
   int32_t* pb = reinterpret_cast<int32_t*>(w + l.pb);
   cudaError_t e = bsk::launch_popcount(sketches_a, na, W, pa, s);
-  if (e == cudaSuccess) e = bsk::launch_popcount(sketches_b, nb, W, pb, s);
-  if (e == cudaSuccess)
-    e = bsk::launch_pairs(bsk::kEstimate, sketches_a, na, sketches_b, nb, N, measure, pa, pb,
-                          reinterpret_cast<const double*>(w + l.L), out, s);
+  const bool self = sketches_a == sketches_b && na == nb;
+  if (e == cudaSuccess) e = self ? cudaMemcpyAsync(pb, pa, na * 4, cudaMemcpyDeviceToDevice, s)
+                                 : bsk::launch_popcount(sketches_b, nb, W, pb, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (use_tc(BINSKETCH_OP_ESTIMATE, N)) {
+    uint8_t* a8 = reinterpret_cast<uint8_t*>(w + l.a8);
+    uint8_t* b8 = self ? a8 : reinterpret_cast<uint8_t*>(w + l.b8);
+    e = bsk::launch_expand(sketches_a, na, N, a8, s);
+    if (e == cudaSuccess && !self) e = bsk::launch_expand(sketches_b, nb, N, b8, s);
+    if (e == cudaSuccess)
+      e = bsk::launch_tc_estimate(a8, na, b8, nb, N, measure, pa, pb, reinterpret_cast<const double*>(w + l.L), out, s);
+    return cuda_status(e);
+  }
+  e = bsk::launch_pairs(bsk::kEstimate, sketches_a, na, sketches_b, nb, N, measure, pa, pb,
+                        reinterpret_cast<const double*>(w + l.L), out, s);
   return cuda_status(e);
 }
 
@@ -217,9 +262,28 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
   int32_t* pq = reinterpret_cast<int32_t*>(w + l.pa);
   int32_t* pd = reinterpret_cast<int32_t*>(w + l.pb);
   cudaError_t e = bsk::launch_popcount(queries, nq, W, pq, s);
-  if (e == cudaSuccess) e = bsk::launch_popcount(db, ndb, W, pd, s);
-  if (e == cudaSuccess)
-    e = bsk::launch_topk(queries, nq, db, ndb, N, measure, k, flags, pq, pd,
+  const bool self = queries == db && nq == ndb;
+  if (e == cudaSuccess) e = self ? cudaMemcpyAsync(pd, pq, nq * 4, cudaMemcpyDeviceToDevice, s)
+                                 : bsk::launch_popcount(db, ndb, W, pd, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (ndb > 0 && use_tc(BINSKETCH_OP_TOPK, N, k)) {
+    // db in popcount-descending order (tight per-tile prefilter), queries in their own order
+    uint8_t* q8 = reinterpret_cast<uint8_t*>(w + l.a8);
+    uint8_t* d8 = reinterpret_cast<uint8_t*>(w + l.b8);
+    const bool sorted = bsk::tc_sortable(N);
+    int32_t* perm = sorted ? reinterpret_cast<int32_t*>(w + l.perm) : nullptr;
+    int32_t* spb = sorted ? reinterpret_cast<int32_t*>(w + l.spb) : pd;
+    if (sorted) e = bsk::launch_sort_by_popcount(pd, ndb, N, reinterpret_cast<uint32_t*>(w + l.bins), perm, spb, s);
+    if (e == cudaSuccess) e = bsk::launch_expand(queries, nq, N, q8, s);
+    if (e == cudaSuccess) e = bsk::launch_expand(db, ndb, N, d8, s, perm);
+    if (e == cudaSuccess)
+      e = bsk::launch_tc_topk(q8, nq, d8, ndb, N, measure, k, flags, pq, spb, perm,
+                              reinterpret_cast<const double*>(w + l.L), cache().convex(N, d),
+                              reinterpret_cast<double*>(w + l.pkey), reinterpret_cast<int32_t*>(w + l.pidx), out_idx,
+                              out_score, s);
+    return cuda_status(e);
+  }
+  e = bsk::launch_topk(queries, nq, db, ndb, N, measure, k, flags, pq, pd,
                          reinterpret_cast<const double*>(w + l.L),
                          l.splits > 1 ? reinterpret_cast<double*>(w + l.pkey) : nullptr,
                          l.splits > 1 ? reinterpret_cast<int32_t*>(w + l.pidx) : nullptr, out_idx, out_score, s);

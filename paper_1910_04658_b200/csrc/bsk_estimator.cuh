@@ -1,0 +1,79 @@
+// bsk_estimator.cuh — the canonical fp64 estimator recipe (DESIGN.md R-C3) and the
+// top-k order, shared by the CUDA-core (pairs.cu) and tensor-core (tc.cu) pair engines.
+// Every fp64 operation is an explicit round-to-nearest intrinsic, and both units are
+// compiled with -fmad=false, so no contraction can change a bit relative to the oracle.
+#pragma once
+#include <cstdint>
+
+namespace bsk {
+
+// ----------------------------------------------------------- estimator ----
+struct Est {
+  double ip, ham, js, cs;
+};
+
+// The canonical recipe; `need` is the measure mask actually consumed.
+__device__ __forceinline__ Est estimate_pair(int pa, int pb, int pab, int N, const double* __restrict__ L,
+                                             uint32_t need) {
+  Est r;
+  const int pu = pa + pb - pab;
+  const double La = L[pa];
+  const double Lb = L[pb];
+  const double S = __dadd_rn(La, Lb);
+  double ip;
+  if (pu == N && pa < N && pb < N) {
+    ip = 0.0;
+  } else {
+    double raw = __dsub_rn(S, L[pu]);
+    double lo = raw > 0.0 ? raw : 0.0;
+    double cap = La < Lb ? La : Lb;
+    ip = lo < cap ? lo : cap;
+  }
+  r.ip = ip;
+  r.ham = 0.0;
+  r.js = 0.0;
+  r.cs = 0.0;
+  if (need & 2u) {
+    double h = __dsub_rn(S, __dmul_rn(2.0, ip));
+    h = h > 0.0 ? h : 0.0;
+    r.ham = h < S ? h : S;
+  }
+  if (need & 4u) {
+    if (pa == 0 && pb == 0) {
+      r.js = 1.0;
+    } else {
+      double v = __ddiv_rn(ip, __dsub_rn(S, ip));
+      v = v > 0.0 ? v : 0.0;
+      r.js = v < 1.0 ? v : 1.0;
+    }
+  }
+  if (need & 8u) {
+    if (pa == 0 || pb == 0) {
+      r.cs = 0.0;
+    } else {
+      double v = __ddiv_rn(ip, __dsqrt_rn(__dmul_rn(La, Lb)));
+      v = v > 0.0 ? v : 0.0;
+      r.cs = v < 1.0 ? v : 1.0;
+    }
+  }
+  return r;
+}
+
+
+// Order (reading R-G17): a before b iff a.key > b.key, or equal keys and
+// a.idx < b.idx. Sentinel (key = -inf, idx = INT_MAX) sorts last.
+__device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+constexpr int kSentinelIdx = 0x7fffffff;
+
+__device__ __forceinline__ double measure_key(const Est& e, uint32_t m) {
+  return m == 1u ? e.ip : m == 2u ? -e.ham : m == 4u ? e.js : e.cs;
+}
+__device__ __forceinline__ float key_to_score(double key, uint32_t m) {
+  return __double2float_rn(m == 2u ? -key : key);
+}
+
+
+}  // namespace bsk

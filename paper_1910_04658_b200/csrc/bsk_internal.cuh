@@ -46,6 +46,9 @@ cudaError_t launch_pairs(int mode, const uint32_t* A, uint64_t na, const uint32_
 
 // Top-k: number of db splits chosen for (nq, ndb, k) (pure function).
 uint32_t topk_splits(uint64_t nq, uint64_t ndb, uint32_t k);
+// Merge `splits` partial top-k lists per query ([nq][splits][k], unsorted ok) into the final lists.
+cudaError_t launch_topk_merge(uint64_t nq, uint32_t splits, uint32_t k, uint32_t measure, const double* part_key,
+                              const int32_t* part_idx, int32_t* out_idx, float* out_score, cudaStream_t s);
 cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint64_t ndb, uint32_t N,
                         uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq,
                         const int32_t* pd, const double* L, double* part_key, int32_t* part_idx,
@@ -54,8 +57,29 @@ cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint6
 // Tensor-core pair engine (tc.cu): sketches widened to {0,1} bytes, rows padded to
 // tc_kpad(N) bytes (multiple of 128), then tcgen05 kind::i8 all-pairs.
 uint32_t tc_kpad(uint32_t N);
-cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* out, cudaStream_t s);
+// perm (optional): output row r is sketch perm[r].
+cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* out, cudaStream_t s,
+                          const int32_t* perm = nullptr);
 cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
                               int32_t* out, cudaStream_t s);
+cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
+                               uint32_t measure, const int32_t* pa, const int32_t* pb, const double* L, float* out,
+                               cudaStream_t s);
+// Fused top-k on the tensor-core engine for k <= tc_topk_max_k(); partial lists
+// [nq][tc_topk_splits][k] in the workspace, then the merge kernel. `prefilter` enables
+// the integer L[pab] bound (valid when L is non-decreasing and convex).
+uint32_t tc_topk_max_k();
+uint32_t tc_topk_max_n();
+uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t k);
+// db order: counting sort by popcount, descending (perm: sorted position -> db row; spb:
+// sorted popcounts; bins: N+1 words of scratch). Needs N <= 65536 (tc_sortable).
+bool tc_sortable(uint32_t N);
+cudaError_t launch_sort_by_popcount(const int32_t* pb, uint64_t n, uint32_t N, uint32_t* bins, int32_t* perm,
+                                    int32_t* spb, cudaStream_t s);
+// D8 rows in `perm` order (or db order when perm == nullptr), pd the matching popcounts.
+cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
+                           uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* pd,
+                           const int32_t* perm, const double* L, bool prefilter, double* part_key, int32_t* part_idx,
+                           int32_t* out_idx, float* out_score, cudaStream_t s);
 
 }  // namespace bsk

@@ -18,61 +18,10 @@
 #include <cstdint>
 
 #include "bsk_device.cuh"
+#include "bsk_estimator.cuh"
 #include "bsk_internal.cuh"
 
 namespace bsk {
-
-// ----------------------------------------------------------- estimator ----
-struct Est {
-  double ip, ham, js, cs;
-};
-
-// The canonical recipe; `need` is the measure mask actually consumed.
-__device__ __forceinline__ Est estimate_pair(int pa, int pb, int pab, int N, const double* __restrict__ L,
-                                             uint32_t need) {
-  Est r;
-  const int pu = pa + pb - pab;
-  const double La = L[pa];
-  const double Lb = L[pb];
-  const double S = __dadd_rn(La, Lb);
-  double ip;
-  if (pu == N && pa < N && pb < N) {
-    ip = 0.0;
-  } else {
-    double raw = __dsub_rn(S, L[pu]);
-    double lo = raw > 0.0 ? raw : 0.0;
-    double cap = La < Lb ? La : Lb;
-    ip = lo < cap ? lo : cap;
-  }
-  r.ip = ip;
-  r.ham = 0.0;
-  r.js = 0.0;
-  r.cs = 0.0;
-  if (need & 2u) {
-    double h = __dsub_rn(S, __dmul_rn(2.0, ip));
-    h = h > 0.0 ? h : 0.0;
-    r.ham = h < S ? h : S;
-  }
-  if (need & 4u) {
-    if (pa == 0 && pb == 0) {
-      r.js = 1.0;
-    } else {
-      double v = __ddiv_rn(ip, __dsub_rn(S, ip));
-      v = v > 0.0 ? v : 0.0;
-      r.js = v < 1.0 ? v : 1.0;
-    }
-  }
-  if (need & 8u) {
-    if (pa == 0 || pb == 0) {
-      r.cs = 0.0;
-    } else {
-      double v = __ddiv_rn(ip, __dsqrt_rn(__dmul_rn(La, Lb)));
-      v = v > 0.0 ? v : 0.0;
-      r.cs = v < 1.0 ? v : 1.0;
-    }
-  }
-  return r;
-}
 
 // ------------------------------------------------------------ mainloop ----
 template <int BM, int BN, int TM, int TN, int KC>
@@ -202,14 +151,6 @@ cudaError_t launch_pairs(int mode, const uint32_t* A, uint64_t na, const uint32_
 }
 
 // ------------------------------------------------------------ top-k (K4) --
-// Order (reading R-G17): a before b iff a.key > b.key, or equal keys and
-// a.idx < b.idx. Sentinel (key = -inf, idx = INT_MAX) sorts last.
-__device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
-  return ka > kb || (ka == kb && ia < ib);
-}
-
-constexpr int kSentinelIdx = 0x7fffffff;
-
 // One warp sorts n (power of two) (key, idx) entries in shared memory, best first.
 __device__ void warp_bitonic_sort(double* key, int* idx, int n) {
   const int lane = threadIdx.x & 31;
@@ -251,13 +192,6 @@ __device__ void block_bitonic_sort(double* key, int* idx, int n) {
       __syncthreads();
     }
   }
-}
-
-__device__ __forceinline__ double measure_key(const Est& e, uint32_t m) {
-  return m == 1u ? e.ip : m == 2u ? -e.ham : m == 4u ? e.js : e.cs;
-}
-__device__ __forceinline__ float key_to_score(double key, uint32_t m) {
-  return __double2float_rn(m == 2u ? -key : key);
 }
 
 constexpr int kTBN = 64, kTKC = 32;
@@ -460,9 +394,15 @@ cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint6
   else if (k <= 256 - kTBN)  e = launch_topk_t<16, 256>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, s);
   else                       e = launch_topk_t<16, 512>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, s);
   if (e != cudaSuccess || splits == 1) return e;
+  return launch_topk_merge(nq, splits, k, measure, part_key, part_idx, out_idx, out_score, s);
+}
+
+cudaError_t launch_topk_merge(uint64_t nq, uint32_t splits, uint32_t k, uint32_t measure, const double* part_key,
+                              const int32_t* part_idx, int32_t* out_idx, float* out_score, cudaStream_t s) {
+  if (nq == 0 || k == 0) return cudaSuccess;
   const uint32_t P = next_pow2(splits * k);
   const size_t smem = (size_t)P * 12;
-  e = cudaFuncSetAttribute(topk_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(topk_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   topk_merge_kernel<<<(unsigned)nq, 256, smem, s>>>(nq, splits, k, P, measure, part_key, part_idx, out_idx, out_score);
   count_launch();

@@ -23,10 +23,12 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 
+#include "bsk_estimator.cuh"
 #include "bsk_internal.cuh"
 
 namespace bsk {
@@ -110,13 +112,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 // ------------------------------------------------------------- expansion ---
 // out[r][b] = bit b of row r (LSB-first words), b < 32W; zero for 32W <= b < Kp.
 __global__ void expand_kernel(const uint32_t* __restrict__ sk, uint64_t n, uint32_t W, uint32_t Kp,
-                              uint8_t* __restrict__ out) {
+                              const int32_t* __restrict__ perm, uint8_t* __restrict__ out) {
   const uint32_t chunks = Kp / 32;   // one 32-byte chunk per sketch word
   const uint64_t total = n * chunks;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t r = i / chunks;
     const uint32_t c = (uint32_t)(i - r * chunks);
-    const uint32_t w = c < W ? __ldg(sk + r * W + c) : 0u;
+    const uint64_t src = perm ? (uint64_t)__ldg(perm + r) : r;   // row r of the output = sketch src
+    const uint32_t w = c < W ? __ldg(sk + src * W + c) : 0u;
     uint32_t b[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -129,38 +132,114 @@ __global__ void expand_kernel(const uint32_t* __restrict__ sk, uint64_t n, uint3
   }
 }
 
+// ------------------------------------------------- db order for top-k ---
+// Counting sort of the db rows by popcount, descending (bin N - pb), so every 256-row
+// tensor-core tile spans a narrow popcount range and the per-tile key bound is tight.
+// Order inside a bin is arbitrary: the top-k result is the unique top-k under
+// (key desc, original index asc), independent of processing order.
+__global__ void pb_hist_kernel(const int32_t* __restrict__ pb, uint64_t n, uint32_t N, uint32_t* __restrict__ bins) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(bins + (N - (uint32_t)__ldg(pb + i)), 1u);
+}
+
+__global__ void pb_scan_kernel(uint32_t* __restrict__ bins, uint32_t nbins) {   // one block, exclusive, in place
+  __shared__ uint32_t part[1024];
+  const uint32_t t = threadIdx.x, per = (nbins + blockDim.x - 1) / blockDim.x;
+  const uint32_t b0 = min(t * per, nbins), b1 = min(b0 + per, nbins);
+  uint32_t sum = 0;
+  for (uint32_t i = b0; i < b1; ++i) sum += bins[i];
+  part[t] = sum;
+  __syncthreads();
+  for (uint32_t o = 1; o < blockDim.x; o <<= 1) {
+    const uint32_t v = t >= o ? part[t - o] : 0u;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  uint32_t run = part[t] - sum;
+  for (uint32_t i = b0; i < b1; ++i) { const uint32_t c = bins[i]; bins[i] = run; run += c; }
+}
+
+__global__ void pb_scatter_kernel(const int32_t* __restrict__ pb, uint64_t n, uint32_t N, uint32_t* __restrict__ cursor,
+                                  int32_t* __restrict__ perm, int32_t* __restrict__ spb) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const int32_t v = __ldg(pb + i);
+    const uint32_t pos = atomicAdd(cursor + (N - (uint32_t)v), 1u);
+    perm[pos] = (int32_t)i;
+    spb[pos] = v;
+  }
+}
+
 // --------------------------------------------------------- pairs kernel ---
-constexpr int kTcM = 128, kTcN = 256, kTcK = 128, kTcStages = 4;
-constexpr uint32_t kTcABytes = kTcM * kTcK, kTcBBytes = kTcN * kTcK, kTcStageBytes = kTcABytes + kTcBBytes;
+// Output tile 128 (A rows) x 256 (B rows). K is streamed in KC-byte chunks: KC = 128
+// (SWIZZLE_128B) for the plain AND-popcount, KC = 64 (SWIZZLE_64B, half-size stages, so
+// deeper rings fit next to the estimator table / per-row top-k heaps) otherwise.
+constexpr int kTcM = 128, kTcN = 256;
 constexpr uint32_t kTcThreads = 192;                       // producer, MMA, 4 epilogue warps
-constexpr uint32_t kTcSmem = kTcStages * kTcStageBytes + 1024 /* barriers */ + 1024 /* align slack */;
+constexpr uint32_t kTcSmemMax = 227 * 1024;
 // instruction descriptor: D s32, A/B u8, K-major, N = 256, M = 128
 constexpr uint32_t kTcIdesc = (2u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+enum TcMode { kTcAndPopc = 0, kTcEstimate = 1, kTcTopk = 2 };
+
+template <int KC>
+struct TcGeom {
+  static constexpr uint32_t kABytes = kTcM * KC, kBBytes = kTcN * KC, kStageBytes = kABytes + kBBytes;
+};
+
+// K-major operand tile of KC-byte rows, swizzled as TMA writes it: 8-row atoms of 8*KC
+// bytes (SBO); descriptor version 1 (sm_100); layout SWIZZLE_128B (2) or SWIZZLE_64B (4).
+template <int KC>
+__device__ __forceinline__ uint64_t desc_sw(uint32_t addr) {
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;                          // leading byte offset (unused, swizzled K-major)
+  d |= (uint64_t)((8u * KC) >> 4) << 32;            // stride byte offset
+  d |= (uint64_t)1u << 46;                          // version
+  d |= (uint64_t)(KC == 128 ? 2u : 4u) << 61;       // swizzle mode
+  return d;
+}
 
 struct TcParams {
   uint64_t na, nb;
-  uint32_t nk;          // K stages per tile = Kp / 128
-  uint32_t tiles_n;     // ceil(nb / 256)
-  uint64_t ntiles;
-  int32_t* out;         // kAndPopc: int32 [na][nb]
+  uint32_t nk;            // K chunks per tile = Kp / KC
+  uint32_t stages;        // ring depth
+  uint32_t tiles_n;       // ceil(nb / 256)
+  uint32_t splits, per;   // work item = (m-tile, split); split s covers n-tiles [s*per, s*per + per)
+  uint64_t nitems;
+  int32_t* out_i32;       // kTcAndPopc: int32 [na][nb]
+  float* out_f32;         // kTcEstimate: float [popcount(measure)][na][nb]
+  uint32_t measure, N, k, flags, prefilter;
+  const int32_t* pa;      // |a_s| per A row
+  const int32_t* pb;      // |b_s| per B row
+  const double* L;        // cardinality table, global (kTcTopk survivors, kTcEstimate if not staged)
+  double* part_key;       // kTcTopk: [na][splits][k] (unsorted partial lists)
+  int32_t* part_idx;
+  uint32_t l_smem;        // kTcEstimate: table staged in shared memory (bytes, 0 = not staged)
+  uint32_t heap_smem;     // kTcTopk: per-row heaps + survivor scratch in shared memory (bytes)
+  const int32_t* perm;    // kTcTopk: B row (sorted by |b_s| descending) -> original db index
+  uint32_t l_topk_smem;   // kTcTopk: table staged after the heaps (bytes, 0 = global)
 };
 
-template <int MODE>
+template <int MODE, int KC>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
+  using G = TcGeom<KC>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // 1 KB alignment by pointer arithmetic on the shared array (keeps the shared address space,
+  // so heap / table accesses compile to LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (tc::saddr(smem_raw) & 1023u)) & 1023u);
+  const uint32_t S = p.stages;
   const uint32_t base = tc::saddr(smem);
-  const uint32_t bars = base + kTcStages * kTcStageBytes;
-  auto full = [&](int s) { return bars + 8u * s; };
-  auto empty = [&](int s) { return bars + 8u * (kTcStages + s); };
-  auto tfull = [&](int a) { return bars + 8u * (2 * kTcStages + a); };
-  auto tempty = [&](int a) { return bars + 8u * (2 * kTcStages + 2 + a); };
-  const uint32_t tmem_slot = bars + 8u * (2 * kTcStages + 4);
+  const uint32_t bars = base + S * G::kStageBytes;
+  auto full = [&](uint32_t s) { return bars + 8u * s; };
+  auto empty = [&](uint32_t s) { return bars + 8u * (S + s); };
+  auto tfull = [&](int a) { return bars + 8u * (2 * S + a); };
+  auto tempty = [&](int a) { return bars + 8u * (2 * S + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * S + 4);
+  uint8_t* extra = smem + S * G::kStageBytes + 1024;        // estimator table or top-k heaps
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kTcStages; ++s) { tc::mbar_init(full(s), 1); tc::mbar_init(empty(s), 1); }
+    for (uint32_t s = 0; s < S; ++s) { tc::mbar_init(full(s), 1); tc::mbar_init(empty(s), 1); }
     for (int a = 0; a < 2; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), 128); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -168,82 +247,329 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tmem_slot));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  const double* L = p.L;
+  double* Ls = reinterpret_cast<double*>(extra + (MODE == kTcTopk ? p.heap_smem : 0u));
+  if ((MODE == kTcEstimate && p.l_smem) || MODE == kTcTopk) {   // top-k always stages the table
+    for (uint32_t i = threadIdx.x; i <= p.N; i += blockDim.x) Ls[i] = p.L[i];
+    L = Ls;
+  }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   uint32_t tmem;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot));
 
+  // every role walks the same (item, n-tile) sequence
+  auto item_range = [&](uint64_t it, uint64_t& mt, uint32_t& sp, uint32_t& nt0, uint32_t& nt1) {
+    mt = it / p.splits;
+    sp = (uint32_t)(it - mt * p.splits);
+    nt0 = sp * p.per;
+    nt1 = min(nt0 + p.per, p.tiles_n);
+  };
+
   if (warp == 0) {
     if (lane == 0) {   // ---- TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const int32_t m0 = (int32_t)((t / p.tiles_n) * kTcM), n0 = (int32_t)((t % p.tiles_n) * kTcN);
-        for (uint32_t kc = 0; kc < p.nk; ++kc) {
-          tc::mbar_wait(empty(stage), phase ^ 1u);
-          const uint32_t sa = base + stage * kTcStageBytes;
-          tc::mbar_expect_tx(full(stage), kTcStageBytes);
-          tc::tma_load_2d(sa, &tmA, (int32_t)(kc * kTcK), m0, full(stage));
-          tc::tma_load_2d(sa + kTcABytes, &tmB, (int32_t)(kc * kTcK), n0, full(stage));
-          if (++stage == kTcStages) { stage = 0; phase ^= 1u; }
+      uint32_t stage = 0, phase = 0;
+      for (uint64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+        uint64_t mt; uint32_t sp, nt0, nt1;
+        item_range(it, mt, sp, nt0, nt1);
+        for (uint32_t nt = nt0; nt < nt1; ++nt) {
+          for (uint32_t kc = 0; kc < p.nk; ++kc) {
+            tc::mbar_wait(empty(stage), phase ^ 1u);
+            const uint32_t sa = base + stage * G::kStageBytes;
+            tc::mbar_expect_tx(full(stage), G::kStageBytes);
+            tc::tma_load_2d(sa, &tmA, (int32_t)(kc * KC), (int32_t)(mt * kTcM), full(stage));
+            tc::tma_load_2d(sa + G::kABytes, &tmB, (int32_t)(kc * KC), (int32_t)(nt * kTcN), full(stage));
+            if (++stage == S) { stage = 0; phase ^= 1u; }
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {   // ---- MMA issuer
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, aphase = 0;
-      for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        tc::mbar_wait(tempty(acc), aphase ^ 1u);
-        tc::fence_after();
-        const uint32_t d = tmem + (uint32_t)acc * kTcN;
-        for (uint32_t kc = 0; kc < p.nk; ++kc) {
-          tc::mbar_wait(full(stage), phase);
+      uint32_t stage = 0, phase = 0, aphase = 0;
+      int acc = 0;
+      for (uint64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+        uint64_t mt; uint32_t sp, nt0, nt1;
+        item_range(it, mt, sp, nt0, nt1);
+        for (uint32_t nt = nt0; nt < nt1; ++nt) {
+          tc::mbar_wait(tempty(acc), aphase ^ 1u);
           tc::fence_after();
-          const uint32_t sa = base + stage * kTcStageBytes;
-          const uint64_t da = tc::desc_sw128(sa), db = tc::desc_sw128(sa + kTcABytes);
+          const uint32_t d = tmem + (uint32_t)acc * kTcN;
+          for (uint32_t kc = 0; kc < p.nk; ++kc) {
+            tc::mbar_wait(full(stage), phase);
+            tc::fence_after();
+            const uint32_t sa = base + stage * G::kStageBytes;
+            const uint64_t da = desc_sw<KC>(sa), db = desc_sw<KC>(sa + G::kABytes);
 #pragma unroll
-          for (int kk = 0; kk < kTcK / 32; ++kk)   // K = 32 bytes per MMA: +2 in 16-B units
-            tc::mma_u8(d, da + 2u * kk, db + 2u * kk, kTcIdesc, (kc | (uint32_t)kk) != 0u);
-          tc::commit(empty(stage));                // frees the smem stage when these MMAs finish
-          if (++stage == kTcStages) { stage = 0; phase ^= 1u; }
+            for (int kk = 0; kk < KC / 32; ++kk)   // K = 32 bytes per MMA: +2 in 16-B units
+              tc::mma_u8(d, da + 2u * kk, db + 2u * kk, kTcIdesc, (kc | (uint32_t)kk) != 0u);
+            tc::commit(empty(stage));              // frees the smem stage when these MMAs finish
+            if (++stage == S) { stage = 0; phase ^= 1u; }
+          }
+          tc::commit(tfull(acc));                  // accumulator ready for the epilogue
+          if (++acc == 2) { acc = 0; aphase ^= 1u; }
         }
-        tc::commit(tfull(acc));                    // accumulator ready for the epilogue
-        if (++acc == 2) { acc = 0; aphase ^= 1u; }
       }
     }
-  } else {             // ---- epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
+  } else if (MODE == kTcTopk) {
+    // ---- top-k epilogue: thread = one query row (TMEM lane), its k best (key, db index)
+    // as a heap (worst at the root) in shared memory. Per 256-column tile: a prefilter
+    // bound pmin on the AND-popcount (db sorted by popcount, so the tile's pb range is
+    // narrow); chunks of 32 columns whose max pab < pmin are skipped with one compare.
+    // Survivors: while a row's heap fills, each lane evaluates its own columns; in steady
+    // state they go through a per-warp queue and are scored lane-parallel (exact fp64
+    // recipe), only the rare insertions being serialised to the owning lane.
     const uint32_t lb = 32u * (uint32_t)(warp & 3);
-    const uint32_t row_in_tile = lb + (uint32_t)lane;
-    int acc = 0;
+    const uint32_t rt = lb + (uint32_t)lane;          // row within the tile
+    const uint32_t m = p.measure, K = p.k;
+    constexpr uint32_t kQCap = 256;                   // per-warp survivor queue entries
+    double* hk = reinterpret_cast<double*>(extra);
+    int32_t* hi = reinterpret_cast<int32_t*>(extra + (size_t)K * kTcM * 8);
+    uint32_t* scr = reinterpret_cast<uint32_t*>(extra + (size_t)K * kTcM * 12);            // [32][128]
+    // this warp's copy of the tile's db popcounts [256] and original indices [256]
+    int32_t* tpb = reinterpret_cast<int32_t*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4) + (size_t)(warp - 2) * 2 * kTcN;
+    int32_t* tpm = tpb + kTcN;
+    uint2* q = reinterpret_cast<uint2*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4) +
+               (size_t)(warp - 2) * kQCap;
+    uint4* cq = reinterpret_cast<uint4*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 +
+                                         4 * kQCap * 8) + (size_t)(warp - 2) * 32;   // per-warp candidate list
+    auto hkey = [&](uint32_t i) -> double& { return hk[i * kTcM + rt]; };
+    auto hidx = [&](uint32_t i) -> int32_t& { return hi[i * kTcM + rt]; };
     uint32_t aphase = 0;
-    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-      const uint64_t m0 = (t / p.tiles_n) * kTcM, n0 = (t % p.tiles_n) * kTcN;
-      tc::mbar_wait(tfull(acc), aphase);
-      tc::fence_after();
-      const uint64_t r = m0 + row_in_tile;
-#pragma unroll 1
-      for (int c = 0; c < kTcN; c += 32) {
-        uint32_t v[32];
-        tc::tmem_ld32(tmem + (lb << 16) + (uint32_t)acc * kTcN + (uint32_t)c, v);
-        if (MODE == kAndPopc && r < p.na && n0 + c < p.nb) {
-          int32_t* o = p.out + r * p.nb + n0 + c;
-          const uint64_t left = p.nb - (n0 + c);   // > 0 here
-          if (left >= 32 && ((reinterpret_cast<uintptr_t>(o) & 15u) == 0)) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              __stcs(reinterpret_cast<int4*>(o + j), make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]));
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if ((uint64_t)j < left) __stcs(o + j, (int32_t)v[j]);
+    int acc = 0;
+    for (uint64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+      uint64_t mt; uint32_t sp, nt0, nt1;
+      item_range(it, mt, sp, nt0, nt1);
+      const uint64_t r = mt * kTcM + rt;
+      const bool valid = r < p.na;
+      const int pa = valid ? __ldg(p.pa + r) : 0;
+      const double La = Ls[pa];
+      const bool filt = p.prefilter && pa > 0;
+      uint32_t cnt = valid ? 0u : K, pmin = 0, pcur = 0;   // invalid rows count as full (never insert)
+      double T = -__longlong_as_double(0x7ff0000000000000LL);
+      int32_t Ti = kSentinelIdx;
+      auto sift_down = [&](uint32_t i) {
+        for (;;) {
+          const uint32_t l = 2 * i + 1, rr = l + 1;
+          uint32_t w = i;
+          if (l < K && before(hkey(w), hidx(w), hkey(l), hidx(l))) w = l;
+          if (rr < K && before(hkey(w), hidx(w), hkey(rr), hidx(rr))) w = rr;
+          if (w == i) break;
+          const double tk = hkey(i); const int32_t ti = hidx(i);
+          hkey(i) = hkey(w); hidx(i) = hidx(w);
+          hkey(w) = tk; hidx(w) = ti;
+          i = w;
+        }
+      };
+      // offer (key, original db index) to this lane's row
+      auto offer = [&](double key, int32_t orig) {
+        if ((p.flags & 1u) && (uint64_t)orig == r) return;
+        if (cnt < K) {
+          hkey(cnt) = key; hidx(cnt) = orig;
+          if (++cnt == K) {
+            for (int i = (int)K / 2 - 1; i >= 0; --i) sift_down((uint32_t)i);
+            T = hkey(0); Ti = hidx(0);
           }
+        } else if (before(key, orig, T, Ti)) {
+          hkey(0) = key; hidx(0) = orig;
+          sift_down(0);
+          T = hkey(0); Ti = hidx(0);
+        }
+      };
+      // Upper bound of the key over every pair of this row with a db row of popcount
+      // pb in [lo, hi] and AND-popcount pab (K10): the IP raw value decreases
+      // in pb for fixed pab (L convex), so IP <= U = min(max(La + L[lo] - L[pa+lo-pab], 0),
+      // La, L[hi]); then JS <= U/(La+L[lo]-U), COS <= U/sqrt(La*L[lo]), -HAM <= min(2U-La-L[lo], 0).
+      // Non-decreasing in pab.
+      auto key_bound = [&](uint32_t pab, uint32_t lo, uint32_t hi_) -> double {
+        const uint32_t pu = min(pa + lo - min(pab, pa + lo), p.N);
+        const double Llo = Ls[lo];
+        double u = La + Llo - Ls[pu];
+        u = u > 0.0 ? u : 0.0;
+        u = fmin(u, fmin(La, Ls[hi_]));
+        if (m == 1u) return u;
+        if (m == 4u) { const double den = La + Llo - u; return den > 0.0 ? fmin(u / den, 1.0) : 1.0; }
+        if (m == 8u) return fmin(u / sqrt(La * Llo), 1.0);
+        return fmin(2.0 * u - La - Llo, 0.0);
+      };
+      // smallest pab whose bound reaches the current threshold (slack for fp64 rounding)
+      auto tile_pmin = [&](uint32_t lo, uint32_t hi_) -> uint32_t {
+        if (!filt || cnt < K || lo == 0) return 0u;
+        const double g = T - 1e-9 * fmax(1.0, fabs(T));
+        const uint32_t pmax = min((uint32_t)pa, hi_);
+        if (key_bound(pmax, lo, hi_) < g) return pmax + 1;          // no pair of the tile can enter
+        uint32_t qq = min(pcur, pmax);
+        int steps = 0;
+        while (qq > 0 && steps < 8 && key_bound(qq - 1, lo, hi_) >= g) { --qq; ++steps; }
+        while (qq < pmax && steps < 8 && key_bound(qq, lo, hi_) < g) { ++qq; ++steps; }
+        if (steps == 8) {                                           // far move: bisect
+          uint32_t a0 = 0, b0 = pmax;
+          while (a0 < b0) { const uint32_t mid = (a0 + b0) / 2; if (key_bound(mid, lo, hi_) >= g) b0 = mid; else a0 = mid + 1; }
+          qq = a0;
+        }
+        pcur = qq;
+        return qq;
+      };
+      // per-tile staging of the db popcounts / original indices (8 columns per lane),
+      // loaded one tile ahead into registers, published to this warp's buffer
+      int32_t pf_pb[8], pf_pm[8];
+      auto prefetch = [&](uint32_t nt) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint64_t col = (uint64_t)nt * kTcN + 32 * u + lane;
+          const bool in = nt < nt1 && col < p.nb;
+          pf_pb[u] = in ? __ldg(p.pb + col) : 0;
+          pf_pm[u] = in ? (p.perm ? __ldg(p.perm + col) : (int32_t)col) : -1;
+        }
+      };
+      prefetch(nt0);
+      for (uint32_t nt = nt0; nt < nt1; ++nt) {
+        const uint64_t n0 = (uint64_t)nt * kTcN;
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { tpb[32 * u + lane] = pf_pb[u]; tpm[32 * u + lane] = pf_pm[u]; }
+        __syncwarp();
+        prefetch(nt + 1);                                     // in flight during this tile
+        const uint32_t nval = (uint32_t)min((uint64_t)kTcN, p.nb - n0);
+        if (valid) pmin = tile_pmin((uint32_t)tpb[nval - 1], (uint32_t)tpb[0]);   // pb descending in the tile
+        const bool direct = __any_sync(0xffffffffu, cnt < K);
+        tc::mbar_wait(tfull(acc), aphase);
+        tc::fence_after();
+#pragma unroll 1
+        for (uint32_t c = 0; c < (uint32_t)kTcN; c += 32) {
+          uint32_t v[32];
+          tc::tmem_ld32(tmem + (lb << 16) + (uint32_t)acc * kTcN + c, v);
+          if (c >= nval) continue;
+          const uint32_t left = nval - c;
+          uint32_t mx = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) mx = max(mx, v[j]);
+          const bool pass = valid && mx >= pmin;
+          if (!__any_sync(0xffffffffu, pass)) continue;
+          // survivor mask of this lane
+          uint32_t sm = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sm |= ((pass && v[j] >= pmin && (uint32_t)j < left) ? 1u : 0u) << j;
+          const uint32_t ns = __popc(sm);
+          uint32_t off = ns;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, off, o); if (lane >= o) off += y; }
+          const uint32_t total = __shfl_sync(0xffffffffu, off, 31);
+          off -= ns;
+          if (direct || total > kQCap) {
+            // per-lane: each lane walks its own survivors (heap filling, or a burst)
+            if (ns) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) scr[j * kTcM + rt] = v[j];
+              uint32_t mm = sm;
+              while (mm) {
+                const uint32_t j = __ffs(mm) - 1; mm &= mm - 1;
+                const double key = measure_key(estimate_pair(pa, tpb[c + j], (int)scr[j * kTcM + rt], (int)p.N, Ls, m), m);
+                if (cnt < K || key >= T) offer(key, tpm[c + j]);
+              }
+            }
+            __syncwarp();
+            continue;
+          }
+          // queue: (column in tile, owner lane << 24 | pab)
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if ((sm >> j) & 1u) q[off++] = make_uint2(c + (uint32_t)j, ((uint32_t)lane << 24) | v[j]);
+          __syncwarp();
+          for (uint32_t b = 0; b < total; b += 32) {
+            const bool has = b + lane < total;
+            const uint2 e = has ? q[b + lane] : make_uint2(0u, 0u);
+            const int owner = (int)(e.y >> 24);
+            const int pa_o = __shfl_sync(0xffffffffu, pa, owner);
+            const double T_o = __shfl_sync(0xffffffffu, T, owner);
+            double key = -__longlong_as_double(0x7ff0000000000000LL);
+            if (has) key = measure_key(estimate_pair(pa_o, tpb[e.x], (int)(e.y & 0xFFFFFFu), (int)p.N, Ls, m), m);
+            // candidates (key >= owner's threshold; ties resolved by the owner) go back to
+            // their owner lanes: every lane then inserts its own rows' candidates, in parallel
+            const bool cand = has && key >= T_o;
+            const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+            if (bal) {
+              __syncwarp();
+              if (cand) {
+                const uint32_t slot = __popc(bal & ((1u << lane) - 1u));
+                cq[slot] = make_uint4(e.x, (uint32_t)owner, __double2loint(key), __double2hiint(key));
+              }
+              __syncwarp();
+              const uint32_t nc = __popc(bal);
+              for (uint32_t t = 0; t < nc; ++t) {
+                const uint4 c4 = cq[t];
+                if (c4.y == (uint32_t)lane) offer(__hiloint2double((int)c4.w, (int)c4.z), tpm[c4.x]);
+              }
+            }
+          }
+          __syncwarp();
+        }
+        tc::fence_before();
+        tc::mbar_arrive(tempty(acc));
+        if (++acc == 2) { acc = 0; aphase ^= 1u; }
+      }
+      if (valid) {   // partial list of this (row, split), unsorted
+        double* ok = p.part_key + (r * p.splits + sp) * K;
+        int32_t* oi = p.part_idx + (r * p.splits + sp) * K;
+        for (uint32_t i = 0; i < K; ++i) {
+          ok[i] = i < cnt ? hkey(i) : -__longlong_as_double(0x7ff0000000000000LL);
+          oi[i] = i < cnt ? hidx(i) : kSentinelIdx;
         }
       }
-      tc::fence_before();
-      tc::mbar_arrive(tempty(acc));
-      if (++acc == 2) { acc = 0; aphase ^= 1u; }
+    }
+  } else {             // ---- andpopc / estimate epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
+    const uint32_t lb = 32u * (uint32_t)(warp & 3);
+    const uint32_t rt = lb + (uint32_t)lane;          // row within the tile
+    uint32_t aphase = 0;
+    int acc = 0;
+    const uint32_t m = p.measure;
+    for (uint64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+      uint64_t mt; uint32_t sp, nt0, nt1;
+      item_range(it, mt, sp, nt0, nt1);
+      const uint64_t r = mt * kTcM + rt;
+      const bool valid = r < p.na;
+      const int pa = (MODE == kTcEstimate && valid) ? __ldg(p.pa + r) : 0;
+      for (uint32_t nt = nt0; nt < nt1; ++nt) {
+        const uint64_t n0 = (uint64_t)nt * kTcN;
+        tc::mbar_wait(tfull(acc), aphase);
+        tc::fence_after();
+#pragma unroll 1
+        for (int c = 0; c < kTcN; c += 32) {
+          uint32_t v[32];
+          tc::tmem_ld32(tmem + (lb << 16) + (uint32_t)acc * kTcN + (uint32_t)c, v);
+          if (!valid || n0 + c >= p.nb) continue;
+          const uint64_t cb = n0 + c;
+          const uint64_t left = p.nb - cb;                 // > 0
+          if (MODE == kTcAndPopc) {
+            int32_t* o = p.out_i32 + r * p.nb + cb;
+            if (left >= 32 && ((reinterpret_cast<uintptr_t>(o) & 15u) == 0)) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                __stcs(reinterpret_cast<int4*>(o + j), make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if ((uint64_t)j < left) __stcs(o + j, (int32_t)v[j]);
+            }
+          } else {
+            const uint64_t plane = p.na * p.nb;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if ((uint64_t)j >= left) break;
+              const Est e = estimate_pair(pa, __ldg(p.pb + cb + j), (int)v[j], (int)p.N, L, m);
+              float* o = p.out_f32 + r * p.nb + cb + j;
+              if (m & 1u) { __stcs(o, __double2float_rn(e.ip)); o += plane; }
+              if (m & 2u) { __stcs(o, __double2float_rn(e.ham)); o += plane; }
+              if (m & 4u) { __stcs(o, __double2float_rn(e.js)); o += plane; }
+              if (m & 8u) { __stcs(o, __double2float_rn(e.cs)); }
+            }
+          }
+        }
+        tc::fence_before();
+        tc::mbar_arrive(tempty(acc));
+        if (++acc == 2) { acc = 0; aphase ^= 1u; }
+      }
     }
   }
   tc::fence_before();
@@ -274,28 +600,62 @@ EncodeTiled encoder() {
   return fn;
 }
 
-bool make_map(CUtensorMap* m, const uint8_t* ptr, uint64_t rows, uint32_t Kp, uint32_t box_rows) {
+bool make_map(CUtensorMap* m, const uint8_t* ptr, uint64_t rows, uint32_t Kp, uint32_t box_rows, uint32_t kc) {
   EncodeTiled enc = encoder();
   if (!enc) return false;
   const cuuint64_t dims[2] = {Kp, rows};
   const cuuint64_t strides[1] = {Kp};
-  const cuuint32_t box[2] = {(cuuint32_t)kTcK, box_rows};
+  const cuuint32_t box[2] = {kc, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(ptr), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             CU_TENSOR_MAP_INTERLEAVE_NONE, kc == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
 
 uint32_t tc_kpad(uint32_t N) { return ((N + 127) / 128) * 128; }
 
-cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* out, cudaStream_t s) {
+cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* out, cudaStream_t s,
+                          const int32_t* perm) {
   if (n == 0) return cudaSuccess;
   const uint32_t W = (N + 31) / 32, Kp = tc_kpad(N);
   const uint64_t total = n * (Kp / 32);
   const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, (uint64_t)num_sms() * 16);
-  expand_kernel<<<(unsigned)blocks, 256, 0, s>>>(sk, n, W, Kp, out);
+  expand_kernel<<<(unsigned)blocks, 256, 0, s>>>(sk, n, W, Kp, perm, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Shared launcher: pick ring depth from the shared memory left after `extra_bytes`, build
+// the TMA maps, size the work items (>= 2 per SM when the db can be split).
+template <int MODE, int KC>
+static cudaError_t tc_launch(const uint8_t* A8, const uint8_t* B8, TcParams& p, uint32_t N, uint32_t extra_bytes,
+                             uint32_t force_splits, cudaStream_t s) {
+  using G = TcGeom<KC>;
+  const uint32_t Kp = tc_kpad(N);
+  if (p.na > 0x7fffffffull || p.nb > 0x7fffffffull) return cudaErrorInvalidValue;
+  const uint32_t fixed = 1024 /* align */ + 1024 /* barriers */ + extra_bytes;
+  if (fixed + 2 * G::kStageBytes > kTcSmemMax) return cudaErrorInvalidConfiguration;
+  p.stages = std::min<uint32_t>(8, (kTcSmemMax - fixed) / G::kStageBytes);
+  alignas(64) CUtensorMap ma, mb;
+  if (!make_map(&ma, A8, p.na, Kp, kTcM, KC) || !make_map(&mb, B8, p.nb, Kp, kTcN, KC)) return cudaErrorNotSupported;
+  p.nk = Kp / KC;
+  p.tiles_n = (uint32_t)((p.nb + kTcN - 1) / kTcN);
+  const uint64_t mtiles = (p.na + kTcM - 1) / kTcM;
+  const uint64_t sms = (uint64_t)num_sms();
+  uint64_t want = (2 * sms + mtiles - 1) / mtiles;               // >= 2 items per SM
+  want = std::min<uint64_t>(want, p.tiles_n);
+  p.splits = force_splits ? force_splits : (uint32_t)std::max<uint64_t>(1, want);
+  p.per = (p.tiles_n + p.splits - 1) / p.splits;
+  p.splits = (p.tiles_n + p.per - 1) / p.per;                    // no empty splits
+  p.nitems = mtiles * p.splits;
+  const uint32_t smem = p.stages * G::kStageBytes + fixed;
+  cudaError_t e = cudaFuncSetAttribute(tc_pairs_kernel<MODE, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  uint64_t grid = std::min<uint64_t>(p.nitems, sms);
+  if (const char* g = std::getenv("BINSKETCH_TC_GRID")) grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, std::strtoull(g, nullptr, 10)));
+  tc_pairs_kernel<MODE, KC><<<(unsigned)grid, kTcThreads, smem, s>>>(ma, mb, p);
   count_launch();
   return cudaGetLastError();
 }
@@ -303,22 +663,73 @@ cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* o
 cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
                               int32_t* out, cudaStream_t s) {
   if (na == 0 || nb == 0) return cudaSuccess;
-  const uint32_t Kp = tc_kpad(N);
-  if (na > 0x7fffffffull || nb > 0x7fffffffull) return cudaErrorInvalidValue;
-  alignas(64) CUtensorMap ma, mb;
-  if (!make_map(&ma, A8, na, Kp, kTcM) || !make_map(&mb, B8, nb, Kp, kTcN)) return cudaErrorNotSupported;
-  TcParams p;
-  p.na = na; p.nb = nb; p.nk = Kp / kTcK;
-  p.tiles_n = (uint32_t)((nb + kTcN - 1) / kTcN);
-  p.ntiles = ((na + kTcM - 1) / kTcM) * (uint64_t)p.tiles_n;
-  p.out = out;
-  cudaError_t e = cudaFuncSetAttribute(tc_pairs_kernel<kAndPopc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+  TcParams p = {};
+  p.na = na; p.nb = nb; p.N = N; p.out_i32 = out;
+  return tc_launch<kTcAndPopc, 128>(A8, B8, p, N, 0, 0, s);
+}
+
+cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
+                               uint32_t measure, const int32_t* pa, const int32_t* pb, const double* L, float* out,
+                               cudaStream_t s) {
+  if (na == 0 || nb == 0) return cudaSuccess;
+  TcParams p = {};
+  p.na = na; p.nb = nb; p.N = N; p.measure = measure; p.pa = pa; p.pb = pb; p.L = L; p.out_f32 = out;
+  const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
+  p.l_smem = (lb <= 64 * 1024) ? lb : 0;
+  return tc_launch<kTcEstimate, 64>(A8, B8, p, N, p.l_smem, 0, s);
+}
+
+uint32_t tc_topk_max_k() { return 64; }
+
+uint32_t tc_topk_max_n() { return 6143; }   // cardinality table (N+1 doubles) staged in shared memory
+
+bool tc_sortable(uint32_t N) { return N <= 65536; }
+
+cudaError_t launch_sort_by_popcount(const int32_t* pb, uint64_t n, uint32_t N, uint32_t* bins, int32_t* perm,
+                                    int32_t* spb, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(bins, 0, (size_t)(N + 1) * 4, s);
   if (e != cudaSuccess) return e;
-  uint64_t grid = std::min<uint64_t>(p.ntiles, (uint64_t)num_sms());
-  if (const char* g = std::getenv("BINSKETCH_TC_GRID")) grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, std::strtoull(g, nullptr, 10)));
-  tc_pairs_kernel<kAndPopc><<<(unsigned)grid, kTcThreads, kTcSmem, s>>>(ma, mb, p);
-  count_launch();
+  const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms() * 8);
+  pb_hist_kernel<<<(unsigned)blocks, 256, 0, s>>>(pb, n, N, bins);
+  pb_scan_kernel<<<1, 1024, 0, s>>>(bins, N + 1);
+  pb_scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(pb, n, N, bins, perm, spb);
+  count_launch(3);
   return cudaGetLastError();
+}
+
+uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t k) {
+  // must match tc_launch's split rule for kTcTopk (workspace sizing)
+  if (nq == 0 || ndb == 0 || k == 0) return 1;
+  const uint64_t tiles_n = (ndb + kTcN - 1) / kTcN, mtiles = (nq + kTcM - 1) / kTcM, sms = 148;
+  uint64_t want = (2 * sms + mtiles - 1) / mtiles;
+  want = std::min<uint64_t>(want, std::min<uint64_t>(tiles_n, std::max<uint32_t>(1, 8192 / k)));
+  const uint64_t splits = std::max<uint64_t>(1, want);
+  const uint64_t per = (tiles_n + splits - 1) / splits;
+  return (uint32_t)((tiles_n + per - 1) / per);
+}
+
+cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
+                           uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* pd,
+                           const int32_t* perm, const double* L, bool prefilter, double* part_key, int32_t* part_idx,
+                           int32_t* out_idx, float* out_score, cudaStream_t s) {
+  if (nq == 0 || k == 0) return cudaSuccess;
+  if (k > tc_topk_max_k()) return cudaErrorInvalidValue;
+  TcParams p = {};
+  p.na = nq; p.nb = ndb; p.N = N; p.measure = measure; p.k = k; p.flags = flags; p.pa = pq; p.pb = pd; p.L = L;
+  p.perm = perm;
+  p.prefilter = (prefilter && perm) ? 1u : 0u;   // the per-tile bound needs the popcount-sorted db
+  p.part_key = part_key; p.part_idx = part_idx;
+  p.heap_smem = k * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 + 4 * 256 * 8 + 4 * 32 * 16;   // heaps, scratch, tile staging, queues, candidates
+  const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
+  if (lb > 48 * 1024) return cudaErrorInvalidValue;   // caller keeps N <= tc_topk_max_n()
+  p.l_topk_smem = lb;
+  // splits computed with the device-independent rule (148) so the workspace matches
+  const uint32_t splits = tc_topk_splits(nq, ndb, k);
+  cudaError_t e = tc_launch<kTcTopk, 64>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, splits, s);
+  if (e != cudaSuccess) return e;
+  if (p.splits != splits) return cudaErrorInvalidConfiguration;
+  return launch_topk_merge(nq, p.splits, k, measure, part_key, part_idx, out_idx, out_score, s);
 }
 
 }  // namespace bsk

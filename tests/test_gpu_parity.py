@@ -233,8 +233,15 @@ def test_andpopc_tc_saturated_and_empty_rows():
     assert got.max() == N
 
 
+@pytest.fixture(params=["tc", "cuda"])
+def engine(request, monkeypatch):
+    """Run a test on both pair engines: tensor-core (tcgen05 kind::i8) and CUDA-core (POPC)."""
+    monkeypatch.setenv("BINSKETCH_ENGINE", request.param)
+    return request.param
+
+
 # ------------------------------------------------------------ estimate -----
-def test_estimate_tiny_full_all_planes():
+def test_estimate_tiny_full_all_planes(engine):
     N, d = synth.TINY_N, synth.TINY.d
     A = _sketches(synth.TINY, N)
     Ad = dev(A.view(np.int32))
@@ -245,7 +252,7 @@ def test_estimate_tiny_full_all_planes():
 
 @pytest.mark.parametrize("N", synth.MEDIUM_NS)
 @pytest.mark.parametrize("measure", [15, 1, 2 | 8, 4])
-def test_estimate_medium_scaled(N, measure):
+def test_estimate_medium_scaled(N, measure, engine):
     A = _sketches(synth.scaled(synth.MEDIUM, 300, seed=91), N)
     B = _sketches(synth.scaled(synth.MEDIUM, 450, seed=92), N)
     B[:40] = A[:40]                         # identical pairs (self-similarity exactness)
@@ -270,7 +277,7 @@ def _check_topk(Q, D, N, d, measure, k, exclude_self=False):
 
 
 @pytest.mark.parametrize("measure", [1, 2, 4, 8])
-def test_topk_tiny(measure):
+def test_topk_tiny(measure, engine):
     N, d = synth.TINY_N, synth.TINY.d
     A = _sketches(synth.TINY, N)
     _check_topk(A, A, N, d, measure, 10)
@@ -278,7 +285,7 @@ def test_topk_tiny(measure):
 
 
 @pytest.mark.parametrize("measure", [4, 8])
-def test_topk_ranking_scaled_split_merge(measure):
+def test_topk_ranking_scaled_split_merge(measure, engine):
     # few queries, many db rows: exercises db splits + the merge kernel
     N, d = synth.RANKING_N, synth.RANKING_DB.d
     D = _sketches(synth.scaled(synth.RANKING_DB, 20_000), N)
@@ -287,7 +294,7 @@ def test_topk_ranking_scaled_split_merge(measure):
 
 
 @pytest.mark.parametrize("k", [1, 50, 64, 65, 100, 192, 193, 256])
-def test_topk_k_sizes_and_ties(k):
+def test_topk_k_sizes_and_ties(k, engine):
     N, d = 1024, 500_000
     D = _sketches(synth.scaled(synth.LARGE, 3000), N)
     D[100:110] = D[5]                    # exact ties: lower index first
@@ -297,7 +304,7 @@ def test_topk_k_sizes_and_ties(k):
     _check_topk(Q, D, N, d, 4, k)
 
 
-def test_topk_padding_and_empty_db():
+def test_topk_padding_and_empty_db(engine):
     N, d = 64, 1000
     D = _sketches(synth.CSRSpec(n=20, d=d, kind=0, p1=5, p2=20, cap=20, zipf_s=1.1, seed=3), N)
     _check_topk(D[:5], D, N, d, 2, 30)                       # k > ndb -> -1 / NaN padding
