@@ -14,7 +14,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbinsketch.so")
+LIB_PATH = os.environ.get("BINSKETCH_LIB_VARIANT") or os.path.join(_HERE, "libbinsketch.so")   # variant: dev A/B builds only
 
 IP, HAM, JS, COS = 1, 2, 4, 8
 MEASURES = {"ip": IP, "ham": HAM, "js": JS, "cos": COS}

@@ -47,13 +47,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         src = os.path.join(CSRC, unit)
         obj = os.path.join(OBJ, unit.replace(".cu", ".o"))
         objs.append(obj)
-        if force or _stale(obj, [src, __file__] + hdrs):
-            cmd = [NVCC, "-c", src, "-o", obj] + COMMON + extra
+        defines = os.environ.get("BSK_NVCC_DEFINES", "").split()   # dev-only instrumentation builds
+        if force or defines or _stale(obj, [src, __file__] + hdrs):
+            cmd = [NVCC, "-c", src, "-o", obj] + COMMON + extra + defines
             if verbose:
                 cmd += ["-Xptxas", "-v"]
                 print(" ".join(cmd), flush=True)
             subprocess.check_call(cmd)
-    if force or _stale(LIB, objs):
+    if force or os.environ.get("BSK_NVCC_DEFINES") or _stale(LIB, objs):
         cmd = [NVCC, "-shared", "-o", LIB] + objs + ARCH
         if verbose:
             print(" ".join(cmd), flush=True)

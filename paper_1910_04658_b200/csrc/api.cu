@@ -77,7 +77,8 @@ TableCache& cache() {
 }
 
 struct Layout {
-  size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, total = 0;
+  size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, qperm = 0, qspb = 0,
+         ctr = 0, total = 0;
   uint32_t splits = 1;
 };
 
@@ -94,6 +95,7 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
   Layout l;
   size_t off = 0;
   if (op == BINSKETCH_OP_ANDPOPC) {   // only the tensor-core engine needs scratch: expanded operands
+    l.ctr = off; off += kAlign;
     l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
     l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
     l.total = off;
@@ -104,6 +106,7 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
   l.pb = off; off += align_up((size_t)nb * 4);
   const bool tc = use_tc(op, N, k);
   if (tc) {
+    l.ctr = off; off += kAlign;
     l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
     l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
   }
@@ -111,6 +114,8 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
     l.bins = off; off += align_up((size_t)(N + 1) * 4);
     l.perm = off; off += align_up((size_t)nb * 4);
     l.spb = off; off += align_up((size_t)nb * 4);
+    l.qperm = off; off += align_up((size_t)na * 4);
+    l.qspb = off; off += align_up((size_t)na * 4);
   }
   if (op == BINSKETCH_OP_TOPK) {
     l.splits = tc ? bsk::tc_topk_splits(na, nb, k) : bsk::topk_splits(na, nb, k);
@@ -206,7 +211,8 @@ binsketch_status binsketch_andpopc(const uint32_t* A, uint64_t na, const uint32_
   uint8_t* b8 = static_cast<uint8_t*>(ws) + l.b8;
   cudaError_t e = bsk::launch_expand(A, na, N, a8, s);
   if (e == cudaSuccess) e = bsk::launch_expand(B, nb, N, b8, s);
-  if (e == cudaSuccess) e = bsk::launch_tc_andpopc(a8, na, b8, nb, N, out, s);
+  if (e == cudaSuccess)
+    e = bsk::launch_tc_andpopc(a8, na, b8, nb, N, out, reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + l.ctr), s);
   return cuda_status(e);
 }
 
@@ -236,7 +242,8 @@ binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, con
     e = bsk::launch_expand(sketches_a, na, N, a8, s);
     if (e == cudaSuccess && !self) e = bsk::launch_expand(sketches_b, nb, N, b8, s);
     if (e == cudaSuccess)
-      e = bsk::launch_tc_estimate(a8, na, b8, nb, N, measure, pa, pb, reinterpret_cast<const double*>(w + l.L), out, s);
+      e = bsk::launch_tc_estimate(a8, na, b8, nb, N, measure, pa, pb, reinterpret_cast<const double*>(w + l.L), out,
+                                  reinterpret_cast<unsigned long long*>(w + l.ctr), s);
     return cuda_status(e);
   }
   e = bsk::launch_pairs(bsk::kEstimate, sketches_a, na, sketches_b, nb, N, measure, pa, pb,
@@ -270,17 +277,25 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
     // db in popcount-descending order (tight per-tile prefilter), queries in their own order
     uint8_t* q8 = reinterpret_cast<uint8_t*>(w + l.a8);
     uint8_t* d8 = reinterpret_cast<uint8_t*>(w + l.b8);
+    // Queries stay in their own order by default: sorting them too (BINSKETCH_TC_QSORT=1) clusters
+    // the heavy rows (large |a_s|, many candidates) into a few straggler tiles; measured 2.5x slower.
     const bool sorted = bsk::tc_sortable(N);
     int32_t* perm = sorted ? reinterpret_cast<int32_t*>(w + l.perm) : nullptr;
     int32_t* spb = sorted ? reinterpret_cast<int32_t*>(w + l.spb) : pd;
-    if (sorted) e = bsk::launch_sort_by_popcount(pd, ndb, N, reinterpret_cast<uint32_t*>(w + l.bins), perm, spb, s);
-    if (e == cudaSuccess) e = bsk::launch_expand(queries, nq, N, q8, s);
+    const char* qs = std::getenv("BINSKETCH_TC_QSORT");   // dev A/B knob
+    const bool qsort = sorted && qs && !std::strcmp(qs, "1");
+    int32_t* qperm = qsort ? reinterpret_cast<int32_t*>(w + l.qperm) : nullptr;
+    int32_t* qspb = qsort ? reinterpret_cast<int32_t*>(w + l.qspb) : pq;
+    uint32_t* bins = reinterpret_cast<uint32_t*>(w + l.bins);
+    if (sorted) e = bsk::launch_sort_by_popcount(pd, ndb, N, bins, perm, spb, s);
+    if (qsort && e == cudaSuccess) e = bsk::launch_sort_by_popcount(pq, nq, N, bins, qperm, qspb, s);
+    if (e == cudaSuccess) e = bsk::launch_expand(queries, nq, N, q8, s, qperm);
     if (e == cudaSuccess) e = bsk::launch_expand(db, ndb, N, d8, s, perm);
     if (e == cudaSuccess)
-      e = bsk::launch_tc_topk(q8, nq, d8, ndb, N, measure, k, flags, pq, spb, perm,
+      e = bsk::launch_tc_topk(q8, nq, d8, ndb, N, measure, k, flags, qspb, qperm, spb, perm,
                               reinterpret_cast<const double*>(w + l.L), cache().convex(N, d),
                               reinterpret_cast<double*>(w + l.pkey), reinterpret_cast<int32_t*>(w + l.pidx), out_idx,
-                              out_score, s);
+                              out_score, reinterpret_cast<unsigned long long*>(w + l.ctr), s);
     return cuda_status(e);
   }
   e = bsk::launch_topk(queries, nq, db, ndb, N, measure, k, flags, pq, pd,

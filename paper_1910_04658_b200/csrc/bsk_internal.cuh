@@ -60,11 +60,12 @@ uint32_t tc_kpad(uint32_t N);
 // perm (optional): output row r is sketch perm[r].
 cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* out, cudaStream_t s,
                           const int32_t* perm = nullptr);
+// ctr: one 8-byte device word of workspace (dynamic tile scheduler; reset by the launcher).
 cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
-                              int32_t* out, cudaStream_t s);
+                              int32_t* out, unsigned long long* ctr, cudaStream_t s);
 cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
                                uint32_t measure, const int32_t* pa, const int32_t* pb, const double* L, float* out,
-                               cudaStream_t s);
+                               unsigned long long* ctr, cudaStream_t s);
 // Fused top-k on the tensor-core engine for k <= tc_topk_max_k(); partial lists
 // [nq][tc_topk_splits][k] in the workspace, then the merge kernel. `prefilter` enables
 // the integer L[pab] bound (valid when L is non-decreasing and convex).
@@ -76,10 +77,12 @@ uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t k);
 bool tc_sortable(uint32_t N);
 cudaError_t launch_sort_by_popcount(const int32_t* pb, uint64_t n, uint32_t N, uint32_t* bins, int32_t* perm,
                                     int32_t* spb, cudaStream_t s);
-// D8 rows in `perm` order (or db order when perm == nullptr), pd the matching popcounts.
+// Q8 rows in `qperm` order and D8 rows in `perm` order (nullptr: original order); pq / pd the
+// matching popcounts. Results land at the original query indices.
 cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
-                           uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* pd,
-                           const int32_t* perm, const double* L, bool prefilter, double* part_key, int32_t* part_idx,
-                           int32_t* out_idx, float* out_score, cudaStream_t s);
+                           uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* qperm,
+                           const int32_t* pd, const int32_t* perm, const double* L, bool prefilter, double* part_key,
+                           int32_t* part_idx, int32_t* out_idx, float* out_score, unsigned long long* ctr,
+                           cudaStream_t s);
 
 }  // namespace bsk

@@ -217,6 +217,8 @@ struct TcParams {
   uint32_t heap_smem;     // kTcTopk: per-row heaps + survivor scratch in shared memory (bytes)
   const int32_t* perm;    // kTcTopk: B row (sorted by |b_s| descending) -> original db index
   uint32_t l_topk_smem;   // kTcTopk: table staged after the heaps (bytes, 0 = global)
+  const int32_t* qperm;   // kTcTopk: A row (queries sorted by |a_s| descending) -> original query index
+  unsigned long long* item_ctr;   // dynamic work queue: next item (zeroed before the launch)
 };
 
 template <int MODE, int KC>
@@ -235,12 +237,18 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   auto tfull = [&](int a) { return bars + 8u * (2 * S + a); };
   auto tempty = [&](int a) { return bars + 8u * (2 * S + 2 + a); };
   const uint32_t tmem_slot = bars + 8u * (2 * S + 4);
+  // dynamic item schedule: the producer takes items from a global counter (heaviest query
+  // tiles first) and publishes them through a 4-slot ring read by the MMA and epilogue roles
+  auto ifull = [&](uint32_t k) { return bars + 8u * (2 * S + 5 + k); };
+  auto iempty = [&](uint32_t k) { return bars + 8u * (2 * S + 9 + k); };
+  const uint32_t iring = bars + 8u * (2 * S + 13);   // 4 x u64 item ids
   uint8_t* extra = smem + S * G::kStageBytes + 1024;        // estimator table or top-k heaps
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     for (uint32_t s = 0; s < S; ++s) { tc::mbar_init(full(s), 1); tc::mbar_init(empty(s), 1); }
     for (int a = 0; a < 2; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), 128); }
+    for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(ifull(k), 1); tc::mbar_init(iempty(k), 5); }   // MMA + 4 epilogue warps
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -259,6 +267,22 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   uint32_t tmem;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot));
 
+  auto publish_item = [&](uint32_t i) -> uint64_t {   // producer lane
+    const uint32_t k = i & 3u, ph = (i >> 2) & 1u;
+    tc::mbar_wait(iempty(k), ph ^ 1u);
+    const uint64_t it = atomicAdd(p.item_ctr, 1ull);
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(iring + 8u * k), "l"(it) : "memory");
+    tc::mbar_arrive(ifull(k));
+    return it;
+  };
+  auto take_item = [&](uint32_t i) -> uint64_t {      // one lane per consumer warp
+    const uint32_t k = i & 3u, ph = (i >> 2) & 1u;
+    tc::mbar_wait(ifull(k), ph);
+    uint64_t it;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(it) : "r"(iring + 8u * k) : "memory");
+    tc::mbar_arrive(iempty(k));
+    return it;
+  };
   // every role walks the same (item, n-tile) sequence
   auto item_range = [&](uint64_t it, uint64_t& mt, uint32_t& sp, uint32_t& nt0, uint32_t& nt1) {
     mt = it / p.splits;
@@ -270,7 +294,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (warp == 0) {
     if (lane == 0) {   // ---- TMA producer
       uint32_t stage = 0, phase = 0;
-      for (uint64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+      for (uint32_t ii = 0;; ++ii) {
+        const uint64_t it = publish_item(ii);
+        if (it >= p.nitems) break;
         uint64_t mt; uint32_t sp, nt0, nt1;
         item_range(it, mt, sp, nt0, nt1);
         for (uint32_t nt = nt0; nt < nt1; ++nt) {
@@ -289,7 +315,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (lane == 0) {   // ---- MMA issuer
       uint32_t stage = 0, phase = 0, aphase = 0;
       int acc = 0;
-      for (uint64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+      for (uint32_t ii = 0;; ++ii) {
+        const uint64_t it = take_item(ii);
+        if (it >= p.nitems) break;
         uint64_t mt; uint32_t sp, nt0, nt1;
         item_range(it, mt, sp, nt0, nt1);
         for (uint32_t nt = nt0; nt < nt1; ++nt) {
@@ -338,12 +366,17 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     auto hidx = [&](uint32_t i) -> int32_t& { return hi[i * kTcM + rt]; };
     uint32_t aphase = 0;
     int acc = 0;
-    for (uint64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+    for (uint32_t ii = 0;; ++ii) {
+      uint64_t it = 0;
+      if (lane == 0) it = take_item(ii);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= p.nitems) break;
       uint64_t mt; uint32_t sp, nt0, nt1;
       item_range(it, mt, sp, nt0, nt1);
-      const uint64_t r = mt * kTcM + rt;
+      const uint64_t r = mt * kTcM + rt;               // row of the (sorted) query matrix
       const bool valid = r < p.na;
       const int pa = valid ? __ldg(p.pa + r) : 0;
+      const uint64_t rq = (valid && p.qperm) ? (uint64_t)__ldg(p.qperm + r) : r;   // original query index
       const double La = Ls[pa];
       const bool filt = p.prefilter && pa > 0;
       uint32_t cnt = valid ? 0u : K, pmin = 0, pcur = 0;   // invalid rows count as full (never insert)
@@ -364,7 +397,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       };
       // offer (key, original db index) to this lane's row
       auto offer = [&](double key, int32_t orig) {
-        if ((p.flags & 1u) && (uint64_t)orig == r) return;
+        if ((p.flags & 1u) && (uint64_t)orig == rq) return;
         if (cnt < K) {
           hkey(cnt) = key; hidx(cnt) = orig;
           if (++cnt == K) {
@@ -510,8 +543,8 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (++acc == 2) { acc = 0; aphase ^= 1u; }
       }
       if (valid) {   // partial list of this (row, split), unsorted
-        double* ok = p.part_key + (r * p.splits + sp) * K;
-        int32_t* oi = p.part_idx + (r * p.splits + sp) * K;
+        double* ok = p.part_key + (rq * p.splits + sp) * K;
+        int32_t* oi = p.part_idx + (rq * p.splits + sp) * K;
         for (uint32_t i = 0; i < K; ++i) {
           ok[i] = i < cnt ? hkey(i) : -__longlong_as_double(0x7ff0000000000000LL);
           oi[i] = i < cnt ? hidx(i) : kSentinelIdx;
@@ -524,7 +557,11 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     uint32_t aphase = 0;
     int acc = 0;
     const uint32_t m = p.measure;
-    for (uint64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+    for (uint32_t ii = 0;; ++ii) {
+      uint64_t it = 0;
+      if (lane == 0) it = take_item(ii);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= p.nitems) break;
       uint64_t mt; uint32_t sp, nt0, nt1;
       item_range(it, mt, sp, nt0, nt1);
       const uint64_t r = mt * kTcM + rt;
@@ -653,6 +690,9 @@ static cudaError_t tc_launch(const uint8_t* A8, const uint8_t* B8, TcParams& p, 
   const uint32_t smem = p.stages * G::kStageBytes + fixed;
   cudaError_t e = cudaFuncSetAttribute(tc_pairs_kernel<MODE, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (!p.item_ctr) return cudaErrorInvalidValue;
+  e = cudaMemsetAsync(p.item_ctr, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
   uint64_t grid = std::min<uint64_t>(p.nitems, sms);
   if (const char* g = std::getenv("BINSKETCH_TC_GRID")) grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, std::strtoull(g, nullptr, 10)));
   tc_pairs_kernel<MODE, KC><<<(unsigned)grid, kTcThreads, smem, s>>>(ma, mb, p);
@@ -661,19 +701,20 @@ static cudaError_t tc_launch(const uint8_t* A8, const uint8_t* B8, TcParams& p, 
 }
 
 cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
-                              int32_t* out, cudaStream_t s) {
+                              int32_t* out, unsigned long long* ctr, cudaStream_t s) {
   if (na == 0 || nb == 0) return cudaSuccess;
   TcParams p = {};
-  p.na = na; p.nb = nb; p.N = N; p.out_i32 = out;
+  p.na = na; p.nb = nb; p.N = N; p.out_i32 = out; p.item_ctr = ctr;
   return tc_launch<kTcAndPopc, 128>(A8, B8, p, N, 0, 0, s);
 }
 
 cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
                                uint32_t measure, const int32_t* pa, const int32_t* pb, const double* L, float* out,
-                               cudaStream_t s) {
+                               unsigned long long* ctr, cudaStream_t s) {
   if (na == 0 || nb == 0) return cudaSuccess;
   TcParams p = {};
   p.na = na; p.nb = nb; p.N = N; p.measure = measure; p.pa = pa; p.pb = pb; p.L = L; p.out_f32 = out;
+  p.item_ctr = ctr;
   const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
   p.l_smem = (lb <= 64 * 1024) ? lb : 0;
   return tc_launch<kTcEstimate, 64>(A8, B8, p, N, p.l_smem, 0, s);
@@ -710,14 +751,15 @@ uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t k) {
 }
 
 cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
-                           uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* pd,
-                           const int32_t* perm, const double* L, bool prefilter, double* part_key, int32_t* part_idx,
-                           int32_t* out_idx, float* out_score, cudaStream_t s) {
+                           uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* qperm,
+                           const int32_t* pd, const int32_t* perm, const double* L, bool prefilter, double* part_key,
+                           int32_t* part_idx, int32_t* out_idx, float* out_score, unsigned long long* ctr,
+                           cudaStream_t s) {
   if (nq == 0 || k == 0) return cudaSuccess;
   if (k > tc_topk_max_k()) return cudaErrorInvalidValue;
   TcParams p = {};
   p.na = nq; p.nb = ndb; p.N = N; p.measure = measure; p.k = k; p.flags = flags; p.pa = pq; p.pb = pd; p.L = L;
-  p.perm = perm;
+  p.perm = perm; p.qperm = qperm; p.item_ctr = ctr;
   p.prefilter = (prefilter && perm) ? 1u : 0u;   // the per-tile bound needs the popcount-sorted db
   p.part_key = part_key; p.part_idx = part_idx;
   p.heap_smem = k * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 + 4 * 256 * 8 + 4 * 32 * 16;   // heaps, scratch, tile staging, queues, candidates
