@@ -131,6 +131,22 @@ def workload_spec(name):
     raise ValueError(name)
 
 
+def max_over_ranks(x: float, ws: int, device: str = "cuda") -> float:
+    """MAX of a per-rank scalar over the process group (plumbing only: NCCL on GPUs, gloo on CPU)."""
+    if ws <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_value(ws: int, units_per_rank_step: int, steps: int, t_max: float) -> float:
+    """Whole-job throughput: all ranks' units over the slowest rank's time (weak scaling)."""
+    return ws * units_per_rank_step * steps / t_max
+
+
 def rank_spec(spec, rank):
     import synth
     if rank == 0:
@@ -217,13 +233,9 @@ def run_ours(args):
         return sum(a.elapsed_time(b) for a, b in ev[name]) * 1e-3     # seconds over K steps
 
     t_step, t_build, t_topk = tot("step"), tot("build"), tot("topk")
-    t_max = t_step
-    if ws > 1:
-        tt = torch.tensor([t_step], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+    t_max = max_over_ranks(t_step, ws)
     pairs_per_step = nq * n                       # ordered pairs scored (self pair included in the count)
-    value = ws * pairs_per_step * args.steps / t_max
+    value = aggregate_value(ws, pairs_per_step, args.steps, t_max)
     clocks = clk.summary()
 
     # --- e2e: host (pinned) CSR -> build -> top-k -> host results, through the public API ---
@@ -248,11 +260,8 @@ def run_ours(args):
             b.record(stream)
             b.synchronize()
             tsum += a.elapsed_time(b) * 1e-3
-        if ws > 1:
-            tt = torch.tensor([tsum], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            tsum = float(tt.item())
-        e2e = {"value": ws * pairs_per_step * args.steps / tsum, "unit": "pairs/s",
+        tsum = max_over_ranks(tsum, ws)
+        e2e = {"value": aggregate_value(ws, pairs_per_step, args.steps, tsum), "unit": "pairs/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     # --- roofline of the dominant kernel ---
