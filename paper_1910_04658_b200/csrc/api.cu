@@ -78,7 +78,7 @@ TableCache& cache() {
 
 struct Layout {
   size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, qperm = 0, qspb = 0,
-         ctr = 0, total = 0;
+         ctr = 0, done = 0, total = 0;
   uint32_t splits = 1;
 };
 
@@ -118,7 +118,8 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
     l.qspb = off; off += align_up((size_t)na * 4);
   }
   if (op == BINSKETCH_OP_TOPK) {
-    l.splits = tc ? bsk::tc_topk_splits(na, nb, k) : bsk::topk_splits(na, nb, k);
+    l.splits = tc ? bsk::tc_topk_splits(na, nb, N, k) : bsk::topk_splits(na, nb, k);
+    if (tc) { l.done = off; off += align_up(((na + 127) / 128) * 4); }
     if (l.splits > 1 || tc) {
       l.pkey = off; off += align_up((size_t)na * l.splits * k * 8);
       l.pidx = off; off += align_up((size_t)na * l.splits * k * 4);
@@ -295,7 +296,8 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
       e = bsk::launch_tc_topk(q8, nq, d8, ndb, N, measure, k, flags, qspb, qperm, spb, perm,
                               reinterpret_cast<const double*>(w + l.L), cache().convex(N, d),
                               reinterpret_cast<double*>(w + l.pkey), reinterpret_cast<int32_t*>(w + l.pidx), out_idx,
-                              out_score, reinterpret_cast<unsigned long long*>(w + l.ctr), s);
+                              out_score, reinterpret_cast<unsigned long long*>(w + l.ctr),
+                              reinterpret_cast<unsigned int*>(w + l.done), s);
     return cuda_status(e);
   }
   e = bsk::launch_topk(queries, nq, db, ndb, N, measure, k, flags, pq, pd,

@@ -71,7 +71,7 @@ cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8
 // the integer L[pab] bound (valid when L is non-decreasing and convex).
 uint32_t tc_topk_max_k();
 uint32_t tc_topk_max_n();
-uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t k);
+uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t N, uint32_t k);   // partial lists per query
 // db order: counting sort by popcount, descending (perm: sorted position -> db row; spb:
 // sorted popcounts; bins: N+1 words of scratch). Needs N <= 65536 (tc_sortable).
 bool tc_sortable(uint32_t N);
@@ -83,6 +83,6 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
                            uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* qperm,
                            const int32_t* pd, const int32_t* perm, const double* L, bool prefilter, double* part_key,
                            int32_t* part_idx, int32_t* out_idx, float* out_score, unsigned long long* ctr,
-                           cudaStream_t s);
+                           unsigned int* done, cudaStream_t s);   // done: ceil(nq/128) words of workspace
 
 }  // namespace bsk

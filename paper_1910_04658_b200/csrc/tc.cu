@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -104,6 +105,30 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr)
+      : "memory");
+}
+
+// Split form for software pipelining: issue a load without waiting, and a wait that
+// names the destination registers as in/out operands (so no use is scheduled before it).
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+      : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+        "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]),
+        "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+        "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+      :
       : "memory");
 }
 
@@ -203,8 +228,10 @@ struct TcParams {
   uint32_t nk;            // K chunks per tile = Kp / KC
   uint32_t stages;        // ring depth
   uint32_t tiles_n;       // ceil(nb / 256)
-  uint32_t splits, per;   // work item = (m-tile, split); split s covers n-tiles [s*per, s*per + per)
-  uint64_t nitems;
+  uint32_t splits, per;   // work item = (db chunk s, m-tile); chunk s covers n-tiles [s*per, s*per + per)
+  uint64_t mtiles, nitems;
+  uint32_t chain;         // kTcTopk: heaps persist across chunks in part_key/idx (one list per row)
+  unsigned int* done;     // kTcTopk chained: per m-tile count of finished (chunk, epilogue warp) pairs
   int32_t* out_i32;       // kTcAndPopc: int32 [na][nb]
   float* out_f32;         // kTcEstimate: float [popcount(measure)][na][nb]
   uint32_t measure, N, k, flags, prefilter;
@@ -217,6 +244,7 @@ struct TcParams {
   uint32_t heap_smem;     // kTcTopk: per-row heaps + survivor scratch in shared memory (bytes)
   const int32_t* perm;    // kTcTopk: B row (sorted by |b_s| descending) -> original db index
   uint32_t l_topk_smem;   // kTcTopk: table staged after the heaps (bytes, 0 = global)
+  double lc;              // log1p(-1/N): closed-form inverse of the table for the tile bound
   const int32_t* qperm;   // kTcTopk: A row (queries sorted by |a_s| descending) -> original query index
   unsigned long long* item_ctr;   // dynamic work queue: next item (zeroed before the launch)
 };
@@ -284,9 +312,11 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     return it;
   };
   // every role walks the same (item, n-tile) sequence
+  // items are chunk-major: all query tiles against db chunk 0, then chunk 1, ... so the
+  // chunk's B operand (sized to stay L2-resident) is fetched from HBM about once
   auto item_range = [&](uint64_t it, uint64_t& mt, uint32_t& sp, uint32_t& nt0, uint32_t& nt1) {
-    mt = it / p.splits;
-    sp = (uint32_t)(it - mt * p.splits);
+    sp = (uint32_t)(it / p.mtiles);
+    mt = it - (uint64_t)sp * p.mtiles;
     nt0 = sp * p.per;
     nt1 = min(nt0 + p.per, p.tiles_n);
   };
@@ -379,9 +409,30 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const uint64_t rq = (valid && p.qperm) ? (uint64_t)__ldg(p.qperm + r) : r;   // original query index
       const double La = Ls[pa];
       const bool filt = p.prefilter && pa > 0;
-      uint32_t cnt = valid ? 0u : K, pmin = 0, pcur = 0;   // invalid rows count as full (never insert)
+      uint32_t cnt = valid ? 0u : K, pmin = 0;   // invalid rows count as full (never insert)
       double T = -__longlong_as_double(0x7ff0000000000000LL);
       int32_t Ti = kSentinelIdx;
+      if (p.chain && sp > 0) {
+        // resume this row's heap from the previous chunk (chunk order per query tile is
+        // enforced by the done counters: 4 epilogue warps finish each chunk)
+        if (lane == 0) {
+          const unsigned int need = 4u * sp;
+          unsigned int v;
+          do { asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.done + mt) : "memory"); } while (v < need);
+        }
+        __syncwarp();
+        if (valid) {
+          const double* ik = p.part_key + rq * K;
+          const int32_t* ii = p.part_idx + rq * K;
+          cnt = 0;
+          for (uint32_t i = 0; i < K; ++i) {
+            const int32_t id = __ldcg(ii + i);
+            hkey(i) = __ldcg(ik + i); hidx(i) = id;
+            cnt += id != kSentinelIdx ? 1u : 0u;
+          }
+          if (cnt == K) { T = hkey(0); Ti = hidx(0); }
+        }
+      }
       auto sift_down = [&](uint32_t i) {
         for (;;) {
           const uint32_t l = 2 * i + 1, rr = l + 1;
@@ -427,21 +478,26 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         return fmin(2.0 * u - La - Llo, 0.0);
       };
       // smallest pab whose bound reaches the current threshold (slack for fp64 rounding)
+      // smallest pab whose bound reaches the current threshold g (slack for fp64 rounding):
+      // closed-form start from the inverse of L(p) = log1p(-p/N)/log1p(-1/N) with a 2-step
+      // low margin, then exact refinement on the staged table (typically 1-3 evaluations)
       auto tile_pmin = [&](uint32_t lo, uint32_t hi_) -> uint32_t {
         if (!filt || cnt < K || lo == 0) return 0u;
         const double g = T - 1e-9 * fmax(1.0, fabs(T));
         const uint32_t pmax = min((uint32_t)pa, hi_);
-        if (key_bound(pmax, lo, hi_) < g) return pmax + 1;          // no pair of the tile can enter
-        uint32_t qq = min(pcur, pmax);
-        int steps = 0;
-        while (qq > 0 && steps < 8 && key_bound(qq - 1, lo, hi_) >= g) { --qq; ++steps; }
-        while (qq < pmax && steps < 8 && key_bound(qq, lo, hi_) < g) { ++qq; ++steps; }
-        if (steps == 8) {                                           // far move: bisect
-          uint32_t a0 = 0, b0 = pmax;
-          while (a0 < b0) { const uint32_t mid = (a0 + b0) / 2; if (key_bound(mid, lo, hi_) >= g) b0 = mid; else a0 = mid + 1; }
-          qq = a0;
-        }
-        pcur = qq;
+        const double Llo = Ls[lo];
+        double t;   // U(pab) >= t  <=>  key bound >= g
+        if (m == 1u) t = g;
+        else if (m == 4u) t = g > -1.0 ? g * (La + Llo) / (1.0 + g) : -1.0;
+        else if (m == 8u) t = g * sqrt(La * Llo);
+        else t = 0.5 * (g + La + Llo);
+        if (t <= 0.0) return 0u;
+        if (fmin(La, Ls[hi_]) < t) return pmax + 1;               // no pair of the tile can enter
+        const double pr = -(double)p.N * expm1((La + Llo - t) * p.lc);
+        const double q0 = (double)pa + (double)lo - fmin(floor(pr) + 2.0, (double)p.N);
+        uint32_t qq = q0 <= 0.0 ? 0u : min((uint32_t)q0, pmax);
+        while (qq > 0 && key_bound(qq - 1, lo, hi_) >= g) --qq;     // (margin makes this rare)
+        while (qq <= pmax && key_bound(qq, lo, hi_) < g) ++qq;
         return qq;
       };
       // per-tile staging of the db popcounts / original indices (8 columns per lane),
@@ -469,17 +525,15 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const bool direct = __any_sync(0xffffffffu, cnt < K);
         tc::mbar_wait(tfull(acc), aphase);
         tc::fence_after();
-#pragma unroll 1
-        for (uint32_t c = 0; c < (uint32_t)kTcN; c += 32) {
-          uint32_t v[32];
-          tc::tmem_ld32(tmem + (lb << 16) + (uint32_t)acc * kTcN + c, v);
-          if (c >= nval) continue;
+        // one 32-column chunk (values v): prefilter, then survivors
+        auto chunk = [&](const uint32_t c, uint32_t (&v)[32]) {
+          if (c >= nval) return;
           const uint32_t left = nval - c;
           uint32_t mx = 0;
 #pragma unroll
           for (int j = 0; j < 32; ++j) mx = max(mx, v[j]);
           const bool pass = valid && mx >= pmin;
-          if (!__any_sync(0xffffffffu, pass)) continue;
+          if (!__any_sync(0xffffffffu, pass)) return;
           // survivor mask of this lane
           uint32_t sm = 0;
 #pragma unroll
@@ -503,7 +557,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               }
             }
             __syncwarp();
-            continue;
+            return;
           }
           // queue: (column in tile, owner lane << 24 | pab)
 #pragma unroll
@@ -537,18 +591,38 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
           }
           __syncwarp();
+                };
+        // TMEM loads software-pipelined: chunk c+1 is in flight while chunk c is tested
+        const uint32_t tb = tmem + (lb << 16) + (uint32_t)acc * kTcN;
+        uint32_t va[32], vb[32];
+        tc::tmem_ld32_issue(tb, va);
+        tc::tmem_ld_wait(va);
+#pragma unroll 1
+        for (uint32_t c = 0; c < (uint32_t)kTcN; c += 64) {
+          tc::tmem_ld32_issue(tb + c + 32, vb);
+          chunk(c, va);
+          tc::tmem_ld_wait(vb);
+          if (c + 64 < (uint32_t)kTcN) tc::tmem_ld32_issue(tb + c + 64, va);
+          chunk(c + 32, vb);
+          if (c + 64 < (uint32_t)kTcN) tc::tmem_ld_wait(va);
         }
         tc::fence_before();
         tc::mbar_arrive(tempty(acc));
         if (++acc == 2) { acc = 0; aphase ^= 1u; }
       }
-      if (valid) {   // partial list of this (row, split), unsorted
-        double* ok = p.part_key + (rq * p.splits + sp) * K;
-        int32_t* oi = p.part_idx + (rq * p.splits + sp) * K;
+      if (valid) {   // partial list of this (row, chunk) — or the row's running heap when chained
+        const uint64_t slot = p.chain ? rq : rq * p.splits + sp;
+        double* ok = p.part_key + slot * K;
+        int32_t* oi = p.part_idx + slot * K;
         for (uint32_t i = 0; i < K; ++i) {
-          ok[i] = i < cnt ? hkey(i) : -__longlong_as_double(0x7ff0000000000000LL);
-          oi[i] = i < cnt ? hidx(i) : kSentinelIdx;
+          __stcg(ok + i, i < cnt ? hkey(i) : -__longlong_as_double(0x7ff0000000000000LL));
+          __stcg(oi + i, i < cnt ? hidx(i) : kSentinelIdx);
         }
+      }
+      if (p.chain) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.done + mt, 1u);
       }
     }
   } else {             // ---- andpopc / estimate epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
@@ -664,6 +738,27 @@ cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* o
   return cudaGetLastError();
 }
 
+// Work decomposition (device independent, so workspace sizes are pure functions):
+// db chunks of <= ~40 MB of widened operand (L2-resident while every query tile visits
+// them), and at least ~2 items per SM. Top-k chains its per-row heaps through the chunks
+// when there are enough query tiles to keep every SM busy; otherwise it uses independent
+// per-chunk partial lists merged afterwards.
+struct TcSplit { uint32_t splits, chain; };
+static TcSplit tc_split_rule(uint64_t na, uint64_t nb, uint32_t N, bool topk, uint32_t k = 0) {
+  const uint64_t tiles_n = (nb + kTcN - 1) / kTcN, mtiles = (na + kTcM - 1) / kTcM, sms = 148;
+  const uint64_t chunk_bytes = 40ull << 20;
+  uint64_t s_l2 = (nb * tc_kpad(N) + chunk_bytes - 1) / chunk_bytes;
+  uint64_t s_par = (2 * sms + mtiles - 1) / mtiles;
+  TcSplit r;
+  r.chain = (topk && mtiles >= 2 * sms) ? 1u : 0u;
+  uint64_t splits = r.chain ? s_l2 : std::max(s_l2, s_par);
+  if (topk && !r.chain && k) splits = std::min<uint64_t>(splits, std::max<uint32_t>(1, 8192 / k));   // merge capacity
+  splits = std::max<uint64_t>(1, std::min<uint64_t>(splits, tiles_n));
+  const uint64_t per = (tiles_n + splits - 1) / splits;
+  r.splits = (uint32_t)((tiles_n + per - 1) / per);
+  return r;
+}
+
 // Shared launcher: pick ring depth from the shared memory left after `extra_bytes`, build
 // the TMA maps, size the work items (>= 2 per SM when the db can be split).
 template <int MODE, int KC>
@@ -677,18 +772,29 @@ static cudaError_t tc_launch(const uint8_t* A8, const uint8_t* B8, TcParams& p, 
   p.stages = std::min<uint32_t>(8, (kTcSmemMax - fixed) / G::kStageBytes);
   alignas(64) CUtensorMap ma, mb;
   if (!make_map(&ma, A8, p.na, Kp, kTcM, KC) || !make_map(&mb, B8, p.nb, Kp, kTcN, KC)) return cudaErrorNotSupported;
+  cudaError_t e = cudaSuccess;
   p.nk = Kp / KC;
   p.tiles_n = (uint32_t)((p.nb + kTcN - 1) / kTcN);
   const uint64_t mtiles = (p.na + kTcM - 1) / kTcM;
   const uint64_t sms = (uint64_t)num_sms();
-  uint64_t want = (2 * sms + mtiles - 1) / mtiles;               // >= 2 items per SM
-  want = std::min<uint64_t>(want, p.tiles_n);
-  p.splits = force_splits ? force_splits : (uint32_t)std::max<uint64_t>(1, want);
+  if (force_splits) {
+    p.splits = force_splits;
+  } else {
+    const TcSplit sc = tc_split_rule(p.na, p.nb, N, MODE == kTcTopk);
+    p.splits = sc.splits;
+    p.chain = sc.chain;
+  }
   p.per = (p.tiles_n + p.splits - 1) / p.splits;
   p.splits = (p.tiles_n + p.per - 1) / p.per;                    // no empty splits
+  p.mtiles = mtiles;
   p.nitems = mtiles * p.splits;
+  if (p.chain && !p.done) return cudaErrorInvalidValue;
+  if (p.chain) {
+    e = cudaMemsetAsync(p.done, 0, mtiles * sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+  }
   const uint32_t smem = p.stages * G::kStageBytes + fixed;
-  cudaError_t e = cudaFuncSetAttribute(tc_pairs_kernel<MODE, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = cudaFuncSetAttribute(tc_pairs_kernel<MODE, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (!p.item_ctr) return cudaErrorInvalidValue;
   e = cudaMemsetAsync(p.item_ctr, 0, sizeof(unsigned long long), s);
@@ -739,27 +845,24 @@ cudaError_t launch_sort_by_popcount(const int32_t* pb, uint64_t n, uint32_t N, u
   return cudaGetLastError();
 }
 
-uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t k) {
-  // must match tc_launch's split rule for kTcTopk (workspace sizing)
+uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t N, uint32_t k) {
+  // partial lists per query in the workspace: 1 when the heaps are chained, else one per chunk
   if (nq == 0 || ndb == 0 || k == 0) return 1;
-  const uint64_t tiles_n = (ndb + kTcN - 1) / kTcN, mtiles = (nq + kTcM - 1) / kTcM, sms = 148;
-  uint64_t want = (2 * sms + mtiles - 1) / mtiles;
-  want = std::min<uint64_t>(want, std::min<uint64_t>(tiles_n, std::max<uint32_t>(1, 8192 / k)));
-  const uint64_t splits = std::max<uint64_t>(1, want);
-  const uint64_t per = (tiles_n + splits - 1) / splits;
-  return (uint32_t)((tiles_n + per - 1) / per);
+  const TcSplit r = tc_split_rule(nq, ndb, N, true, k);
+  return r.chain ? 1u : r.splits;
 }
 
 cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
                            uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* qperm,
                            const int32_t* pd, const int32_t* perm, const double* L, bool prefilter, double* part_key,
                            int32_t* part_idx, int32_t* out_idx, float* out_score, unsigned long long* ctr,
-                           cudaStream_t s) {
+                           unsigned int* done, cudaStream_t s) {
   if (nq == 0 || k == 0) return cudaSuccess;
   if (k > tc_topk_max_k()) return cudaErrorInvalidValue;
   TcParams p = {};
   p.na = nq; p.nb = ndb; p.N = N; p.measure = measure; p.k = k; p.flags = flags; p.pa = pq; p.pb = pd; p.L = L;
   p.perm = perm; p.qperm = qperm; p.item_ctr = ctr;
+  p.lc = std::log1p(-1.0 / (double)N);
   p.prefilter = (prefilter && perm) ? 1u : 0u;   // the per-tile bound needs the popcount-sorted db
   p.part_key = part_key; p.part_idx = part_idx;
   p.heap_smem = k * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 + 4 * 256 * 8 + 4 * 32 * 16;   // heaps, scratch, tile staging, queues, candidates
@@ -767,11 +870,14 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
   if (lb > 48 * 1024) return cudaErrorInvalidValue;   // caller keeps N <= tc_topk_max_n()
   p.l_topk_smem = lb;
   // splits computed with the device-independent rule (148) so the workspace matches
-  const uint32_t splits = tc_topk_splits(nq, ndb, k);
-  cudaError_t e = tc_launch<kTcTopk, 64>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, splits, s);
+  const TcSplit sc = tc_split_rule(nq, ndb, N, true, k);
+  p.chain = sc.chain;
+  p.done = done;
+  cudaError_t e = tc_launch<kTcTopk, 64>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, sc.splits, s);
   if (e != cudaSuccess) return e;
-  if (p.splits != splits) return cudaErrorInvalidConfiguration;
-  return launch_topk_merge(nq, p.splits, k, measure, part_key, part_idx, out_idx, out_score, s);
+  const uint32_t lists = p.chain ? 1u : p.splits;
+  if (lists != tc_topk_splits(nq, ndb, N, k)) return cudaErrorInvalidConfiguration;
+  return launch_topk_merge(nq, lists, k, measure, part_key, part_idx, out_idx, out_score, s);
 }
 
 }  // namespace bsk
