@@ -78,17 +78,27 @@ TableCache& cache() {
 
 struct Layout {
   size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, qperm = 0, qspb = 0,
-         ctr = 0, done = 0, total = 0;
+         ctr = 0, done = 0, pab = 0, total = 0;
   uint32_t splits = 1;
 };
 
 // Pair engine: tensor cores (tcgen05 kind::i8 on {0,1}-byte operands, tc.cu) or CUDA
 // cores (LOP3 + POPC, pairs.cu). BINSKETCH_ENGINE=cuda|tc overrides (A/B measurement).
-bool use_tc(int op, uint32_t N, uint32_t k = 0) {
+bool engine_cuda() {
   const char* e = std::getenv("BINSKETCH_ENGINE");
-  if (e && !std::strcmp(e, "cuda")) return false;
+  return e && !std::strcmp(e, "cuda");
+}
+bool use_tc(int op, uint32_t N, uint32_t k = 0) {
+  if (engine_cuda()) return false;
   if (op == BINSKETCH_OP_TOPK) return k <= bsk::tc_topk_max_k() && N <= bsk::tc_topk_max_n();
   return true;
+}
+// Top-k beyond the fused kernel's limits (k > 64 or N > 6143): tensor-core AND-popcount into a
+// workspace table pab[nq][ndb], then the CUDA-core threshold top-k reading it — when the table
+// fits the budget; otherwise the CUDA-core kernels end to end.
+constexpr size_t kPabBudget = size_t(4) << 30;
+bool use_tc_pab(uint32_t N, uint64_t nq, uint64_t ndb, uint32_t k) {
+  return !engine_cuda() && !use_tc(BINSKETCH_OP_TOPK, N, k) && nq * ndb * 4 <= kPabBudget;
 }
 
 Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
@@ -105,6 +115,13 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
   l.pa = off; off += align_up((size_t)na * 4);
   l.pb = off; off += align_up((size_t)nb * 4);
   const bool tc = use_tc(op, N, k);
+  const bool tcp = op == BINSKETCH_OP_TOPK && use_tc_pab(N, na, nb, k);
+  if (tcp) {
+    l.ctr = off; off += kAlign;
+    l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
+    l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
+    l.pab = off; off += align_up((size_t)na * nb * 4);
+  }
   if (tc) {
     l.ctr = off; off += kAlign;
     l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
@@ -300,10 +317,23 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
                               reinterpret_cast<unsigned int*>(w + l.done), s);
     return cuda_status(e);
   }
+  const int32_t* pab = nullptr;
+  if (ndb > 0 && use_tc_pab(N, nq, ndb, k)) {
+    uint8_t* q8 = reinterpret_cast<uint8_t*>(w + l.a8);
+    uint8_t* d8 = self ? q8 : reinterpret_cast<uint8_t*>(w + l.b8);
+    int32_t* pabw = reinterpret_cast<int32_t*>(w + l.pab);
+    e = bsk::launch_expand(queries, nq, N, q8, s);
+    if (e == cudaSuccess && !self) e = bsk::launch_expand(db, ndb, N, d8, s);
+    if (e == cudaSuccess)
+      e = bsk::launch_tc_andpopc(q8, nq, d8, ndb, N, pabw, reinterpret_cast<unsigned long long*>(w + l.ctr), s);
+    if (e != cudaSuccess) return cuda_status(e);
+    pab = pabw;
+  }
   e = bsk::launch_topk(queries, nq, db, ndb, N, measure, k, flags, pq, pd,
                          reinterpret_cast<const double*>(w + l.L),
                          l.splits > 1 ? reinterpret_cast<double*>(w + l.pkey) : nullptr,
-                         l.splits > 1 ? reinterpret_cast<int32_t*>(w + l.pidx) : nullptr, out_idx, out_score, s);
+                         l.splits > 1 ? reinterpret_cast<int32_t*>(w + l.pidx) : nullptr, out_idx, out_score, s,
+                         pab);
   return cuda_status(e);
 }
 

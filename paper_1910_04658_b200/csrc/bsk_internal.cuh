@@ -52,7 +52,8 @@ cudaError_t launch_topk_merge(uint64_t nq, uint32_t splits, uint32_t k, uint32_t
 cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint64_t ndb, uint32_t N,
                         uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq,
                         const int32_t* pd, const double* L, double* part_key, int32_t* part_idx,
-                        int32_t* out_idx, float* out_score, cudaStream_t s);
+                        int32_t* out_idx, float* out_score, cudaStream_t s,
+                        const int32_t* pab = nullptr);   // pab[nq][ndb] precomputed (tensor cores) or null
 
 // Tensor-core pair engine (tc.cu): sketches widened to {0,1} bytes, rows padded to
 // tc_kpad(N) bytes (multiple of 128), then tcgen05 kind::i8 all-pairs.

@@ -203,13 +203,15 @@ struct TopkCfg {
   using C = TileCfg<TQ, kTBN, TM, TN, kTKC>;
 };
 
-template <int TQ, int CAP>
+// FROMPAB: the AND-popcounts come precomputed (pab[nq][ndb], from the tensor-core engine)
+// instead of the LOP3+POPC mainloop.
+template <int TQ, int CAP, bool FROMPAB>
 __global__ void __launch_bounds__(256)
 topk_kernel(const uint32_t* __restrict__ Q, uint64_t nq, const uint32_t* __restrict__ D, uint64_t ndb,
             uint32_t N, uint32_t measure, uint32_t k, uint32_t flags, const int32_t* __restrict__ pq,
             const int32_t* __restrict__ pd, const double* __restrict__ Lg, uint32_t splits,
             double* __restrict__ part_key, int32_t* __restrict__ part_idx, int32_t* __restrict__ out_idx,
-            float* __restrict__ out_score) {
+            float* __restrict__ out_score, const int32_t* __restrict__ pab) {
   using Cfg = TopkCfg<TQ, CAP>;
   using C = typename Cfg::C;
   constexpr int TM = Cfg::TM, TN = Cfg::TN;
@@ -258,7 +260,19 @@ topk_kernel(const uint32_t* __restrict__ Q, uint64_t nq, const uint32_t* __restr
 
   for (uint64_t n0 = c_begin; n0 < c_end; n0 += kTBN) {
     uint32_t acc[TM][TN];
-    mainloop<TQ, kTBN, TM, TN, kTKC>(Q, nq, q0, D, c_end, n0, W, As, Bs, acc);
+    if (FROMPAB) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const uint64_t r = q0 + ty + i * C::kThreadsY;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const uint64_t c = n0 + tx + j * C::kThreadsX;
+          acc[i][j] = (r < nq && c < c_end) ? (uint32_t)__ldcs(pab + r * ndb + c) : 0u;
+        }
+      }
+    } else {
+      mainloop<TQ, kTBN, TM, TN, kTKC>(Q, nq, q0, D, c_end, n0, W, As, Bs, acc);
+    }
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
       const int ql = ty + i * C::kThreadsY;
@@ -365,34 +379,47 @@ uint32_t topk_splits(uint64_t nq, uint64_t ndb, uint32_t k) {
   return (uint32_t)std::max<uint64_t>(1, s);
 }
 
-template <int TQ, int CAP>
-static cudaError_t launch_topk_t(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint64_t ndb, uint32_t N,
-                                 uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq,
-                                 const int32_t* pd, const double* L, uint32_t splits, double* part_key,
-                                 int32_t* part_idx, int32_t* out_idx, float* out_score, cudaStream_t s) {
+template <int TQ, int CAP, bool FROMPAB>
+static cudaError_t launch_topk_t2(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint64_t ndb, uint32_t N,
+                                  uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq,
+                                  const int32_t* pd, const double* L, uint32_t splits, double* part_key,
+                                  int32_t* part_idx, int32_t* out_idx, float* out_score, const int32_t* pab,
+                                  cudaStream_t s) {
   using C = typename TopkCfg<TQ, CAP>::C;
   const bool l_in_smem = N + 1 <= kMaxSmemL;
   const size_t smem = (size_t)TQ * CAP * 8 + TQ * 8 + (l_in_smem ? ((N + 2) & ~1u) * 8 : 0) +
                       (size_t)TQ * CAP * 4 + TQ * 4 * 2 + 16 + C::kSmemWords * 4;
-  cudaError_t e = cudaFuncSetAttribute(topk_kernel<TQ, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(topk_kernel<TQ, CAP, FROMPAB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((nq + TQ - 1) / TQ), splits);
-  topk_kernel<TQ, CAP><<<grid, 256, smem, s>>>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits,
-                                                part_key, part_idx, out_idx, out_score);
+  topk_kernel<TQ, CAP, FROMPAB><<<grid, 256, smem, s>>>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits,
+                                                         part_key, part_idx, out_idx, out_score, pab);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int TQ, int CAP>
+static cudaError_t launch_topk_t(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint64_t ndb, uint32_t N,
+                                 uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq,
+                                 const int32_t* pd, const double* L, uint32_t splits, double* part_key,
+                                 int32_t* part_idx, int32_t* out_idx, float* out_score, const int32_t* pab,
+                                 cudaStream_t s) {
+  return pab ? launch_topk_t2<TQ, CAP, true>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key,
+                                             part_idx, out_idx, out_score, pab, s)
+             : launch_topk_t2<TQ, CAP, false>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key,
+                                              part_idx, out_idx, out_score, pab, s);
 }
 
 cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint64_t ndb, uint32_t N,
                         uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* pd,
                         const double* L, double* part_key, int32_t* part_idx, int32_t* out_idx,
-                        float* out_score, cudaStream_t s) {
+                        float* out_score, cudaStream_t s, const int32_t* pab) {
   if (nq == 0 || k == 0) return cudaSuccess;
   const uint32_t splits = topk_splits(nq, ndb, k);
   cudaError_t e;
-  if (k <= 128 - kTBN)       e = launch_topk_t<32, 128>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, s);
-  else if (k <= 256 - kTBN)  e = launch_topk_t<16, 256>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, s);
-  else                       e = launch_topk_t<16, 512>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, s);
+  if (k <= 128 - kTBN)       e = launch_topk_t<32, 128>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, pab, s);
+  else if (k <= 256 - kTBN)  e = launch_topk_t<16, 256>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, pab, s);
+  else                       e = launch_topk_t<16, 512>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, pab, s);
   if (e != cudaSuccess || splits == 1) return e;
   return launch_topk_merge(nq, splits, k, measure, part_key, part_idx, out_idx, out_score, s);
 }

@@ -481,8 +481,11 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       // smallest pab whose bound reaches the current threshold g (slack for fp64 rounding):
       // closed-form start from the inverse of L(p) = log1p(-p/N)/log1p(-1/N) with a 2-step
       // low margin, then exact refinement on the staged table (typically 1-3 evaluations)
+      uint32_t c_lo = 0xFFFFFFFFu, c_hi = 0, c_pmin = 0;   // last (lo, hi, T) -> pmin
+      double c_T = 0.0;
       auto tile_pmin = [&](uint32_t lo, uint32_t hi_) -> uint32_t {
         if (!filt || cnt < K || lo == 0) return 0u;
+        if (lo == c_lo && hi_ == c_hi && T == c_T) return c_pmin;   // sorted db: runs of equal ranges
         const double g = T - 1e-9 * fmax(1.0, fabs(T));
         const uint32_t pmax = min((uint32_t)pa, hi_);
         const double Llo = Ls[lo];
@@ -493,11 +496,14 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         else t = 0.5 * (g + La + Llo);
         if (t <= 0.0) return 0u;
         if (fmin(La, Ls[hi_]) < t) return pmax + 1;               // no pair of the tile can enter
-        const double pr = -(double)p.N * expm1((La + Llo - t) * p.lc);
-        const double q0 = (double)pa + (double)lo - fmin(floor(pr) + 2.0, (double)p.N);
-        uint32_t qq = q0 <= 0.0 ? 0u : min((uint32_t)q0, pmax);
+        // fp32 start (hardware exp); its error is far below the 2-step margin, and the
+        // result is made exact by the table refinement below
+        const float pr = -(float)p.N * expm1f((float)((La + Llo - t) * p.lc));
+        const float q0 = (float)pa + (float)lo - fminf(floorf(pr) + 2.0f, (float)p.N);
+        uint32_t qq = q0 <= 0.0f ? 0u : min((uint32_t)q0, pmax);
         while (qq > 0 && key_bound(qq - 1, lo, hi_) >= g) --qq;     // (margin makes this rare)
         while (qq <= pmax && key_bound(qq, lo, hi_) < g) ++qq;
+        c_lo = lo; c_hi = hi_; c_T = T; c_pmin = qq;
         return qq;
       };
       // per-tile staging of the db popcounts / original indices (8 columns per lane),
