@@ -54,6 +54,10 @@ def _lib_():
         L.orc_topk.argtypes = [vp, u64, vp, u64, u32, u64, u32, u32, u32, vp, vp, ctypes.c_int]
         L.orc_topk.restype = None
         L.orc_exact.argtypes = [vp, i64, vp, i64, vp]; L.orc_exact.restype = None
+        L.orc_join.argtypes = [vp, u64, vp, u64, u32, u64, u32, vp, u32, u32, vp]
+        L.orc_join.restype = None
+        L.orc_join_exact.argtypes = [vp, vp, u64, vp, vp, u64, u32, vp, u32, u32, vp]
+        L.orc_join_exact.restype = None
         L.orc_enumerate.argtypes = [u32, u32, vp, i64, vp, i64, vp, vp]
         L.orc_enumerate.restype = ctypes.c_int
         _lib = L
@@ -152,6 +156,71 @@ def exact(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     out = np.empty(4, dtype=np.float64)
     _lib_().orc_exact(_p(a), len(a), _p(b), len(b), _p(out))
     return out
+
+
+def join(Q: np.ndarray, D: np.ndarray, N: int, d: int, measure: int, thresholds,
+         exclude_self: bool = False) -> np.ndarray:
+    """Threshold join from sketches (Exp. 2's O'; reading R-J1).
+
+    Returns uint32 bits [nthr][nq][ceil(ndb/32)].
+    """
+    Q = np.ascontiguousarray(Q, dtype=np.uint32)
+    D = np.ascontiguousarray(D, dtype=np.uint32)
+    thr = np.ascontiguousarray(np.atleast_1d(np.asarray(thresholds, dtype=np.float64)))
+    out = np.empty((len(thr), Q.shape[0], (D.shape[0] + 31) // 32), dtype=np.uint32)
+    _lib_().orc_join(_p(Q), Q.shape[0], _p(D), D.shape[0], N, d, measure, _p(thr), len(thr),
+                     1 if exclude_self else 0, _p(out))
+    return out
+
+
+def join_exact(qptr, qidx, dptr, didx, measure: int, thresholds, exclude_self: bool = False) -> np.ndarray:
+    """Threshold join on the uncompressed rows (Exp. 2's ground truth O). CSR, sorted supports."""
+    qptr = np.ascontiguousarray(qptr, dtype=np.int64)
+    qidx = np.ascontiguousarray(qidx, dtype=np.int32)
+    dptr = np.ascontiguousarray(dptr, dtype=np.int64)
+    didx = np.ascontiguousarray(didx, dtype=np.int32)
+    thr = np.ascontiguousarray(np.atleast_1d(np.asarray(thresholds, dtype=np.float64)))
+    nq, ndb = len(qptr) - 1, len(dptr) - 1
+    out = np.empty((len(thr), nq, (ndb + 31) // 32), dtype=np.uint32)
+    _lib_().orc_join_exact(_p(qptr), _p(qidx), nq, _p(dptr), _p(didx), ndb, measure, _p(thr), len(thr),
+                           1 if exclude_self else 0, _p(out))
+    return out
+
+
+def bits_to_sets(bits: np.ndarray, ndb: int) -> list[set]:
+    """Rows of a [nq][ceil(ndb/32)] bit matrix as Python sets of column indices."""
+    out = []
+    for row in np.asarray(bits, dtype=np.uint32):
+        cols = np.nonzero(np.unpackbits(row.view(np.uint8), bitorder="little")[:ndb])[0]
+        out.append(set(int(c) for c in cols))
+    return out
+
+
+def ranking_metrics(O: list[set], Op: list[set]) -> dict:
+    """Experiment 2's measures per query, macro-averaged.
+
+    accuracy = |O ∩ O'| / |O ∪ O'|, precision = |O ∩ O'| / |O'|,
+    recall = |O ∩ O'| / |O|, F1 = 2 p r / (p + r). Queries with O = O' = ∅ are
+    skipped; a 0/0 precision or recall counts as 0 and F1 = 0 when
+    p + r = 0 (reading R-J2).
+    """
+    acc, pre, rec, f1 = [], [], [], []
+    skipped = 0
+    for o, op in zip(O, Op):
+        u = len(o | op)
+        if u == 0:
+            skipped += 1
+            continue
+        i = len(o & op)
+        p = i / len(op) if op else 0.0
+        r = i / len(o) if o else 0.0
+        acc.append(i / u)
+        pre.append(p)
+        rec.append(r)
+        f1.append(2 * p * r / (p + r) if p + r > 0 else 0.0)
+    mean = (lambda v: float(np.mean(v)) if v else float("nan"))
+    return {"accuracy": mean(acc), "precision": mean(pre), "recall": mean(rec), "f1": mean(f1),
+            "query_count": len(acc), "skipped_queries": skipped}
 
 
 def enumerate_expectations(d: int, N: int, a, b):

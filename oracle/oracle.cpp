@@ -341,6 +341,75 @@ void orc_exact(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, doubl
 }
 
 // ---------------------------------------------------------------------------
+// Threshold similarity join, the retrieval step of Experiment 2 (PAPER.md:
+// 690-700: "compute the points in the training partition whose similarities
+// are higher than a certain threshold"; thresholds PAPER.md:697). Reading
+// R-J1: pair (i, j) is reported at threshold t iff key(i,j) >= key(t), with
+// key = the measure's value for IP / JS / COS and -HAM for Hamming (distance
+// at most t), evaluated in fp64 exactly as top-k keys are (R-G17).
+// out_bits: uint32 [nthr][nq][ceil(ndb/32)], bit j%32 of word j/32 of row i
+// (LSB first, tail bits 0), plane t for thresholds[t]. flags & 1: skip j == i.
+//
+// orc_join: estimates from sketches by the canonical recipe (orc_estimate_pair).
+// orc_join_exact: exact similarities of the uncompressed sparse rows (CSR,
+// sorted supports) by the merge walk of orc_exact — the ground truth O.
+// ---------------------------------------------------------------------------
+static void join_set(uint32_t* out_bits, uint64_t nq, uint64_t ndb, uint32_t nthr, int m, const double* thr,
+                     uint64_t i, uint64_t j, const double* e) {
+  const uint64_t wpr = (ndb + 31) / 32;
+  const double key = (m == 1) ? -e[m] : e[m];
+  for (uint32_t t = 0; t < nthr; ++t) {
+    const double tk = (m == 1) ? -thr[t] : thr[t];
+    if (key >= tk) out_bits[((uint64_t)t * nq + i) * wpr + j / 32] |= 1u << (j % 32);
+  }
+}
+
+void orc_join(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint64_t ndb, uint32_t N, uint64_t d,
+              uint32_t measure, const double* thr, uint32_t nthr, uint32_t flags, uint32_t* out_bits) {
+  const uint64_t W = orc_words(N), wpr = (ndb + 31) / 32;
+  int m = 0;
+  while (m < 4 && measure != (1u << m)) ++m;
+  std::memset(out_bits, 0, (size_t)nthr * nq * wpr * 4);
+  if (m == 4) return;
+  std::vector<double> L(N + 1);
+  orc_card_table(N, d, L.data());
+  std::vector<int32_t> pd(ndb);
+  for (uint64_t j = 0; j < ndb; ++j) pd[j] = popcount_row(D + j * W, W);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t i = 0; i < (int64_t)nq; ++i) {
+    const uint32_t* qi = Q + (uint64_t)i * W;
+    const int pq = popcount_row(qi, W);
+    for (uint64_t j = 0; j < ndb; ++j) {
+      if ((flags & 1u) && (int64_t)j == i) continue;
+      int pab = 0;
+      for (uint64_t w = 0; w < W; ++w) pab += popc_fast(qi[w] & D[j * W + w]);
+      double e[4];
+      orc_estimate_pair(pq, pd[j], pab, N, L.data(), e);
+      join_set(out_bits, nq, ndb, nthr, m, thr, (uint64_t)i, j, e);
+    }
+  }
+}
+
+void orc_join_exact(const int64_t* qptr, const int32_t* qidx, uint64_t nq, const int64_t* dptr,
+                    const int32_t* didx, uint64_t ndb, uint32_t measure, const double* thr, uint32_t nthr,
+                    uint32_t flags, uint32_t* out_bits) {
+  const uint64_t wpr = (ndb + 31) / 32;
+  int m = 0;
+  while (m < 4 && measure != (1u << m)) ++m;
+  std::memset(out_bits, 0, (size_t)nthr * nq * wpr * 4);
+  if (m == 4) return;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t i = 0; i < (int64_t)nq; ++i) {
+    for (uint64_t j = 0; j < ndb; ++j) {
+      if ((flags & 1u) && (int64_t)j == i) continue;
+      double e[4];
+      orc_exact(qidx + qptr[i], qptr[i + 1] - qptr[i], didx + dptr[j], dptr[j + 1] - dptr[j], e);
+      join_set(out_bits, nq, ndb, nthr, m, thr, (uint64_t)i, j, e);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Exhaustive enumeration of Lemma 1's expectations: the
 // mean of |a_s| and of <a_s,b_s> over ALL N^d maps pi, computed by sketching
 // with every map (orc_sketch) and counting bits. a, b are sorted supports in

@@ -104,3 +104,67 @@ def scaled(spec: CSRSpec, n: int, seed: int | None = None) -> CSRSpec:
     """Same distribution, fewer rows (parity cases the oracle finishes quickly)."""
     return CSRSpec(n=n, d=spec.d, kind=spec.kind, p1=spec.p1, p2=spec.p2, cap=spec.cap,
                    zipf_s=spec.zipf_s, seed=spec.seed if seed is None else seed, perm=spec.perm)
+
+
+# --- Experiment 2 inputs (PAPER.md:690-706): near-duplicate structure + 90/10 split ---
+def plant_near_duplicates(indptr, indices, d: int, frac: float, seed: int, keep_lo: float = 0.5):
+    """Replace a seeded fraction of rows by perturbed copies of earlier rows.
+
+    Real corpora have near-duplicate documents; i.i.d. Zipf rows do not, so a
+    threshold join at the paper's high thresholds (0.95 ... 0.5) would be empty.
+    Row i (chosen with probability ``frac``, i >= 1) becomes a copy of a random
+    earlier row in which each feature is kept with probability ``keep`` ~
+    U[keep_lo, 1] and otherwise replaced by a uniform feature in [0, d); the
+    result is deduplicated and sorted. Input preparation only (no method
+    arithmetic). Returns new (indptr, indices).
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n = len(indptr) - 1
+    rows = [indices[indptr[i]:indptr[i + 1]] for i in range(n)]
+    pick = rng.random(n) < frac
+    src = (rng.random(n) * np.arange(n)).astype(np.int64)
+    keep = keep_lo + (1.0 - keep_lo) * rng.random(n)
+    for i in range(1, n):
+        if not pick[i]:
+            continue
+        s = rows[src[i]]
+        k = rng.random(len(s)) < keep[i]
+        fresh = rng.integers(0, d, size=int((~k).sum()), dtype=np.int64).astype(np.int32)
+        r = np.unique(np.concatenate([s[k], fresh]))
+        rows[i] = r if len(r) else s[:1].copy()
+    counts = np.array([len(r) for r in rows], dtype=np.int64)
+    out_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=out_ptr[1:])
+    out_idx = np.concatenate(rows).astype(np.int32) if n else np.zeros(0, dtype=np.int32)
+    return out_ptr, out_idx
+
+
+def split_rows(n: int, frac_query: float, seed: int):
+    """Seeded random partition of row ids into (training, querying) parts, each sorted
+    (PAPER.md:692-694: "randomly, partition the dataset into two parts -- 90% and 10%")."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    p = rng.permutation(n)
+    nq = int(round(n * frac_query))
+    return np.sort(p[nq:]), np.sort(p[:nq])
+
+
+def take_rows(indptr, indices, rows):
+    """CSR of the selected rows, in the given order."""
+    rows = np.asarray(rows, dtype=np.int64)
+    counts = indptr[rows + 1] - indptr[rows]
+    out_ptr = np.zeros(len(rows) + 1, dtype=np.int64)
+    np.cumsum(counts, out=out_ptr[1:])
+    out_idx = np.empty(int(out_ptr[-1]), dtype=np.int32)
+    for t, r in enumerate(rows):
+        out_idx[out_ptr[t]:out_ptr[t + 1]] = indices[indptr[r]:indptr[r + 1]]
+    return out_ptr, out_idx
+
+
+# Exp. 2 workload: the Ranking corpus distribution (NYTimes-like d), 101,000 rows with
+# 30% planted near-duplicates, split 90/10 into training (db) and querying parts.
+EXP2 = CSRSpec(n=101_000, d=102_660, kind=1, p1=230, p2=SIGMA, cap=900, zipf_s=1.05, seed=7)
+EXP2_N = 4096
+EXP2_DUP_FRAC = 0.3
+EXP2_DUP_SEED = 8
+EXP2_SPLIT_SEED = 9
+EXP2_THRESHOLDS = (0.95, 0.9, 0.85, 0.8, 0.6, 0.5, 0.2, 0.1)   # PAPER.md:697
