@@ -62,12 +62,17 @@ enum {
   BINSKETCH_COS = 8  /* cosine, Algorithm 4                            */
 };
 
-enum { BINSKETCH_TOPK_EXCLUDE_SELF = 1 };  /* topk flags: skip db row j == query row i */
+enum { BINSKETCH_TOPK_EXCLUDE_SELF = 1 };  /* topk / join flags: skip db row j == query row i */
+enum { BINSKETCH_JOIN_EXCLUDE_SELF = 1,    /* join flags */
+       BINSKETCH_JOIN_EXACT = 2 };         /* rows are uncompressed bit vectors: exact similarities */
+
+enum { BINSKETCH_MAX_THRESHOLDS = 16 };    /* thresholds per binsketch_join call */
 
 enum { BINSKETCH_MAX_K = 256 };            /* largest k binsketch_topk accepts */
 
 /* ops for binsketch_workspace_bytes */
-enum { BINSKETCH_OP_ANDPOPC = 1, BINSKETCH_OP_ESTIMATE = 2, BINSKETCH_OP_TOPK = 3 };
+enum { BINSKETCH_OP_ANDPOPC = 1, BINSKETCH_OP_ESTIMATE = 2, BINSKETCH_OP_TOPK = 3, BINSKETCH_OP_JOIN = 4,
+       BINSKETCH_OP_JOIN_LIST = 5 };
 
 /* W = ceil(N/32), words per sketch row. */
 uint32_t binsketch_words(uint32_t N);
@@ -146,6 +151,49 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
                                 uint32_t N, uint64_t d, uint32_t measure, uint32_t k, uint32_t flags,
                                 int32_t* out_idx, float* out_score, void* ws, size_t ws_bytes,
                                 binsketch_stream_t stream);
+
+/* Threshold similarity join — the retrieval step of Experiment 2 (PAPER.md:690-700:
+ * "compute the points in the training partition whose similarities are higher than a
+ * certain threshold"; thresholds PAPER.md:697; reading R-J1). For each query i, db row j
+ * and threshold t, bit j of row i of plane t is set iff key(i,j) >= key(t), where key is
+ * the fp64 estimate of binsketch_topk (IP, JS, COS as is; -HAM for Hamming, so a Hamming
+ * threshold selects distances <= t) and key(t) = t (-t for Hamming).
+ * flags: BINSKETCH_JOIN_EXCLUDE_SELF skips j == i; BINSKETCH_JOIN_EXACT treats the rows as
+ *   the UNCOMPRESSED binary vectors (e.g. built by binsketch_build with the identity map,
+ *   N = d) and uses the exact similarities |a∩b|, |a|+|b|-2|a∩b|, |a∩b|/|a∪b|,
+ *   |a∩b|/sqrt(|a||b|) (JS(∅,∅) = 1, COS with an empty side = 0) — Exp. 2's ground truth O.
+ * thresholds: HOST double[nthr], 1 <= nthr <= BINSKETCH_MAX_THRESHOLDS, not NaN, any order.
+ * measure: exactly one BINSKETCH_* bit. d: saturation cap (ignored with JOIN_EXACT).
+ * out_bits: device uint32[nthr][nq][ceil(ndb/32)] (bit j%32 of word j/32, LSB first; tail
+ *   bits 0), fully overwritten. The result is a set, so it is bit-identical run to run.
+ * ws: >= binsketch_workspace_bytes(BINSKETCH_OP_JOIN, nq, ndb, N, 0).
+ * Runs on the tensor-core engine (K11): AND-popcounts as in binsketch_andpopc,
+ * a per-tile bound at the lowest threshold skips hopeless pairs, survivors are scored
+ * exactly and their bits set. */
+binsketch_status binsketch_join(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb,
+                                uint32_t N, uint64_t d, uint32_t measure, const double* thresholds,
+                                uint32_t nthr, uint32_t flags, uint32_t* out_bits, void* ws, size_t ws_bytes,
+                                binsketch_stream_t stream);
+
+/* Match list of one join plane (bits: device uint32[nq][ceil(ndb/32)], as written by
+ * binsketch_join): row_ptr (device int64[nq+1]) = prefix sums of the per-query match
+ * counts; for each query the matches in ascending db index: out_j (device int32[cap]) and
+ * out_score (device float[cap]) = the measure's value (estimate, or exact with
+ * BINSKETCH_JOIN_EXACT), recomputed from the rows. Entries at positions >= capacity are
+ * counted in row_ptr but not written; capacity = 0 (out_j, out_score may be NULL) computes
+ * row_ptr only. queries / db / N / d / measure / flags as for the binsketch_join call.
+ * ws: >= binsketch_workspace_bytes(BINSKETCH_OP_JOIN_LIST, nq, ndb, N, 0). */
+binsketch_status binsketch_join_list(const uint32_t* bits, const uint32_t* queries, uint64_t nq, const uint32_t* db,
+                                     uint64_t ndb, uint32_t N, uint64_t d, uint32_t measure, uint32_t flags,
+                                     int64_t* row_ptr, int32_t* out_j, float* out_score, uint64_t capacity,
+                                     void* ws, size_t ws_bytes, binsketch_stream_t stream);
+
+/* Experiment 2's per-query counts: for two join planes over the same
+ * (nq, ndb) — O' = bits_est (from sketches), O = bits_true (exact) — out (device
+ * int64[3][nq]) = |O'_i|, |O_i|, |O'_i ∩ O_i|. accuracy, precision, recall and F1 are
+ * ratios of these (R-J2). */
+binsketch_status binsketch_join_confusion(const uint32_t* bits_est, const uint32_t* bits_true, uint64_t nq,
+                                          uint64_t ndb, int64_t* out, binsketch_stream_t stream);
 
 /* Workspace bytes needed by op (BINSKETCH_OP_*) for na (queries) x nb (db)
  * rows of N-bit sketches and top-k size k (ignored for other ops). Pure

@@ -20,7 +20,9 @@ IP, HAM, JS, COS = 1, 2, 4, 8
 MEASURES = {"ip": IP, "ham": HAM, "js": JS, "cos": COS}
 TOPK_EXCLUDE_SELF = 1
 MAX_K = 256
-OP_ANDPOPC, OP_ESTIMATE, OP_TOPK = 1, 2, 3
+OP_ANDPOPC, OP_ESTIMATE, OP_TOPK, OP_JOIN, OP_JOIN_LIST = 1, 2, 3, 4, 5
+JOIN_EXCLUDE_SELF, JOIN_EXACT = 1, 2
+MAX_THRESHOLDS = 16
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "EINDEX", 3: "ECUDA", 4: "EWORKSPACE", 5: "EUNSUPPORTED"}
 
@@ -37,6 +39,10 @@ SIGNATURES = {
     "binsketch_andpopc": (_int, [_vp, _u64, _vp, _u64, _u32, _vp, _vp, _sz, _vp]),
     "binsketch_estimate": (_int, [_vp, _u64, _vp, _u64, _u32, _u64, _u32, _vp, _vp, _sz, _vp]),
     "binsketch_topk": (_int, [_vp, _u64, _vp, _u64, _u32, _u64, _u32, _u32, _u32, _vp, _vp, _vp, _sz, _vp]),
+    "binsketch_join": (_int, [_vp, _u64, _vp, _u64, _u32, _u64, _u32, _vp, _u32, _u32, _vp, _vp, _sz, _vp]),
+    "binsketch_join_list": (_int, [_vp, _vp, _u64, _vp, _u64, _u32, _u64, _u32, _u32, _vp, _vp, _vp, _u64, _vp, _sz,
+                                   _vp]),
+    "binsketch_join_confusion": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),
     "binsketch_workspace_bytes": (_sz, [_int, _u64, _u64, _u32, _u32]),
     "binsketch_card_table": (_int, [_u32, _u64, _vp]),
     "binsketch_device_status": (_int, [_vp]),
@@ -193,6 +199,59 @@ def topk(Q: torch.Tensor, D: torch.Tensor, N: int, d: int, measure: int, k: int,
         _dev(out_idx, torch.int32, "out_idx") if out_idx.numel() else None,
         _dev(out_score, torch.float32, "out_score") if out_score.numel() else None, wp, wn, _stream()))
     return out_idx, out_score
+
+
+def join(Q: torch.Tensor, D: torch.Tensor, N: int, d: int, measure: int, thresholds, exclude_self: bool = False,
+         exact: bool = False, out: torch.Tensor | None = None, ws=None) -> torch.Tensor:
+    """Threshold join (Exp. 2): int32 bit planes [nthr][nq][ceil(ndb/32)] (binsketch_join)."""
+    nq, ndb = Q.shape[0], D.shape[0]
+    thr = (ctypes.c_double * len(thresholds))(*[float(t) for t in thresholds])
+    wpr = (ndb + 31) // 32
+    if out is None:
+        out = torch.empty((len(thresholds), nq, wpr), dtype=torch.int32, device="cuda")
+    ws, wp, wn = _workspace(OP_JOIN, nq, ndb, N, 0, ws)
+    flags = (JOIN_EXCLUDE_SELF if exclude_self else 0) | (JOIN_EXACT if exact else 0)
+    _check("binsketch_join", _lib().binsketch_join(
+        _words_tensor(Q, "queries") if nq else None, nq, _words_tensor(D, "db") if ndb else None, ndb, N, d, measure,
+        ctypes.cast(thr, ctypes.c_void_p), len(thresholds), flags,
+        _words_tensor(out, "out_bits") if out.numel() else None, wp, wn, _stream()))
+    return out
+
+
+def join_list(bits: torch.Tensor, Q: torch.Tensor, D: torch.Tensor, N: int, d: int, measure: int,
+              exact: bool = False, ws=None):
+    """CSR match list of one join plane: (row_ptr int64[nq+1], cols int32[total], scores float[total])."""
+    nq, ndb = Q.shape[0], D.shape[0]
+    row_ptr = torch.empty(nq + 1, dtype=torch.int64, device="cuda")
+    ws, wp, wn = _workspace(OP_JOIN_LIST, nq, ndb, N, 0, ws)
+    flags = JOIN_EXACT if exact else 0
+    args = lambda cap, oj, osc: _lib().binsketch_join_list(   # noqa: E731
+        _words_tensor(bits, "bits") if bits.numel() else None, _words_tensor(Q, "queries") if nq else None, nq,
+        _words_tensor(D, "db") if ndb else None, ndb, N, d, measure, flags, _dev(row_ptr, torch.int64, "row_ptr"),
+        oj, osc, cap, wp, wn, _stream())
+    if nq == 0:
+        row_ptr.zero_()
+        return row_ptr, torch.empty(0, dtype=torch.int32, device="cuda"), torch.empty(0, device="cuda")
+    _check("binsketch_join_list", args(0, None, None))
+    total = int(row_ptr[-1].item())
+    cols = torch.empty(max(total, 1), dtype=torch.int32, device="cuda")
+    scores = torch.empty(max(total, 1), dtype=torch.float32, device="cuda")
+    if total:
+        _check("binsketch_join_list", args(total, _dev(cols, torch.int32, "out_j"), _dev(scores, torch.float32,
+                                                                                         "out_score")))
+    return row_ptr, cols[:total], scores[:total]
+
+
+def join_confusion(bits_est: torch.Tensor, bits_true: torch.Tensor, ndb: int) -> torch.Tensor:
+    """int64 [3][nq]: |O'|, |O|, |O' ∩ O| per query (binsketch_join_confusion)."""
+    nq = bits_est.shape[0]
+    out = torch.empty((3, nq), dtype=torch.int64, device="cuda")
+    if nq:
+        _check("binsketch_join_confusion", _lib().binsketch_join_confusion(
+            _words_tensor(bits_est, "bits_est") if bits_est.numel() else None,
+            _words_tensor(bits_true, "bits_true") if bits_true.numel() else None, nq, ndb,
+            _dev(out, torch.int64, "out"), _stream()))
+    return out
 
 
 def card_table(N: int, d: int):

@@ -28,6 +28,7 @@ UNITS = {
     "build.cu": [],
     "pairs.cu": ["-fmad=false"],
     "tc.cu": ["-fmad=false"],
+    "join.cu": ["-fmad=false"],
 }
 HEADERS = ["bsk_internal.cuh", "bsk_device.cuh", "bsk_estimator.cuh"]
 

@@ -78,7 +78,7 @@ TableCache& cache() {
 
 struct Layout {
   size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, qperm = 0, qspb = 0,
-         ctr = 0, done = 0, pab = 0, total = 0;
+         ctr = 0, done = 0, pab = 0, cnt = 0, total = 0;
   uint32_t splits = 1;
 };
 
@@ -114,6 +114,21 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
   l.L = off; off += align_up((size_t)(N + 1) * 8);
   l.pa = off; off += align_up((size_t)na * 4);
   l.pb = off; off += align_up((size_t)nb * 4);
+  if (op == BINSKETCH_OP_JOIN) {   // tensor-core join: widened operands, db sorted by popcount
+    l.ctr = off; off += kAlign;
+    l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
+    l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
+    l.bins = off; off += align_up((size_t)(N + 1) * 4);
+    l.perm = off; off += align_up((size_t)nb * 4);
+    l.spb = off; off += align_up((size_t)nb * 4);
+    l.total = off;
+    return l;
+  }
+  if (op == BINSKETCH_OP_JOIN_LIST) {
+    l.cnt = off; off += align_up((size_t)na * 4);
+    l.total = off;
+    return l;
+  }
   const bool tc = use_tc(op, N, k);
   const bool tcp = op == BINSKETCH_OP_TOPK && use_tc_pab(N, na, nb, k);
   if (tcp) {
@@ -335,6 +350,94 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
                          l.splits > 1 ? reinterpret_cast<int32_t*>(w + l.pidx) : nullptr, out_idx, out_score, s,
                          pab);
   return cuda_status(e);
+}
+
+binsketch_status binsketch_join(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb, uint32_t N,
+                                uint64_t d, uint32_t measure, const double* thresholds, uint32_t nthr, uint32_t flags,
+                                uint32_t* out_bits, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
+  if (N < 2 || !one_bit(measure) || (flags & ~3u)) return BINSKETCH_EINVAL;
+  if (nthr == 0 || nthr > BINSKETCH_MAX_THRESHOLDS || !thresholds) return BINSKETCH_EINVAL;
+  for (uint32_t t = 0; t < nthr; ++t)
+    if (std::isnan(thresholds[t])) return BINSKETCH_EINVAL;
+  if (nq == 0 || ndb == 0) return BINSKETCH_OK;
+  const bool exact = (flags & BINSKETCH_JOIN_EXACT) != 0;
+  if (!queries || !db || !out_bits || (!exact && d == 0)) return BINSKETCH_EINVAL;
+  if (nq > 0x7fffffffull || ndb > 0x7fffffffull) return BINSKETCH_EUNSUPPORTED;
+  const Layout l = layout(BINSKETCH_OP_JOIN, nq, ndb, N, 0);
+  if (!ws || ws_bytes < l.total) return BINSKETCH_EWORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  if (!exact) {
+    binsketch_status st = upload_table(N, d, ws, l, s);
+    if (st != BINSKETCH_OK) return st;
+  }
+  const uint32_t W = binsketch_words(N);
+  int32_t* pq = reinterpret_cast<int32_t*>(w + l.pa);
+  int32_t* pd = reinterpret_cast<int32_t*>(w + l.pb);
+  cudaError_t e = bsk::launch_popcount(queries, nq, W, pq, s);
+  const bool self = queries == db && nq == ndb;
+  if (e == cudaSuccess) e = self ? cudaMemcpyAsync(pd, pq, nq * 4, cudaMemcpyDeviceToDevice, s)
+                                 : bsk::launch_popcount(db, ndb, W, pd, s);
+  int32_t* perm = reinterpret_cast<int32_t*>(w + l.perm);
+  int32_t* spb = reinterpret_cast<int32_t*>(w + l.spb);
+  uint8_t* q8 = reinterpret_cast<uint8_t*>(w + l.a8);
+  uint8_t* d8 = reinterpret_cast<uint8_t*>(w + l.b8);
+  if (e == cudaSuccess) e = bsk::launch_sort_by_popcount(pd, ndb, N, reinterpret_cast<uint32_t*>(w + l.bins), perm, spb, s);
+  if (e == cudaSuccess) e = bsk::launch_expand(queries, nq, N, q8, s);
+  if (e == cudaSuccess) e = bsk::launch_expand(db, ndb, N, d8, s, perm);
+  const uint64_t wpr = (ndb + 31) / 32;
+  if (e == cudaSuccess) e = cudaMemsetAsync(out_bits, 0, (size_t)nthr * nq * wpr * 4, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  // threshold keys (R-J1), descending; tslot maps each back to its output plane
+  double tkey[BINSKETCH_MAX_THRESHOLDS];
+  uint32_t tslot[BINSKETCH_MAX_THRESHOLDS];
+  for (uint32_t t = 0; t < nthr; ++t) { tslot[t] = t; tkey[t] = measure == BINSKETCH_HAM ? -thresholds[t] : thresholds[t]; }
+  for (uint32_t a = 1; a < nthr; ++a)
+    for (uint32_t b = a; b > 0 && tkey[b] > tkey[b - 1]; --b) { std::swap(tkey[b], tkey[b - 1]); std::swap(tslot[b], tslot[b - 1]); }
+  const bool prefilter = exact || cache().convex(N, d);
+  e = bsk::launch_tc_join(q8, nq, d8, ndb, N, measure, tkey, tslot, nthr, flags & BINSKETCH_JOIN_EXCLUDE_SELF, exact, pq,
+                          spb, perm, reinterpret_cast<const double*>(w + l.L), prefilter, out_bits,
+                          reinterpret_cast<unsigned long long*>(w + l.ctr), s);
+  return cuda_status(e);
+}
+
+binsketch_status binsketch_join_list(const uint32_t* bits, const uint32_t* queries, uint64_t nq, const uint32_t* db,
+                                     uint64_t ndb, uint32_t N, uint64_t d, uint32_t measure, uint32_t flags,
+                                     int64_t* row_ptr, int32_t* out_j, float* out_score, uint64_t capacity, void* ws,
+                                     size_t ws_bytes, binsketch_stream_t stream) {
+  if (N < 2 || !one_bit(measure) || (flags & ~3u)) return BINSKETCH_EINVAL;
+  if (nq == 0) return BINSKETCH_OK;
+  const bool exact = (flags & BINSKETCH_JOIN_EXACT) != 0;
+  if (!row_ptr || (ndb > 0 && !bits)) return BINSKETCH_EINVAL;
+  if (capacity > 0 && (!out_j || !out_score || !queries || (ndb > 0 && !db) || (!exact && d == 0)))
+    return BINSKETCH_EINVAL;
+  if (ndb > 0x7fffffffull) return BINSKETCH_EUNSUPPORTED;
+  const Layout l = layout(BINSKETCH_OP_JOIN_LIST, nq, ndb, N, 0);
+  if (!ws || ws_bytes < l.total) return BINSKETCH_EWORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  cudaError_t e = bsk::launch_join_rowptr(bits, nq, ndb, reinterpret_cast<int32_t*>(w + l.cnt), row_ptr, s);
+  if (e != cudaSuccess || capacity == 0 || ndb == 0) return cuda_status(e);
+  if (!exact) {
+    binsketch_status st = upload_table(N, d, ws, l, s);
+    if (st != BINSKETCH_OK) return st;
+  }
+  const uint32_t W = binsketch_words(N);
+  int32_t* pq = reinterpret_cast<int32_t*>(w + l.pa);
+  int32_t* pd = reinterpret_cast<int32_t*>(w + l.pb);
+  e = bsk::launch_popcount(queries, nq, W, pq, s);
+  if (e == cudaSuccess) e = bsk::launch_popcount(db, ndb, W, pd, s);
+  if (e == cudaSuccess)
+    e = bsk::launch_join_list(bits, nq, ndb, queries, db, N, pq, pd, reinterpret_cast<const double*>(w + l.L), measure,
+                              exact, row_ptr, out_j, out_score, capacity, s);
+  return cuda_status(e);
+}
+
+binsketch_status binsketch_join_confusion(const uint32_t* bits_est, const uint32_t* bits_true, uint64_t nq,
+                                          uint64_t ndb, int64_t* out, binsketch_stream_t stream) {
+  if (nq == 0) return BINSKETCH_OK;
+  if (!out || (ndb > 0 && (!bits_est || !bits_true))) return BINSKETCH_EINVAL;
+  return cuda_status(bsk::launch_join_confusion(bits_est, bits_true, nq, ndb, out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 binsketch_status binsketch_card_table(uint32_t N, uint64_t d, double* host_out) {

@@ -60,6 +60,19 @@ __device__ __forceinline__ Est estimate_pair(int pa, int pb, int pab, int N, con
 }
 
 
+// Exact similarity key of two uncompressed rows from (|a|, |b|, |a AND b|) — the threshold
+// join's ground truth (Exp. 2's O): the recipe above with L = identity
+// (no estimation), keys as in measure_key (-HAM for Hamming). Integers up to 2^31 are exact
+// in fp64, so IP and HAM are exact and JS / COS are one correctly rounded division.
+__device__ __forceinline__ double exact_key(int pa, int pb, int pab, uint32_t m) {
+  const double ip = (double)pab;
+  const double S = __dadd_rn((double)pa, (double)pb);
+  if (m == 1u) return ip;
+  if (m == 2u) return -__dsub_rn(S, __dmul_rn(2.0, ip));
+  if (m == 4u) return (pa == 0 && pb == 0) ? 1.0 : __ddiv_rn(ip, __dsub_rn(S, ip));
+  return (pa == 0 || pb == 0) ? 0.0 : __ddiv_rn(ip, __dsqrt_rn(__dmul_rn((double)pa, (double)pb)));
+}
+
 // Order (reading R-G17): a before b iff a.key > b.key, or equal keys and
 // a.idx < b.idx. Sentinel (key = -inf, idx = INT_MAX) sorts last.
 __device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {

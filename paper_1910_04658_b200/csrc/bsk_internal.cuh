@@ -74,7 +74,7 @@ uint32_t tc_topk_max_k();
 uint32_t tc_topk_max_n();
 uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t N, uint32_t k);   // partial lists per query
 // db order: counting sort by popcount, descending (perm: sorted position -> db row; spb:
-// sorted popcounts; bins: N+1 words of scratch). Needs N <= 65536 (tc_sortable).
+// sorted popcounts; bins: N+1 words of scratch). Top-k uses it for N <= 65536 (tc_sortable).
 bool tc_sortable(uint32_t N);
 cudaError_t launch_sort_by_popcount(const int32_t* pb, uint64_t n, uint32_t N, uint32_t* bins, int32_t* perm,
                                     int32_t* spb, cudaStream_t s);
@@ -85,5 +85,23 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
                            const int32_t* pd, const int32_t* perm, const double* L, bool prefilter, double* part_key,
                            int32_t* part_idx, int32_t* out_idx, float* out_score, unsigned long long* ctr,
                            unsigned int* done, cudaStream_t s);   // done: ceil(nq/128) words of workspace
+
+// Threshold join on the tensor-core engine (Exp. 2): bits [nthr][nq][ceil(ndb/32)] (zeroed by the
+// caller); tkey descending with tslot[t] its bitmap plane; D8 rows in `perm` order (pd sorted
+// popcounts, descending) when prefilter is on. exact: L unused, keys from exact_key.
+uint32_t tc_join_max_thresholds();
+cudaError_t launch_tc_join(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
+                           uint32_t measure, const double* tkey, const uint32_t* tslot, uint32_t nthr, uint32_t flags,
+                           bool exact, const int32_t* pq, const int32_t* pd, const int32_t* perm, const double* L,
+                           bool prefilter, uint32_t* bits, unsigned long long* ctr, cudaStream_t s);
+// join.cu: per-row counts (int32 scratch [nq]) -> row_ptr [nq+1]; list; confusion counts [3][nq].
+cudaError_t launch_join_rowptr(const uint32_t* bits, uint64_t nq, uint64_t ndb, int32_t* counts, int64_t* row_ptr,
+                               cudaStream_t s);
+cudaError_t launch_join_list(const uint32_t* bits, uint64_t nq, uint64_t ndb, const uint32_t* Q, const uint32_t* D,
+                             uint32_t N, const int32_t* pq, const int32_t* pd, const double* L, uint32_t measure,
+                             bool exact, const int64_t* row_ptr, int32_t* out_j, float* out_score, uint64_t cap,
+                             cudaStream_t s);
+cudaError_t launch_join_confusion(const uint32_t* est, const uint32_t* tru, uint64_t nq, uint64_t ndb, int64_t* out,
+                                  cudaStream_t s);
 
 }  // namespace bsk

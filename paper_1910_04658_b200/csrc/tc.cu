@@ -204,7 +204,8 @@ constexpr uint32_t kTcThreads = 192;                       // producer, MMA, 4 e
 constexpr uint32_t kTcSmemMax = 227 * 1024;
 // instruction descriptor: D s32, A/B u8, K-major, N = 256, M = 128
 constexpr uint32_t kTcIdesc = (2u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
-enum TcMode { kTcAndPopc = 0, kTcEstimate = 1, kTcTopk = 2 };
+enum TcMode { kTcAndPopc = 0, kTcEstimate = 1, kTcTopk = 2, kTcJoin = 3 };
+constexpr uint32_t kTcMaxThr = 16;   // thresholds per join launch
 
 template <int KC>
 struct TcGeom {
@@ -247,6 +248,11 @@ struct TcParams {
   double lc;              // log1p(-1/N): closed-form inverse of the table for the tile bound
   const int32_t* qperm;   // kTcTopk: A row (queries sorted by |a_s| descending) -> original query index
   unsigned long long* item_ctr;   // dynamic work queue: next item (zeroed before the launch)
+  uint32_t* bits;         // kTcJoin: match bitmaps [nthr][na][wpr] (zeroed before the launch)
+  uint64_t wpr;           // kTcJoin: words per bitmap row = ceil(nb / 32)
+  uint32_t nthr, exact;   // kTcJoin: threshold count; exact similarities (L = identity) instead of estimates
+  double tkey[kTcMaxThr];     // kTcJoin: threshold keys, descending
+  uint32_t tslot[kTcMaxThr];  // kTcJoin: bitmap plane of each key
 };
 
 template <int MODE, int KC>
@@ -284,8 +290,8 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   const double* L = p.L;
-  double* Ls = reinterpret_cast<double*>(extra + (MODE == kTcTopk ? p.heap_smem : 0u));
-  if ((MODE == kTcEstimate && p.l_smem) || MODE == kTcTopk) {   // top-k always stages the table
+  double* Ls = reinterpret_cast<double*>(extra + ((MODE == kTcTopk || MODE == kTcJoin) ? p.heap_smem : 0u));
+  if ((MODE == kTcEstimate && p.l_smem) || MODE == kTcTopk || (MODE == kTcJoin && p.l_topk_smem)) {   // top-k always stages the table
     for (uint32_t i = threadIdx.x; i <= p.N; i += blockDim.x) Ls[i] = p.L[i];
     L = Ls;
   }
@@ -631,6 +637,162 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (lane == 0) atomicAdd(p.done + mt, 1u);
       }
     }
+  } else if (MODE == kTcJoin) {
+    // ---- threshold-join epilogue (Exp. 2; R-J1): thread = one query row
+    // (TMEM lane). Per 256-column tile the prefilter bound of the top-k epilogue, taken at
+    // the LOWEST threshold key, gives pmin; 32-column chunks whose max pab < pmin are skipped
+    // with one compare. Survivors go through a per-warp queue and are scored lane-parallel
+    // (canonical fp64 recipe, or the exact key); a match sets its bit in every plane whose
+    // threshold it reaches (bit = original db index, so the bitmap is order independent).
+    const uint32_t lb = 32u * (uint32_t)(warp & 3);
+    const uint32_t rt = lb + (uint32_t)lane;
+    const uint32_t m = p.measure;
+    const bool exact = p.exact != 0u;
+    constexpr uint32_t kJQ = 1024;                    // per-warp queue: one chunk of 32 x 32 always fits
+    int32_t* tpb = reinterpret_cast<int32_t*>(extra) + (size_t)(warp - 2) * 2 * kTcN;
+    int32_t* tpm = tpb + kTcN;
+    uint2* q = reinterpret_cast<uint2*>(extra + 4 * 2 * kTcN * 4) + (size_t)(warp - 2) * kJQ;
+    const double g = p.tkey[p.nthr - 1] - 1e-9 * fmax(1.0, fabs(p.tkey[p.nthr - 1]));   // lowest key, with slack
+    const uint64_t plane = p.na * p.wpr;
+    auto Lv = [&](uint32_t x) -> double { return exact ? (double)x : L[x]; };
+    uint32_t aphase = 0;
+    int acc = 0;
+    for (uint32_t ii = 0;; ++ii) {
+      uint64_t it = 0;
+      if (lane == 0) it = take_item(ii);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= p.nitems) break;
+      uint64_t mt; uint32_t sp, nt0, nt1;
+      item_range(it, mt, sp, nt0, nt1);
+      const uint64_t r = mt * kTcM + rt;
+      const bool valid = r < p.na;
+      const int pa = valid ? __ldg(p.pa + r) : 0;
+      const double La = Lv((uint32_t)pa);
+      // key bound over the tile's pb range [lo, hi] (see the top-k epilogue; L = identity when exact)
+      auto key_bound = [&](uint32_t pab, uint32_t lo, uint32_t hi_) -> double {
+        const uint32_t pu = min(pa + lo - min(pab, pa + lo), p.N);
+        const double Llo = Lv(lo);
+        double u = La + Llo - Lv(pu);
+        u = u > 0.0 ? u : 0.0;
+        u = fmin(u, fmin(La, Lv(hi_)));
+        if (m == 1u) return u;
+        if (m == 4u) { const double den = La + Llo - u; return den > 0.0 ? fmin(u / den, 1.0) : 1.0; }
+        if (m == 8u) return fmin(u / sqrt(La * Llo), 1.0);
+        return fmin(2.0 * u - La - Llo, 0.0);
+      };
+      uint32_t c_lo = 0xFFFFFFFFu, c_hi = 0, c_pmin = 0;
+      auto tile_pmin = [&](uint32_t lo, uint32_t hi_) -> uint32_t {
+        if (!p.prefilter || lo == 0) return 0u;
+        if (lo == c_lo && hi_ == c_hi) return c_pmin;
+        const uint32_t pmax = min((uint32_t)pa, hi_);
+        const double Llo = Lv(lo);
+        double t;
+        if (m == 1u) t = g;
+        else if (m == 4u) t = g > -1.0 ? g * (La + Llo) / (1.0 + g) : -1.0;
+        else if (m == 8u) t = g * sqrt(La * Llo);
+        else t = 0.5 * (g + La + Llo);
+        uint32_t qq;
+        if (t <= 0.0) {
+          qq = 0u;
+        } else if (fmin(La, Lv(hi_)) < t) {
+          qq = pmax + 1;
+        } else {
+          float q0;
+          if (exact) {
+            q0 = (float)t - 2.0f;
+          } else {
+            const float pr = -(float)p.N * expm1f((float)((La + Llo - t) * p.lc));
+            q0 = (float)pa + (float)lo - fminf(floorf(pr) + 2.0f, (float)p.N);
+          }
+          qq = q0 <= 0.0f ? 0u : min((uint32_t)q0, pmax);
+          while (qq > 0 && key_bound(qq - 1, lo, hi_) >= g) --qq;
+          while (qq <= pmax && key_bound(qq, lo, hi_) < g) ++qq;
+        }
+        c_lo = lo; c_hi = hi_; c_pmin = qq;
+        return qq;
+      };
+      int32_t pf_pb[8], pf_pm[8];
+      auto prefetch = [&](uint32_t nt) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint64_t col = (uint64_t)nt * kTcN + 32 * u + lane;
+          const bool in = nt < nt1 && col < p.nb;
+          pf_pb[u] = in ? __ldg(p.pb + col) : 0;
+          pf_pm[u] = in ? (p.perm ? __ldg(p.perm + col) : (int32_t)col) : -1;
+        }
+      };
+      prefetch(nt0);
+      for (uint32_t nt = nt0; nt < nt1; ++nt) {
+        const uint64_t n0 = (uint64_t)nt * kTcN;
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { tpb[32 * u + lane] = pf_pb[u]; tpm[32 * u + lane] = pf_pm[u]; }
+        __syncwarp();
+        prefetch(nt + 1);
+        const uint32_t nval = (uint32_t)min((uint64_t)kTcN, p.nb - n0);
+        const uint32_t pmin = valid ? tile_pmin((uint32_t)tpb[nval - 1], (uint32_t)tpb[0]) : 0u;
+        tc::mbar_wait(tfull(acc), aphase);
+        tc::fence_after();
+        auto chunk = [&](const uint32_t c, uint32_t (&v)[32]) {
+          if (c >= nval) return;
+          const uint32_t left = nval - c;
+          uint32_t mx = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) mx = max(mx, v[j]);
+          const bool pass = valid && mx >= pmin;
+          if (!__any_sync(0xffffffffu, pass)) return;
+          uint32_t sm = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sm |= ((pass && v[j] >= pmin && (uint32_t)j < left) ? 1u : 0u) << j;
+          const uint32_t ns = __popc(sm);
+          uint32_t off = ns;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, off, o); if (lane >= o) off += y; }
+          const uint32_t total = __shfl_sync(0xffffffffu, off, 31);
+          off -= ns;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if ((sm >> j) & 1u) q[off++] = make_uint2((c + (uint32_t)j) | ((uint32_t)lane << 16), v[j]);
+          __syncwarp();
+          for (uint32_t b = 0; b < total; b += 32) {
+            const bool has = b + lane < total;
+            const uint2 e = has ? q[b + lane] : make_uint2(0u, 0u);
+            const int owner = (int)(e.x >> 16);
+            const uint32_t col = e.x & 0xFFFFu;
+            const int pa_o = __shfl_sync(0xffffffffu, pa, owner);
+            const uint64_t r_o = __shfl_sync(0xffffffffu, r, owner);
+            if (has) {
+              const int32_t j = tpm[col];
+              if (!((p.flags & 1u) && (uint64_t)j == r_o)) {
+                const double key = exact ? exact_key(pa_o, tpb[col], (int)e.y, m)
+                                         : measure_key(estimate_pair(pa_o, tpb[col], (int)e.y, (int)p.N, L, m), m);
+                uint32_t* row = p.bits + r_o * p.wpr + ((uint32_t)j >> 5);
+                const uint32_t bit = 1u << ((uint32_t)j & 31u);
+                for (uint32_t t = 0; t < p.nthr; ++t)
+                  if (key >= p.tkey[t]) atomicOr(row + (uint64_t)p.tslot[t] * plane, bit);
+              }
+            }
+          }
+          __syncwarp();
+        };
+        const uint32_t tb = tmem + (lb << 16) + (uint32_t)acc * kTcN;
+        uint32_t va[32], vb[32];
+        tc::tmem_ld32_issue(tb, va);
+        tc::tmem_ld_wait(va);
+#pragma unroll 1
+        for (uint32_t c = 0; c < (uint32_t)kTcN; c += 64) {
+          tc::tmem_ld32_issue(tb + c + 32, vb);
+          chunk(c, va);
+          tc::tmem_ld_wait(vb);
+          if (c + 64 < (uint32_t)kTcN) tc::tmem_ld32_issue(tb + c + 64, va);
+          chunk(c + 32, vb);
+          if (c + 64 < (uint32_t)kTcN) tc::tmem_ld_wait(va);
+        }
+        tc::fence_before();
+        tc::mbar_arrive(tempty(acc));
+        if (++acc == 2) { acc = 0; aphase ^= 1u; }
+      }
+    }
   } else {             // ---- andpopc / estimate epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
     const uint32_t lb = 32u * (uint32_t)(warp & 3);
     const uint32_t rt = lb + (uint32_t)lane;          // row within the tile
@@ -884,6 +1046,26 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
   const uint32_t lists = p.chain ? 1u : p.splits;
   if (lists != tc_topk_splits(nq, ndb, N, k)) return cudaErrorInvalidConfiguration;
   return launch_topk_merge(nq, lists, k, measure, part_key, part_idx, out_idx, out_score, s);
+}
+
+uint32_t tc_join_max_thresholds() { return kTcMaxThr; }
+
+cudaError_t launch_tc_join(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
+                           uint32_t measure, const double* tkey, const uint32_t* tslot, uint32_t nthr, uint32_t flags,
+                           bool exact, const int32_t* pq, const int32_t* pd, const int32_t* perm, const double* L,
+                           bool prefilter, uint32_t* bits, unsigned long long* ctr, cudaStream_t s) {
+  if (nq == 0 || ndb == 0 || nthr == 0) return cudaSuccess;
+  if (nthr > kTcMaxThr || (!exact && !L)) return cudaErrorInvalidValue;
+  TcParams p = {};
+  p.na = nq; p.nb = ndb; p.N = N; p.measure = measure; p.flags = flags; p.pa = pq; p.pb = pd; p.L = exact ? nullptr : L;
+  p.perm = perm; p.item_ctr = ctr; p.bits = bits; p.wpr = (ndb + 31) / 32; p.nthr = nthr; p.exact = exact ? 1u : 0u;
+  for (uint32_t t = 0; t < nthr; ++t) { p.tkey[t] = tkey[t]; p.tslot[t] = tslot[t]; }
+  p.lc = std::log1p(-1.0 / (double)N);
+  p.prefilter = (prefilter && perm) ? 1u : 0u;
+  p.heap_smem = 4 * 2 * kTcN * 4 + 4 * 1024 * 8;        // tile staging + survivor queues
+  const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
+  p.l_topk_smem = (!exact && lb <= 64 * 1024) ? lb : 0u;   // else the table is read from global (L1)
+  return tc_launch<kTcJoin, 64>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, 0, s);
 }
 
 }  // namespace bsk

@@ -34,7 +34,7 @@ def _declared():
 
 def test_exports_every_declared_symbol(lib):
     names = _declared()
-    assert len(names) == 14
+    assert len(names) == 17
     for name in names:
         assert hasattr(lib, name), name
     from paper_1910_04658_b200.binsketch import SIGNATURES
@@ -95,6 +95,26 @@ def test_host_detected_errors(lib):
     assert lib.binsketch_topk(None, 4, None, 4, 64, 10, 1, 5, 2, None, None, None, 0, None) == EINVAL  # flags
     assert lib.binsketch_topk(None, 4, None, 4, 64, 10, 1, 0, 0, None, None, None, 0, None) == 0       # k = 0
     assert lib.binsketch_topk(vp(8), 4, vp(8), 4, 64, 10, 1, 257, 0, vp(8), vp(8), None, 0, None) == EUNSUP
+    # threshold join (host checks happen before any device work)
+    u64, u32 = ctypes.c_uint64, ctypes.c_uint32
+    lib.binsketch_join.argtypes = [vp, u64, vp, u64, u32, u64, u32, vp, u32, u32, vp, vp, ctypes.c_size_t, vp]
+    thr = (ctypes.c_double * 17)(*([0.5] * 17))
+    nan = (ctypes.c_double * 1)(float("nan"))
+    t1 = ctypes.cast(thr, vp)
+    assert lib.binsketch_join(vp(8), 4, vp(8), 4, 64, 10, 4, t1, 1, 0, vp(8), vp(8), 0, None) == 4   # EWORKSPACE
+    assert lib.binsketch_join(None, 4, None, 4, 64, 10, 5, t1, 1, 0, None, None, 0, None) == EINVAL  # 2 bits
+    assert lib.binsketch_join(None, 4, None, 4, 64, 10, 4, t1, 1, 4, None, None, 0, None) == EINVAL  # flags
+    assert lib.binsketch_join(None, 4, None, 4, 64, 10, 4, t1, 0, 0, None, None, 0, None) == EINVAL  # nthr 0
+    assert lib.binsketch_join(None, 4, None, 4, 64, 10, 4, t1, 17, 0, None, None, 0, None) == EINVAL  # nthr 17
+    assert lib.binsketch_join(None, 4, None, 4, 64, 10, 4, None, 1, 0, None, None, 0, None) == EINVAL  # no thr
+    assert lib.binsketch_join(None, 4, None, 4, 64, 10, 4, ctypes.cast(nan, vp), 1, 0, None, None, 0,
+                              None) == EINVAL                                                     # NaN
+    assert lib.binsketch_join(None, 0, None, 4, 64, 10, 4, t1, 16, 0, None, None, 0, None) == 0       # empty
+    assert lib.binsketch_join(None, 4, None, 4, 64, 10, 4, t1, 2, 0, None, None, 0, None) == EINVAL   # nulls
+    assert lib.binsketch_join(vp(8), 4, vp(8), 4, 64, 0, 4, t1, 2, 0, vp(8), None, 0, None) == EINVAL  # d = 0
+    lib.binsketch_join_confusion.argtypes = [vp, vp, u64, u64, vp, vp]
+    assert lib.binsketch_join_confusion(None, None, 0, 5, None, None) == 0
+    assert lib.binsketch_join_confusion(None, None, 3, 5, vp(8), None) == EINVAL
 
 
 def test_product_shares_no_code_with_oracle():
