@@ -72,7 +72,7 @@ enum { BINSKETCH_MAX_K = 256 };            /* largest k binsketch_topk accepts *
 
 /* ops for binsketch_workspace_bytes */
 enum { BINSKETCH_OP_ANDPOPC = 1, BINSKETCH_OP_ESTIMATE = 2, BINSKETCH_OP_TOPK = 3, BINSKETCH_OP_JOIN = 4,
-       BINSKETCH_OP_JOIN_LIST = 5 };
+       BINSKETCH_OP_JOIN_LIST = 5, BINSKETCH_OP_BCS_ESTIMATE = 6 };
 
 /* W = ceil(N/32), words per sketch row. */
 uint32_t binsketch_words(uint32_t N);
@@ -194,6 +194,35 @@ binsketch_status binsketch_join_list(const uint32_t* bits, const uint32_t* queri
  * ratios of these (R-J2). */
 binsketch_status binsketch_join_confusion(const uint32_t* bits_est, const uint32_t* bits_true, uint64_t nq,
                                           uint64_t ndb, int64_t* out, binsketch_stream_t stream);
+
+/* BCS parity sketch (Definition 2; the paper's comparison sketch for IP,
+ * HAM and JS): out_words[r] bit j = parity of the number of entries e of row r with
+ * pi[indices[e]] == j (u_s[j] = sum_{i: b(i) = j} u[i] mod 2). Rows are sets in Definition 2;
+ * a repeated index in a CSR row counts twice and cancels (reading R-B1). Arguments, layout,
+ * errors and the pi table as for binsketch_build / binsketch_build_seeded (same map b = pi). */
+binsketch_status binsketch_bcs_build(const uint32_t* pi, uint64_t d, uint32_t N, const int64_t* indptr,
+                                     const int32_t* indices, uint64_t n, uint32_t* out_words,
+                                     binsketch_stream_t stream);
+binsketch_status binsketch_bcs_build_seeded(uint64_t seed, uint64_t d, uint32_t N, const int64_t* indptr,
+                                            const int32_t* indices, uint64_t n, uint32_t* out_words,
+                                            binsketch_stream_t stream);
+
+/* All-pairs estimates from BCS sketches (readings R-B2, R-B3 — the paper defines the sketch,
+ * not an estimator; SPEC.md:240-243's Hamming inversion, extended to |a| and so to IP/JS/COS):
+ * with m = |a_s XOR b_s| = pa + pb - 2 pab and B[x] = log1p(-2x/N)/log1p(-2/N) (B[0] = 0,
+ * B[x] = d once 2x >= N; see binsketch_bcs_table):
+ *   HAM = min(B[m], d);  n_a = B[pa], n_b = B[pb];  S = n_a + n_b
+ *   IP  = min(max((S - HAM)/2, 0), min(n_a, n_b))
+ *   JS  = (pa == pb == 0) ? 1 : clamp(IP/(S-IP), 0, 1);  COS = (pa == 0 || pb == 0) ? 0 : clamp(IP/sqrt(n_a n_b), 0, 1)
+ * in fp64 in this order, stored as float planes (IP, HAM, JS, COS order) like binsketch_estimate.
+ * Tensor-core engine (pab as in binsketch_andpopc).
+ * ws: >= binsketch_workspace_bytes(BINSKETCH_OP_BCS_ESTIMATE, na, nb, N, 0). */
+binsketch_status binsketch_bcs_estimate(const uint32_t* sketches_a, uint64_t na, const uint32_t* sketches_b,
+                                        uint64_t nb, uint32_t N, uint64_t d, uint32_t measure, float* out,
+                                        void* ws, size_t ws_bytes, binsketch_stream_t stream);
+
+/* The BCS table B (HOST double[N+1]) binsketch_bcs_estimate uploads. */
+binsketch_status binsketch_bcs_table(uint32_t N, uint64_t d, double* host_out);
 
 /* Workspace bytes needed by op (BINSKETCH_OP_*) for na (queries) x nb (db)
  * rows of N-bit sketches and top-k size k (ignored for other ops). Pure

@@ -58,6 +58,10 @@ def _lib_():
         L.orc_join.restype = None
         L.orc_join_exact.argtypes = [vp, vp, u64, vp, vp, u64, u32, vp, u32, u32, vp]
         L.orc_join_exact.restype = None
+        L.orc_bcs_sketch.argtypes = [vp, u64, u32, vp, vp, u64, vp]; L.orc_bcs_sketch.restype = ctypes.c_int
+        L.orc_bcs_table.argtypes = [u32, u64, vp]; L.orc_bcs_table.restype = None
+        L.orc_bcs_estimate_pair.argtypes = [i32, i32, i32, u64, vp, vp]; L.orc_bcs_estimate_pair.restype = None
+        L.orc_bcs_estimate.argtypes = [vp, u64, vp, u64, u32, u64, u32, vp]; L.orc_bcs_estimate.restype = None
         L.orc_enumerate.argtypes = [u32, u32, vp, i64, vp, i64, vp, vp]
         L.orc_enumerate.restype = ctypes.c_int
         _lib = L
@@ -221,6 +225,37 @@ def ranking_metrics(O: list[set], Op: list[set]) -> dict:
     mean = (lambda v: float(np.mean(v)) if v else float("nan"))
     return {"accuracy": mean(acc), "precision": mean(pre), "recall": mean(rec), "f1": mean(f1),
             "query_count": len(acc), "skipped_queries": skipped}
+
+
+def bcs_sketch(pi: np.ndarray, d: int, N: int, indptr: np.ndarray, indices: np.ndarray):
+    """BCS parity sketches: (uint32[n][W], status)."""
+    n = len(indptr) - 1
+    out = np.empty((n, words(N)), dtype=np.uint32)
+    st = _lib_().orc_bcs_sketch(_p(np.ascontiguousarray(pi, dtype=np.uint32)), d, N,
+                                _p(np.ascontiguousarray(indptr, dtype=np.int64)),
+                                _p(np.ascontiguousarray(indices, dtype=np.int32)), n, _p(out))
+    return out, int(st)
+
+
+def bcs_table(N: int, d: int) -> np.ndarray:
+    B = np.empty(N + 1, dtype=np.float64)
+    _lib_().orc_bcs_table(N, d, _p(B))
+    return B
+
+
+def bcs_estimate_pair(pa: int, pb: int, m: int, d: int, B: np.ndarray) -> np.ndarray:
+    out = np.empty(4, dtype=np.float64)
+    _lib_().orc_bcs_estimate_pair(pa, pb, m, d, _p(B), _p(out))
+    return out
+
+
+def bcs_estimate(A: np.ndarray, B: np.ndarray, N: int, d: int, measure: int) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.uint32)
+    B = np.ascontiguousarray(B, dtype=np.uint32)
+    planes = bin(measure & 15).count("1")
+    out = np.empty((planes, A.shape[0], B.shape[0]), dtype=np.float32)
+    _lib_().orc_bcs_estimate(_p(A), A.shape[0], _p(B), B.shape[0], N, d, measure, _p(out))
+    return out
 
 
 def enumerate_expectations(d: int, N: int, a, b):

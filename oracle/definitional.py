@@ -121,3 +121,26 @@ def topk_bruteforce(keys: list[float], k: int, exclude: int | None = None):
     """Indices of the k best keys under (key desc, index asc) (reading R-G17)."""
     order = sorted((j for j in range(len(keys)) if j != exclude), key=lambda j: (-keys[j], j))
     return order[:k]
+
+
+# ---- BCS (PAPER.md:321-331, Definition 2) ----
+def bcs_sketch_bits(a_dense: list[int], b_map: list[int], N: int) -> list[int]:
+    """u_s[j] = sum_{i : b(i) = j} u[i] mod 2, literally."""
+    return [sum(a_dense[i] for i in range(len(a_dense)) if b_map[i] == j) % 2 for j in range(N)]
+
+
+def bcs_table(N: int, d: int) -> list[float]:
+    """B[x] = ln(1-2x/N)/ln(1-2/N) (log1p form), B[0] = 0, d once 2x >= N (R-B2)."""
+    return [0.0] + [float(d) if 2 * x >= N else math.log1p(-2.0 * x / N) / math.log1p(-2.0 / N)
+                    for x in range(1, N + 1)]
+
+
+def bcs_estimate(pa: int, pb: int, m: int, d: int, B: list[float]):
+    """(IP, HAM, JS, COS) from BCS popcounts (R-B2, R-B3), same operation order as oracle.cpp."""
+    na, nb = B[pa], B[pb]
+    ham = min(B[m], float(d))
+    S = na + nb
+    ip = min(max((S - ham) * 0.5, 0.0), min(na, nb))
+    js = 1.0 if (pa == 0 and pb == 0) else min(max(ip / (S - ip), 0.0), 1.0)
+    cs = 0.0 if (pa == 0 or pb == 0) else min(max(ip / math.sqrt(na * nb), 0.0), 1.0)
+    return ip, ham, js, cs

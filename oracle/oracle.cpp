@@ -410,6 +410,81 @@ void orc_join_exact(const int64_t* qptr, const int32_t* qidx, uint64_t nq, const
 }
 
 // ---------------------------------------------------------------------------
+// BCS parity sketch, PAPER.md:321-331 (Definition 2):
+//   u_s[j] = sum_{i : b(i) = j} u[i]  (mod 2),  b = the same random map pi.
+// A CSR row is read as the multiset of its entries (reading R-B1): each entry
+// toggles its bucket, so a repeated index cancels.
+// ---------------------------------------------------------------------------
+int orc_bcs_sketch(const uint32_t* pi, uint64_t d, uint32_t N, const int64_t* indptr, const int32_t* indices,
+                   uint64_t n, uint32_t* out) {
+  const uint64_t W = orc_words(N);
+  int status = 0;
+  for (uint64_t r = 0; r < n; ++r) {
+    uint32_t* row = out + r * W;
+    for (uint64_t w = 0; w < W; ++w) row[w] = 0;
+    if (indptr[r + 1] < indptr[r]) { status = 1; continue; }
+    for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) {
+      const int64_t i = indices[e - indptr[0]];
+      if (i < 0 || (uint64_t)i >= d || pi[i] >= N) { status = 1; continue; }
+      const uint32_t j = pi[i];
+      row[j / 32] ^= 1u << (j % 32);
+    }
+  }
+  return status;
+}
+
+// BCS estimator table (R-B2, SPEC.md:240-243 inverted parity-collision law):
+//   B[0] = 0;  B[x] = d if 2x >= N, else ln(1 - 2x/N) / ln(1 - 2/N)  (log1p form, as R-G11)
+void orc_bcs_table(uint32_t N, uint64_t d, double* B) {
+  B[0] = 0.0;
+  for (uint32_t x = 1; x <= N; ++x)
+    B[x] = (2.0 * (double)x >= (double)N) ? (double)d : std::log1p(-2.0 * (double)x / (double)N) / std::log1p(-2.0 / (double)N);
+}
+
+// BCS estimates (R-B2, R-B3) from pa = |a_s|, pb = |b_s| and m = |a_s XOR b_s|:
+//   HAM = min(B[m], d); n_a = B[pa]; n_b = B[pb]; S = n_a + n_b
+//   IP = min(max((S - HAM) * 0.5, 0), min(n_a, n_b))
+//   JS = (pa == 0 && pb == 0) ? 1 : clamp(IP / (S - IP), 0, 1)
+//   COS = (pa == 0 || pb == 0) ? 0 : clamp(IP / sqrt(n_a * n_b), 0, 1)
+// out = {IP, HAM, JS, COS}.
+void orc_bcs_estimate_pair(int32_t pa, int32_t pb, int32_t m, uint64_t d, const double* B, double* out) {
+  const double na = B[pa], nb = B[pb];
+  const double h = B[m];
+  const double ham = std::min(h, (double)d);
+  const double S = na + nb;
+  const double ip = std::min(std::max((S - ham) * 0.5, 0.0), std::min(na, nb));
+  double js, cs;
+  if (pa == 0 && pb == 0) js = 1.0;
+  else js = std::min(std::max(ip / (S - ip), 0.0), 1.0);
+  if (pa == 0 || pb == 0) cs = 0.0;
+  else cs = std::min(std::max(ip / std::sqrt(na * nb), 0.0), 1.0);
+  out[0] = ip; out[1] = ham; out[2] = js; out[3] = cs;
+}
+
+// All pairs from BCS sketches; m from the XOR popcount of the words (planes as orc_estimate).
+void orc_bcs_estimate(const uint32_t* A, uint64_t na, const uint32_t* Bm, uint64_t nb, uint32_t N, uint64_t d,
+                      uint32_t measure, float* out) {
+  const uint64_t W = orc_words(N);
+  std::vector<double> T(N + 1);
+  orc_bcs_table(N, d, T.data());
+  int planes[4], np = 0;
+  for (int m = 0; m < 4; ++m)
+    if (measure & (1u << m)) planes[np++] = m;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)na; ++i) {
+    const int pa = popcount_row(A + (uint64_t)i * W, W);
+    for (uint64_t j = 0; j < nb; ++j) {
+      const int pb = popcount_row(Bm + j * W, W);
+      int x = 0;
+      for (uint64_t w = 0; w < W; ++w) x += popc_fast(A[(uint64_t)i * W + w] ^ Bm[j * W + w]);
+      double e[4];
+      orc_bcs_estimate_pair(pa, pb, x, d, T.data(), e);
+      for (int p = 0; p < np; ++p) out[((uint64_t)p * na + (uint64_t)i) * nb + j] = (float)e[planes[p]];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Exhaustive enumeration of Lemma 1's expectations: the
 // mean of |a_s| and of <a_s,b_s> over ALL N^d maps pi, computed by sketching
 // with every map (orc_sketch) and counting bits. a, b are sorted supports in

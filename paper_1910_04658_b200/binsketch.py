@@ -20,7 +20,7 @@ IP, HAM, JS, COS = 1, 2, 4, 8
 MEASURES = {"ip": IP, "ham": HAM, "js": JS, "cos": COS}
 TOPK_EXCLUDE_SELF = 1
 MAX_K = 256
-OP_ANDPOPC, OP_ESTIMATE, OP_TOPK, OP_JOIN, OP_JOIN_LIST = 1, 2, 3, 4, 5
+OP_ANDPOPC, OP_ESTIMATE, OP_TOPK, OP_JOIN, OP_JOIN_LIST, OP_BCS_ESTIMATE = 1, 2, 3, 4, 5, 6
 JOIN_EXCLUDE_SELF, JOIN_EXACT = 1, 2
 MAX_THRESHOLDS = 16
 
@@ -35,6 +35,10 @@ SIGNATURES = {
     "binsketch_make_pi": (_int, [_u64, _u64, _u32, _vp, _vp]),
     "binsketch_build": (_int, [_vp, _u64, _u32, _vp, _vp, _u64, _vp, _vp]),
     "binsketch_build_seeded": (_int, [_u64, _u64, _u32, _vp, _vp, _u64, _vp, _vp]),
+    "binsketch_bcs_build": (_int, [_vp, _u64, _u32, _vp, _vp, _u64, _vp, _vp]),
+    "binsketch_bcs_build_seeded": (_int, [_u64, _u64, _u32, _vp, _vp, _u64, _vp, _vp]),
+    "binsketch_bcs_estimate": (_int, [_vp, _u64, _vp, _u64, _u32, _u64, _u32, _vp, _vp, _sz, _vp]),
+    "binsketch_bcs_table": (_int, [_u32, _u64, _vp]),
     "binsketch_popcount": (_int, [_vp, _u64, _u32, _vp, _vp]),
     "binsketch_andpopc": (_int, [_vp, _u64, _vp, _u64, _u32, _vp, _vp, _sz, _vp]),
     "binsketch_estimate": (_int, [_vp, _u64, _vp, _u64, _u32, _u64, _u32, _vp, _vp, _sz, _vp]),
@@ -138,6 +142,51 @@ def build_seeded(seed: int, d: int, N: int, indptr: torch.Tensor, indices: torch
         seed, d, N, _dev(indptr, torch.int64, "indptr"),
         _dev(indices, torch.int32, "indices") if indices.numel() else None, n,
         _words_tensor(out, "out") if out.numel() else None, _stream()))
+    return out
+
+
+def bcs_build(pi: torch.Tensor, d: int, N: int, indptr: torch.Tensor, indices: torch.Tensor,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+    """BCS parity sketches with a pi table."""
+    n = indptr.numel() - 1
+    if out is None:
+        out = torch.empty((n, words(N)), dtype=torch.int32, device="cuda")
+    _check("binsketch_bcs_build", _lib().binsketch_bcs_build(
+        _words_tensor(pi, "pi") if pi.numel() else None, d, N, _dev(indptr, torch.int64, "indptr"),
+        _dev(indices, torch.int32, "indices") if indices.numel() else None, n,
+        _words_tensor(out, "out") if out.numel() else None, _stream()))
+    return out
+
+
+def bcs_build_seeded(seed: int, d: int, N: int, indptr: torch.Tensor, indices: torch.Tensor,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    n = indptr.numel() - 1
+    if out is None:
+        out = torch.empty((n, words(N)), dtype=torch.int32, device="cuda")
+    _check("binsketch_bcs_build_seeded", _lib().binsketch_bcs_build_seeded(
+        seed, d, N, _dev(indptr, torch.int64, "indptr"),
+        _dev(indices, torch.int32, "indices") if indices.numel() else None, n,
+        _words_tensor(out, "out") if out.numel() else None, _stream()))
+    return out
+
+
+def bcs_estimate(A: torch.Tensor, B: torch.Tensor, N: int, d: int, measure: int = 15,
+                 out: torch.Tensor | None = None, ws=None) -> torch.Tensor:
+    na, nb = A.shape[0], B.shape[0]
+    planes = bin(measure & 15).count("1")
+    if out is None:
+        out = torch.empty((planes, na, nb), dtype=torch.float32, device="cuda")
+    ws, wp, wn = _workspace(OP_BCS_ESTIMATE, na, nb, N, 0, ws)
+    _check("binsketch_bcs_estimate", _lib().binsketch_bcs_estimate(
+        _words_tensor(A, "A") if na else None, na, _words_tensor(B, "B") if nb else None, nb, N, d, measure,
+        _dev(out, torch.float32, "out") if out.numel() else None, wp, wn, _stream()))
+    return out
+
+
+def bcs_table(N: int, d: int):
+    import numpy as np
+    out = np.empty(N + 1, dtype=np.float64)
+    _check("binsketch_bcs_table", _lib().binsketch_bcs_table(N, d, out.ctypes.data))
     return out
 
 

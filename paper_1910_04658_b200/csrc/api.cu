@@ -11,6 +11,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <utility>
 
 #include "binsketch.h"
@@ -24,9 +25,11 @@ inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 // Cardinality table, Algorithm 1 line 3 with q = 1 - 1/N
 // (PAPER.md:358): L[k] = ln(1-k/N)/ln(q) evaluated as log1p(-k/N)/log1p(-1/N)
 // (reading R-G11); L[N] = d (saturation, R-G12).
+// BCS table (R-B2): B[x] = log1p(-2x/N)/log1p(-2/N) for 0 < 2x < N, B[0] = 0, B[x] = d once
+// 2x >= N (the parity-collision law inverted; cached under kind 1).
 struct TableCache {
   std::mutex mu;
-  std::map<std::pair<uint32_t, uint64_t>, double*> tables;
+  std::map<std::tuple<uint32_t, uint64_t, int>, double*> tables;
   std::map<std::pair<uint32_t, uint64_t>, bool> convex_;
 
   // L non-decreasing with non-decreasing increments (to 1e-9 relative): the condition
@@ -51,9 +54,9 @@ struct TableCache {
     return ok;
   }
 
-  const double* get(uint32_t N, uint64_t d) {
+  const double* get(uint32_t N, uint64_t d, int kind = 0) {
     std::lock_guard<std::mutex> lock(mu);
-    auto key = std::make_pair(N, d);
+    auto key = std::make_tuple(N, d, kind);
     auto it = tables.find(key);
     if (it != tables.end()) return it->second;
     double* t = nullptr;
@@ -63,9 +66,16 @@ struct TableCache {
       t = static_cast<double*>(std::malloc((size_t)(N + 1) * sizeof(double)));
       if (!t) return nullptr;
     }
-    const double c = std::log1p(-1.0 / (double)N);
-    for (uint32_t k = 0; k < N; ++k) t[k] = std::log1p(-(double)k / (double)N) / c;
-    t[N] = (double)d;
+    if (kind == 0) {
+      const double c = std::log1p(-1.0 / (double)N);
+      for (uint32_t k = 0; k < N; ++k) t[k] = std::log1p(-(double)k / (double)N) / c;
+      t[N] = (double)d;
+    } else {
+      const double c = std::log1p(-2.0 / (double)N);
+      t[0] = 0.0;
+      for (uint32_t k = 1; k <= N; ++k)
+        t[k] = (2.0 * (double)k >= (double)N) ? (double)d : std::log1p(-2.0 * (double)k / (double)N) / c;
+    }
     tables.emplace(key, t);
     return t;
   }
@@ -124,6 +134,13 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
     l.total = off;
     return l;
   }
+  if (op == BINSKETCH_OP_BCS_ESTIMATE) {   // always the tensor-core engine
+    l.ctr = off; off += kAlign;
+    l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
+    l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
+    l.total = off;
+    return l;
+  }
   if (op == BINSKETCH_OP_JOIN_LIST) {
     l.cnt = off; off += align_up((size_t)na * 4);
     l.total = off;
@@ -165,8 +182,8 @@ inline binsketch_status cuda_status(cudaError_t e) { return e == cudaSuccess ? B
 
 inline bool one_bit(uint32_t m) { return m == 1u || m == 2u || m == 4u || m == 8u; }
 
-binsketch_status upload_table(uint32_t N, uint64_t d, void* ws, const Layout& l, cudaStream_t s) {
-  const double* t = cache().get(N, d);
+binsketch_status upload_table(uint32_t N, uint64_t d, void* ws, const Layout& l, cudaStream_t s, int kind = 0) {
+  const double* t = cache().get(N, d, kind);
   if (!t) return BINSKETCH_ECUDA;
   return cuda_status(cudaMemcpyAsync(static_cast<char*>(ws) + l.L, t, (size_t)(N + 1) * 8,
                                      cudaMemcpyHostToDevice, s));
@@ -195,14 +212,14 @@ binsketch_status binsketch_make_pi(uint64_t seed, uint64_t d, uint32_t N, uint32
 
 static binsketch_status build_common(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t N,
                                      const int64_t* indptr, const int32_t* indices, uint64_t n,
-                                     uint32_t* out, binsketch_stream_t stream) {
+                                     uint32_t* out, binsketch_stream_t stream, bool parity = false) {
   if (N < 2) return BINSKETCH_EINVAL;
   if (n == 0) return BINSKETCH_OK;
   if (d == 0 || indptr == nullptr || indices == nullptr || out == nullptr) return BINSKETCH_EINVAL;
   if (d > 0x80000000ull) return BINSKETCH_EINVAL;  // int32 indices cannot address more
   if (!bsk::status_ptr()) return BINSKETCH_ECUDA;
   return cuda_status(bsk::launch_build(pi, seed, d, N, indptr, indices, n, out,
-                                       reinterpret_cast<cudaStream_t>(stream)));
+                                       reinterpret_cast<cudaStream_t>(stream), parity));
 }
 
 binsketch_status binsketch_build(const uint32_t* pi, uint64_t d, uint32_t N, const int64_t* indptr,
@@ -216,6 +233,19 @@ binsketch_status binsketch_build_seeded(uint64_t seed, uint64_t d, uint32_t N, c
                                         const int32_t* indices, uint64_t n, uint32_t* out_words,
                                         binsketch_stream_t stream) {
   return build_common(nullptr, seed, d, N, indptr, indices, n, out_words, stream);
+}
+
+binsketch_status binsketch_bcs_build(const uint32_t* pi, uint64_t d, uint32_t N, const int64_t* indptr,
+                                     const int32_t* indices, uint64_t n, uint32_t* out_words,
+                                     binsketch_stream_t stream) {
+  if (n > 0 && pi == nullptr) return BINSKETCH_EINVAL;
+  return build_common(pi, 0, d, N, indptr, indices, n, out_words, stream, true);
+}
+
+binsketch_status binsketch_bcs_build_seeded(uint64_t seed, uint64_t d, uint32_t N, const int64_t* indptr,
+                                            const int32_t* indices, uint64_t n, uint32_t* out_words,
+                                            binsketch_stream_t stream) {
+  return build_common(nullptr, seed, d, N, indptr, indices, n, out_words, stream, true);
 }
 
 binsketch_status binsketch_popcount(const uint32_t* sk, uint64_t n, uint32_t N, int32_t* out,
@@ -438,6 +468,43 @@ binsketch_status binsketch_join_confusion(const uint32_t* bits_est, const uint32
   if (nq == 0) return BINSKETCH_OK;
   if (!out || (ndb > 0 && (!bits_est || !bits_true))) return BINSKETCH_EINVAL;
   return cuda_status(bsk::launch_join_confusion(bits_est, bits_true, nq, ndb, out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+binsketch_status binsketch_bcs_estimate(const uint32_t* sketches_a, uint64_t na, const uint32_t* sketches_b,
+                                        uint64_t nb, uint32_t N, uint64_t d, uint32_t measure, float* out, void* ws,
+                                        size_t ws_bytes, binsketch_stream_t stream) {
+  if (N < 2 || measure == 0 || (measure & ~15u)) return BINSKETCH_EINVAL;
+  if (na == 0 || nb == 0) return BINSKETCH_OK;
+  if (!sketches_a || !sketches_b || !out || d == 0) return BINSKETCH_EINVAL;
+  const Layout l = layout(BINSKETCH_OP_BCS_ESTIMATE, na, nb, N, 0);
+  if (!ws || ws_bytes < l.total) return BINSKETCH_EWORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  binsketch_status st = upload_table(N, d, ws, l, s, 1);
+  if (st != BINSKETCH_OK) return st;
+  const uint32_t W = binsketch_words(N);
+  int32_t* pa = reinterpret_cast<int32_t*>(w + l.pa);
+  int32_t* pb = reinterpret_cast<int32_t*>(w + l.pb);
+  uint8_t* a8 = reinterpret_cast<uint8_t*>(w + l.a8);
+  const bool self = sketches_a == sketches_b && na == nb;
+  uint8_t* b8 = self ? a8 : reinterpret_cast<uint8_t*>(w + l.b8);
+  cudaError_t e = bsk::launch_popcount(sketches_a, na, W, pa, s);
+  if (e == cudaSuccess) e = self ? cudaMemcpyAsync(pb, pa, na * 4, cudaMemcpyDeviceToDevice, s)
+                                 : bsk::launch_popcount(sketches_b, nb, W, pb, s);
+  if (e == cudaSuccess) e = bsk::launch_expand(sketches_a, na, N, a8, s);
+  if (e == cudaSuccess && !self) e = bsk::launch_expand(sketches_b, nb, N, b8, s);
+  if (e == cudaSuccess)
+    e = bsk::launch_tc_estimate(a8, na, b8, nb, N, measure, pa, pb, reinterpret_cast<const double*>(w + l.L), out,
+                                reinterpret_cast<unsigned long long*>(w + l.ctr), s, true, (double)d);
+  return cuda_status(e);
+}
+
+binsketch_status binsketch_bcs_table(uint32_t N, uint64_t d, double* host_out) {
+  if (N < 2 || !host_out) return BINSKETCH_EINVAL;
+  const double* t = cache().get(N, d, 1);
+  if (!t) return BINSKETCH_ECUDA;
+  for (uint32_t k = 0; k <= N; ++k) host_out[k] = t[k];
+  return BINSKETCH_OK;
 }
 
 binsketch_status binsketch_card_table(uint32_t N, uint64_t d, double* host_out) {

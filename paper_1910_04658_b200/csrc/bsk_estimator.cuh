@@ -60,6 +60,49 @@ __device__ __forceinline__ Est estimate_pair(int pa, int pb, int pab, int N, con
 }
 
 
+// BCS (Definition 2) estimates from parity sketches (readings R-B2, R-B3;
+// the paper gives the sketch, not an estimator): a bucket's parity differs between a_s and
+// b_s with probability (1 - (1-2/N)^h)/2 for h = |a XOR b|, so with the table
+// B[x] = log1p(-2x/N)/log1p(-2/N) (B[0] = 0, B[x] = d once 2x >= N) and
+// m = |a_s XOR b_s| = pa + pb - 2 pab:
+//   HAM = min(B[m], d);  n_a = B[pa], n_b = B[pb] (the same law for |a|);  S = n_a + n_b
+//   IP  = min(max((S - HAM)/2, 0), min(n_a, n_b));  JS / COS as in the BinSketch recipe.
+__device__ __forceinline__ Est bcs_estimate_pair(int pa, int pb, int pab, double dcap, const double* __restrict__ B,
+                                                 uint32_t need) {
+  Est r;
+  const double na = B[pa], nb = B[pb];
+  const double h = B[pa + pb - 2 * pab];
+  const double ham = h < dcap ? h : dcap;
+  const double S = __dadd_rn(na, nb);
+  double ip = __dmul_rn(__dsub_rn(S, ham), 0.5);
+  ip = ip > 0.0 ? ip : 0.0;
+  const double cap = na < nb ? na : nb;
+  ip = ip < cap ? ip : cap;
+  r.ip = ip;
+  r.ham = ham;
+  r.js = 0.0;
+  r.cs = 0.0;
+  if (need & 4u) {
+    if (pa == 0 && pb == 0) {
+      r.js = 1.0;
+    } else {
+      double v = __ddiv_rn(ip, __dsub_rn(S, ip));
+      v = v > 0.0 ? v : 0.0;
+      r.js = v < 1.0 ? v : 1.0;
+    }
+  }
+  if (need & 8u) {
+    if (pa == 0 || pb == 0) {
+      r.cs = 0.0;
+    } else {
+      double v = __ddiv_rn(ip, __dsqrt_rn(__dmul_rn(na, nb)));
+      v = v > 0.0 ? v : 0.0;
+      r.cs = v < 1.0 ? v : 1.0;
+    }
+  }
+  return r;
+}
+
 // Exact similarity key of two uncompressed rows from (|a|, |b|, |a AND b|) — the threshold
 // join's ground truth (Exp. 2's O): the recipe above with L = identity
 // (no estimation), keys as in measure_key (-HAM for Hamming). Integers up to 2^31 are exact

@@ -30,10 +30,10 @@ int num_sms();
 
 cudaError_t launch_make_pi(uint64_t seed, uint64_t d, uint32_t N, uint32_t* pi, cudaStream_t s);
 
-// pi == nullptr -> seeded (in-kernel pi); else table gather.
+// pi == nullptr -> seeded (in-kernel pi); else table gather. parity: BCS (XOR) instead of OR.
 cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t N,
                          const int64_t* indptr, const int32_t* indices, uint64_t n,
-                         uint32_t* out, cudaStream_t s);
+                         uint32_t* out, cudaStream_t s, bool parity = false);
 
 cudaError_t launch_popcount(const uint32_t* sk, uint64_t n, uint32_t W, int32_t* out, cudaStream_t s);
 
@@ -64,9 +64,10 @@ cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* o
 // ctr: one 8-byte device word of workspace (dynamic tile scheduler; reset by the launcher).
 cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
                               int32_t* out, unsigned long long* ctr, cudaStream_t s);
+// bcs: BCS parity sketches, L = the BCS table, dcap = d (bcs_estimate_pair).
 cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
                                uint32_t measure, const int32_t* pa, const int32_t* pb, const double* L, float* out,
-                               unsigned long long* ctr, cudaStream_t s);
+                               unsigned long long* ctr, cudaStream_t s, bool bcs = false, double dcap = 0.0);
 // Fused top-k on the tensor-core engine for k <= tc_topk_max_k(); partial lists
 // [nq][tc_topk_splits][k] in the workspace, then the merge kernel. `prefilter` enables
 // the integer L[pab] bound (valid when L is non-decreasing and convex).

@@ -161,6 +161,14 @@ __device__ __forceinline__ void sts_v4(uint32_t a, uint32_t x, uint32_t y, uint3
 __device__ __forceinline__ void red_or_shared(uint32_t a, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
 }
+__device__ __forceinline__ void red_xor_shared(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+// A sketch bit: OR (BinSketch) or XOR (BCS parity buckets).
+template <bool XOR>
+__device__ __forceinline__ void put_bit(uint32_t a, uint32_t v) {
+  if (XOR) red_xor_shared(a, v); else red_or_shared(a, v);
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -231,8 +239,8 @@ template <int K>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K)); }
 
 // LOGN > 0: N = 2^LOGN >= 32 compiled in (sketch-word and row shifts become immediates);
-// LOGN = 0: any N.
-template <int MODE, int LOGN, bool VEC>
+// LOGN = 0: any N. XOR: BCS parity sketch (bits toggled instead of set).
+template <int MODE, int LOGN, bool VEC, bool XOR>
 __global__ void __launch_bounds__(BuildCfg<MODE>::kThreads, BuildCfg<MODE>::kBlocks)
 build_kernel(const BuildParams p) {
   constexpr int NS = BuildCfg<MODE>::kStages;
@@ -396,7 +404,7 @@ build_kernel(const BuildParams p) {
             maxj = max(maxj, jj);
             jj = min(jj, N - 1);
           }
-          red_or_shared(ra + ((jj >> 5) << 2), 1u << (jj & 31u));
+          put_bit<XOR>(ra + ((jj >> 5) << 2), 1u << (jj & 31u));
         }
       }
     } else if (ok) {
@@ -505,12 +513,12 @@ build_kernel(const BuildParams p) {
           }
           if (FULL) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) red_or_shared(addr[u] + (j[u] >> 3), bit[u]);
+            for (int u = 0; u < 8; ++u) put_bit<XOR>(addr[u] + (j[u] >> 3), bit[u]);
           } else {   // tile tail: skip the zero-filled elements (they would all hit one word)
             const int rem = span - wb;
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-              if (128 * (u >> 2) + 4 * lane + (u & 3) < rem) red_or_shared(addr[u] + (j[u] >> 3), bit[u]);
+              if (128 * (u >> 2) + 4 * lane + (u & 3) < rem) put_bit<XOR>(addr[u] + (j[u] >> 3), bit[u]);
           }
         };
         if (ws + kStage <= span) {
@@ -556,9 +564,9 @@ build_kernel(const BuildParams p) {
 }
 
 // Fallback for very wide sketches (one row's W words do not fit a warp's share of
-// shared memory): rows zeroed by cudaMemsetAsync, then global atomicOr.
+// shared memory): rows zeroed by cudaMemsetAsync, then global atomicOr (atomicXor: BCS).
 __global__ void build_wide_kernel(const uint32_t* __restrict__ pi, uint64_t seed, uint64_t d, ModN mn,
-                                  bool seeded, const int64_t* __restrict__ indptr,
+                                  bool seeded, bool parity, const int64_t* __restrict__ indptr,
                                   const int32_t* __restrict__ indices, uint64_t n,
                                   uint32_t* __restrict__ out, uint32_t W, unsigned int* status) {
   const int lane = threadIdx.x & 31;
@@ -573,7 +581,8 @@ __global__ void build_wide_kernel(const uint32_t* __restrict__ pi, uint64_t seed
       if (idx < 0 || (uint64_t)idx >= d) { bad = kStatusIndex; continue; }
       uint32_t j = seeded ? pi_seeded(seed, (uint64_t)idx, mn) : __ldg(pi + idx);
       if (j >= mn.N) { bad = kStatusIndex; continue; }
-      atomicOr(out + r * W + (j >> 5), 1u << (j & 31u));
+      if (parity) atomicXor(out + r * W + (j >> 5), 1u << (j & 31u));
+      else atomicOr(out + r * W + (j >> 5), 1u << (j & 31u));
     }
   }
   if (bad) latch(status, bad);
@@ -587,7 +596,7 @@ static uint32_t bits_for(uint64_t v) {   // number of bits to represent 0..v
 
 cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t N,
                          const int64_t* indptr, const int32_t* indices, uint64_t n,
-                         uint32_t* out, cudaStream_t s) {
+                         uint32_t* out, cudaStream_t s, bool parity) {
   if (n == 0) return cudaSuccess;
   const uint32_t W = (N + 31) / 32;
   const ModN mn = make_modn(N);
@@ -639,7 +648,7 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
   if (RW == 0) {
     cudaError_t e = cudaMemsetAsync(out, 0, n * (size_t)W * 4, s);
     if (e != cudaSuccess) return e;
-    build_wide_kernel<<<sms * 8, 256, 0, s>>>(pi, seed, d, mn, pi == nullptr, indptr, indices, n, out, W, st);
+    build_wide_kernel<<<sms * 8, 256, 0, s>>>(pi, seed, d, mn, pi == nullptr, parity, indptr, indices, n, out, W, st);
     count_launch();
     return cudaGetLastError();
   }
@@ -653,16 +662,22 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
   const uint64_t want = (ntiles + (threads / 32) - 1) / (threads / 32);
   const int fit = (int)std::max<size_t>(1, std::min<size_t>((size_t)bps, optin / std::max<size_t>(smem, 1)));
   const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms * fit));
-  // compiled-in sketch widths: the configs' N = 1024 (W = 32) and 4096 (W = 128)
-  const int logn = N == 1024 ? 10 : (N == 4096 ? 12 : 0);
+  // compiled-in sketch widths: the configs' N = 1024 (W = 32) and 4096 (W = 128); the BCS
+  // parity variant is instantiated for the generic width only
+  const int logn = parity ? 0 : (N == 1024 ? 10 : (N == 4096 ? 12 : 0));
   const bool vec = (reinterpret_cast<uintptr_t>(indices) & 15u) == 0;
   cudaError_t e = cudaSuccess;
-#define BSK_LAUNCH_BUILD3(M, LN, V)                                                                           \
-  do {                                                                                                        \
-    e = cudaFuncSetAttribute(build_kernel<M, LN, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    if (e != cudaSuccess) return e;                                                                           \
-    build_kernel<M, LN, V><<<(unsigned)blocks, threads, smem, s>>>(bp);                                       \
-    count_launch();                                                                                           \
+#define BSK_LAUNCH_BUILD4(M, LN, V, X)                                                                           \
+  do {                                                                                                           \
+    e = cudaFuncSetAttribute(build_kernel<M, LN, V, X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                              \
+    build_kernel<M, LN, V, X><<<(unsigned)blocks, threads, smem, s>>>(bp);                                       \
+    count_launch();                                                                                              \
+  } while (0)
+#define BSK_LAUNCH_BUILD3(M, LN, V)                       \
+  do {                                                    \
+    if (LN == 0 && parity) BSK_LAUNCH_BUILD4(M, 0, V, true); \
+    else BSK_LAUNCH_BUILD4(M, LN, V, false);              \
   } while (0)
 #define BSK_LAUNCH_BUILD2(M, LN)                 \
   do {                                           \
@@ -685,6 +700,7 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
 #undef BSK_LAUNCH_BUILD
 #undef BSK_LAUNCH_BUILD2
 #undef BSK_LAUNCH_BUILD3
+#undef BSK_LAUNCH_BUILD4
   return cudaGetLastError();
 }
 

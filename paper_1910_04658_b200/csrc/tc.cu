@@ -251,6 +251,8 @@ struct TcParams {
   uint32_t* bits;         // kTcJoin: match bitmaps [nthr][na][wpr] (zeroed before the launch)
   uint64_t wpr;           // kTcJoin: words per bitmap row = ceil(nb / 32)
   uint32_t nthr, exact;   // kTcJoin: threshold count; exact similarities (L = identity) instead of estimates
+  uint32_t bcs;           // kTcEstimate: BCS parity sketches (L = the BCS table B, dcap = d)
+  double dcap;
   double tkey[kTcMaxThr];     // kTcJoin: threshold keys, descending
   uint32_t tslot[kTcMaxThr];  // kTcJoin: bitmap plane of each key
 };
@@ -836,7 +838,8 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               if ((uint64_t)j >= left) break;
-              const Est e = estimate_pair(pa, __ldg(p.pb + cb + j), (int)v[j], (int)p.N, L, m);
+              const Est e = p.bcs ? bcs_estimate_pair(pa, __ldg(p.pb + cb + j), (int)v[j], p.dcap, L, m)
+                                  : estimate_pair(pa, __ldg(p.pb + cb + j), (int)v[j], (int)p.N, L, m);
               float* o = p.out_f32 + r * p.nb + cb + j;
               if (m & 1u) { __stcs(o, __double2float_rn(e.ip)); o += plane; }
               if (m & 2u) { __stcs(o, __double2float_rn(e.ham)); o += plane; }
@@ -984,10 +987,11 @@ cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8,
 
 cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
                                uint32_t measure, const int32_t* pa, const int32_t* pb, const double* L, float* out,
-                               unsigned long long* ctr, cudaStream_t s) {
+                               unsigned long long* ctr, cudaStream_t s, bool bcs, double dcap) {
   if (na == 0 || nb == 0) return cudaSuccess;
   TcParams p = {};
   p.na = na; p.nb = nb; p.N = N; p.measure = measure; p.pa = pa; p.pb = pb; p.L = L; p.out_f32 = out;
+  p.bcs = bcs ? 1u : 0u; p.dcap = dcap;
   p.item_ctr = ctr;
   const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
   p.l_smem = (lb <= 64 * 1024) ? lb : 0;

@@ -34,7 +34,7 @@ def _declared():
 
 def test_exports_every_declared_symbol(lib):
     names = _declared()
-    assert len(names) == 17
+    assert len(names) == 21
     for name in names:
         assert hasattr(lib, name), name
     from paper_1910_04658_b200.binsketch import SIGNATURES
@@ -61,6 +61,14 @@ def test_card_table_bit_identical_to_oracle(lib, N, d):
     out = np.empty(N + 1, dtype=np.float64)
     assert lib.binsketch_card_table(N, d, out.ctypes.data) == 0
     assert out.tobytes() == oracle.card_table(N, d).tobytes()
+
+
+def test_bcs_table_bit_identical_to_oracle(lib):
+    lib.binsketch_bcs_table.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p]
+    for N, d in ((2, 10), (1024, 50_000), (4096, 102_660), (1223, 5000)):
+        out = np.empty(N + 1, dtype=np.float64)
+        assert lib.binsketch_bcs_table(N, d, out.ctypes.data) == 0
+        assert out.tobytes() == oracle.bcs_table(N, d).tobytes()
 
 
 def test_workspace_sizing(lib):
