@@ -108,6 +108,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "memory");
 }
 
+// 32 lanes x 8 consecutive columns.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+      : "r"(taddr)
+      : "memory");
+}
+
 // Split form for software pipelining: issue a load without waiting, and a wait that
 // names the destination registers as in/out operands (so no use is scheduled before it).
 __device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&v)[32]) {
@@ -200,12 +210,21 @@ __global__ void pb_scatter_kernel(const int32_t* __restrict__ pb, uint64_t n, ui
 // (SWIZZLE_128B) for the plain AND-popcount, KC = 64 (SWIZZLE_64B, half-size stages, so
 // deeper rings fit next to the estimator table / per-row top-k heaps) otherwise.
 constexpr int kTcM = 128, kTcN = 256;
-constexpr uint32_t kTcThreads = 192;                       // producer, MMA, 4 epilogue warps
 constexpr uint32_t kTcSmemMax = 227 * 1024;
 // instruction descriptor: D s32, A/B u8, K-major, N = 256, M = 128
 constexpr uint32_t kTcIdesc = (2u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
 enum TcMode { kTcAndPopc = 0, kTcEstimate = 1, kTcTopk = 2, kTcJoin = 3 };
 constexpr uint32_t kTcMaxThr = 16;   // thresholds per join launch
+
+// Roles per mode: warp 0 TMA producer, warp 1 MMA issuer, then kEpi epilogue warps (kEpi/4 per
+// TMEM lane quadrant, each owning 256/(kEpi/4) columns of the tile). The estimate epilogue (fp64
+// recipe per pair, latency-bound) runs 16 warps reading 8-column chunks; the others 4 warps.
+template <int MODE>
+struct TcRoles {
+  static constexpr int kEpi = MODE == kTcEstimate ? 16 : 4;
+  static constexpr uint32_t kThreads = 64 + 32 * kEpi;
+  static constexpr int kCW = MODE == kTcEstimate ? 8 : 32;   // columns per TMEM load (andpopc / estimate)
+};
 
 template <int KC>
 struct TcGeom {
@@ -258,7 +277,7 @@ struct TcParams {
 };
 
 template <int MODE, int KC>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(TcRoles<MODE>::kThreads, 1)
 tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
   using G = TcGeom<KC>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -283,8 +302,8 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
   if (warp == 0 && lane == 0) {
     for (uint32_t s = 0; s < S; ++s) { tc::mbar_init(full(s), 1); tc::mbar_init(empty(s), 1); }
-    for (int a = 0; a < 2; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), 128); }
-    for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(ifull(k), 1); tc::mbar_init(iempty(k), 5); }   // MMA + 4 epilogue warps
+    for (int a = 0; a < 2; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), 32 * TcRoles<MODE>::kEpi); }
+    for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(ifull(k), 1); tc::mbar_init(iempty(k), 1 + TcRoles<MODE>::kEpi); }   // MMA + epilogue warps
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -796,11 +815,22 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
     }
   } else {             // ---- andpopc / estimate epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
+    // Thread = one row of the tile (its TMEM lane); the kEpi/4 warps of a lane quadrant split
+    // the 256 columns. Each 32 x CW chunk is transposed through a per-warp shared scratch
+    // ([plane][32][CW+1], conflict-free writes) so that stores are row-contiguous.
+    constexpr int CW = TcRoles<MODE>::kCW, NG = TcRoles<MODE>::kEpi / 4;
+    constexpr int RPI = 32 / CW;                      // rows per store instruction
+    constexpr uint32_t kTr = 32 * (CW + 1);           // one transposed plane
+    constexpr uint32_t kPl = MODE == kTcAndPopc ? 1 : 4;
+    const int ew = warp - 2;
     const uint32_t lb = 32u * (uint32_t)(warp & 3);
     const uint32_t rt = lb + (uint32_t)lane;          // row within the tile
+    const uint32_t cg0 = (uint32_t)(ew >> 2) * (kTcN / NG), cg1 = cg0 + kTcN / NG;
+    uint32_t* tr = reinterpret_cast<uint32_t*>(extra + p.l_smem) + (size_t)ew * kPl * kTr;
     uint32_t aphase = 0;
     int acc = 0;
     const uint32_t m = p.measure;
+    const uint32_t nplanes = MODE == kTcEstimate ? (uint32_t)__popc(m) : 1u;
     for (uint32_t ii = 0;; ++ii) {
       uint64_t it = 0;
       if (lane == 0) it = take_item(ii);
@@ -811,42 +841,56 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const uint64_t r = mt * kTcM + rt;
       const bool valid = r < p.na;
       const int pa = (MODE == kTcEstimate && valid) ? __ldg(p.pa + r) : 0;
+      const uint64_t r0 = mt * kTcM + lb;             // first row of this warp's quadrant
+      const uint32_t nrows = r0 < p.na ? (uint32_t)min((uint64_t)32, p.na - r0) : 0u;
       for (uint32_t nt = nt0; nt < nt1; ++nt) {
         const uint64_t n0 = (uint64_t)nt * kTcN;
         tc::mbar_wait(tfull(acc), aphase);
         tc::fence_after();
 #pragma unroll 1
-        for (int c = 0; c < kTcN; c += 32) {
-          uint32_t v[32];
-          tc::tmem_ld32(tmem + (lb << 16) + (uint32_t)acc * kTcN + (uint32_t)c, v);
-          if (!valid || n0 + c >= p.nb) continue;
+        for (uint32_t c = cg0; c < cg1; c += CW) {
+          uint32_t v[CW];
+          if constexpr (CW == 32) tc::tmem_ld32(tmem + (lb << 16) + (uint32_t)acc * kTcN + c, v);
+          else tc::tmem_ld8(tmem + (lb << 16) + (uint32_t)acc * kTcN + c, v);
+          if (n0 + c >= p.nb || nrows == 0) continue;    // warp-uniform
           const uint64_t cb = n0 + c;
-          const uint64_t left = p.nb - cb;                 // > 0
+          const uint32_t left = (uint32_t)min((uint64_t)CW, p.nb - cb);
           if (MODE == kTcAndPopc) {
-            int32_t* o = p.out_i32 + r * p.nb + cb;
-            if (left >= 32 && ((reinterpret_cast<uintptr_t>(o) & 15u) == 0)) {
 #pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                __stcs(reinterpret_cast<int4*>(o + j), make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if ((uint64_t)j < left) __stcs(o + j, (int32_t)v[j]);
-            }
+            for (int j = 0; j < CW; ++j) tr[lane * (CW + 1) + j] = v[j];
           } else {
-            const uint64_t plane = p.na * p.nb;
+            const int32_t pbl = lane < (int)left ? __ldg(p.pb + cb + lane) : 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if ((uint64_t)j >= left) break;
-              const Est e = p.bcs ? bcs_estimate_pair(pa, __ldg(p.pb + cb + j), (int)v[j], p.dcap, L, m)
-                                  : estimate_pair(pa, __ldg(p.pb + cb + j), (int)v[j], (int)p.N, L, m);
-              float* o = p.out_f32 + r * p.nb + cb + j;
-              if (m & 1u) { __stcs(o, __double2float_rn(e.ip)); o += plane; }
-              if (m & 2u) { __stcs(o, __double2float_rn(e.ham)); o += plane; }
-              if (m & 4u) { __stcs(o, __double2float_rn(e.js)); o += plane; }
-              if (m & 8u) { __stcs(o, __double2float_rn(e.cs)); }
+            for (int j = 0; j < CW; ++j) {
+              const int pb = __shfl_sync(0xffffffffu, pbl, j);
+              if (valid && (uint32_t)j < left) {
+                const Est e = p.bcs ? bcs_estimate_pair(pa, pb, (int)v[j], p.dcap, L, m)
+                                    : estimate_pair(pa, pb, (int)v[j], (int)p.N, L, m);
+                uint32_t q = 0;
+                if (m & 1u) tr[(q++) * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.ip));
+                if (m & 2u) tr[(q++) * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.ham));
+                if (m & 4u) tr[(q++) * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.js));
+                if (m & 8u) tr[q * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.cs));
+              }
             }
           }
+          __syncwarp();
+          {
+            const uint32_t col = (uint32_t)lane % CW, rsub = (uint32_t)lane / CW;
+            const uint64_t plane = p.na * p.nb;
+            if (col < left) {
+              for (uint32_t rr = rsub; rr < nrows; rr += RPI) {
+                const uint64_t o = (r0 + rr) * p.nb + cb + col;
+                if (MODE == kTcAndPopc) {
+                  __stcs(p.out_i32 + o, (int32_t)tr[rr * (CW + 1) + col]);
+                } else {
+                  for (uint32_t q = 0; q < nplanes; ++q)
+                    __stcs(reinterpret_cast<uint32_t*>(p.out_f32) + q * plane + o, tr[q * kTr + rr * (CW + 1) + col]);
+                }
+              }
+            }
+          }
+          __syncwarp();
         }
         tc::fence_before();
         tc::mbar_arrive(tempty(acc));
@@ -972,7 +1016,7 @@ static cudaError_t tc_launch(const uint8_t* A8, const uint8_t* B8, TcParams& p, 
   if (e != cudaSuccess) return e;
   uint64_t grid = std::min<uint64_t>(p.nitems, sms);
   if (const char* g = std::getenv("BINSKETCH_TC_GRID")) grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, std::strtoull(g, nullptr, 10)));
-  tc_pairs_kernel<MODE, KC><<<(unsigned)grid, kTcThreads, smem, s>>>(ma, mb, p);
+  tc_pairs_kernel<MODE, KC><<<(unsigned)grid, TcRoles<MODE>::kThreads, smem, s>>>(ma, mb, p);
   count_launch();
   return cudaGetLastError();
 }
@@ -982,7 +1026,7 @@ cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8,
   if (na == 0 || nb == 0) return cudaSuccess;
   TcParams p = {};
   p.na = na; p.nb = nb; p.N = N; p.out_i32 = out; p.item_ctr = ctr;
-  return tc_launch<kTcAndPopc, 128>(A8, B8, p, N, 0, 0, s);
+  return tc_launch<kTcAndPopc, 128>(A8, B8, p, N, TcRoles<kTcAndPopc>::kEpi * 4 * 32 * (TcRoles<kTcAndPopc>::kCW + 1), 0, s);   // transposes
 }
 
 cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
@@ -995,7 +1039,8 @@ cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8
   p.item_ctr = ctr;
   const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
   p.l_smem = (lb <= 64 * 1024) ? lb : 0;
-  return tc_launch<kTcEstimate, 64>(A8, B8, p, N, p.l_smem, 0, s);
+  return tc_launch<kTcEstimate, 64>(A8, B8, p, N,
+                                    p.l_smem + TcRoles<kTcEstimate>::kEpi * 4 * 4 * 32 * (TcRoles<kTcEstimate>::kCW + 1), 0, s);   // table + 4-plane transposes
 }
 
 uint32_t tc_topk_max_k() { return 64; }

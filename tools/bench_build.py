@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="buildonly")
 ap.add_argument("--modes", default="auto,global,cache,seeded")
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--bcs", action="store_true", help="BCS parity sketch (XOR) instead of BinSketch (OR)")
 a = ap.parse_args()
 spec, N = {"buildonly": (synth.BUILD_ONLY, synth.BUILD_ONLY_N), "large": (synth.LARGE, synth.LARGE_N),
            "ranking": (synth.RANKING_DB, synth.RANKING_N), "medium": (synth.MEDIUM, 1000)}[a.config]
@@ -32,12 +33,15 @@ rows = np.sort(np.random.default_rng(0).choice(n, min(n, 5000), replace=False))
 sub_ptr = np.zeros(len(rows) + 1, dtype=np.int64)
 sub_ptr[1:] = np.cumsum(ip_h[rows + 1] - ip_h[rows])
 sub_idx = np.concatenate([ix_h[ip_h[r]:ip_h[r + 1]] for r in rows])
-ref, _ = oracle.sketch(oracle.make_pi(synth.PI_SEED, d, N), d, N, sub_ptr, sub_idx)
+ref, _ = (oracle.bcs_sketch if a.bcs else oracle.sketch)(oracle.make_pi(synth.PI_SEED, d, N), d, N, sub_ptr, sub_idx)
+build_t, build_s = (bs.bcs_build, bs.bcs_build_seeded) if a.bcs else (bs.build, bs.build_seeded)
 for mode in a.modes.split(","):
     if mode in ("global", "cache", "smem16"):
         os.environ["BINSKETCH_BUILD_MODE"] = mode
-    fn = (lambda: bs.build_seeded(synth.PI_SEED, d, N, ip, ix, out=out)) if mode == "seeded" else \
-         (lambda: bs.build(pi, d, N, ip, ix, out=out))
+    else:
+        os.environ.pop("BINSKETCH_BUILD_MODE", None)
+    fn = (lambda: build_s(synth.PI_SEED, d, N, ip, ix, out=out)) if mode == "seeded" else \
+         (lambda: build_t(pi, d, N, ip, ix, out=out))
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -49,5 +53,5 @@ for mode in a.modes.split(","):
     bs.device_status()
     ok = np.array_equal(out[torch.from_numpy(rows).cuda()].cpu().numpy().view(np.uint32), ref)
     t = statistics.median(ts)
-    print(json.dumps({"config": a.config, "mode": mode, "ms": t * 1e3, "rows_per_s": n / t,
+    print(json.dumps({"config": a.config, "sketch": "bcs" if a.bcs else "binsketch", "mode": mode, "ms": t * 1e3, "rows_per_s": n / t,
                       "alg_GBps": alg / t / 1e9, "frac_hbm_6555": alg / t / 6555.2e9, "parity_sampled": ok}), flush=True)
