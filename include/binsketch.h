@@ -72,7 +72,10 @@ enum { BINSKETCH_MAX_K = 256 };            /* largest k binsketch_topk accepts *
 
 /* ops for binsketch_workspace_bytes */
 enum { BINSKETCH_OP_ANDPOPC = 1, BINSKETCH_OP_ESTIMATE = 2, BINSKETCH_OP_TOPK = 3, BINSKETCH_OP_JOIN = 4,
-       BINSKETCH_OP_JOIN_LIST = 5, BINSKETCH_OP_BCS_ESTIMATE = 6 };
+       BINSKETCH_OP_JOIN_LIST = 5, BINSKETCH_OP_BCS_ESTIMATE = 6,
+       BINSKETCH_OP_MSE = 7 /* na = n rows, nb = d */ };
+
+enum { BINSKETCH_MSE_BCS = 1 };            /* mse flags: sketches are BCS parity sketches */
 
 /* W = ceil(N/32), words per sketch row. */
 uint32_t binsketch_words(uint32_t N);
@@ -223,6 +226,25 @@ binsketch_status binsketch_bcs_estimate(const uint32_t* sketches_a, uint64_t na,
 
 /* The BCS table B (HOST double[N+1]) binsketch_bcs_estimate uploads. */
 binsketch_status binsketch_bcs_table(uint32_t N, uint64_t d, double* host_out);
+
+/* Experiment 1, fidelity of the estimate: over every unordered pair
+ * i < j of one corpus whose EXACT similarity reaches threshold t ("pairs whose similarities
+ * are higher than" t; reading R-M1: >= t, and for Hamming a distance <= t):
+ *   out_count[t] = number of such pairs,  out_sse[t] = sum over them of (est - true)^2
+ * so MSE = out_sse / out_count (the paper reports -ln MSE for JS / COS, MSE for IP).
+ * est: binsketch_estimate's fp64 recipe from `sketches` (device uint32[n][W(N)]), or with
+ *   BINSKETCH_MSE_BCS binsketch_bcs_estimate's from BCS sketches; true: exact similarity of
+ *   `exact` (device uint32[n][W(d)], the uncompressed rows, e.g. binsketch_build with the
+ *   identity map and N = d).
+ * thresholds: HOST double[nthr], 1 <= nthr <= BINSKETCH_MAX_THRESHOLDS, not NaN.
+ * out_sse: device double[nthr]; out_count: device uint64[nthr]. Sums are fp64 in a fixed
+ * order (fixed grid, independent of the device), so results are bit-identical run to run.
+ * Runs two tensor-core AND-popcount tables per block of 4096 rows and a fused reduction.
+ * ws: >= binsketch_workspace_bytes(BINSKETCH_OP_MSE, n, d, N, 0). */
+binsketch_status binsketch_mse(const uint32_t* sketches, const uint32_t* exact, uint64_t n, uint32_t N, uint64_t d,
+                               uint32_t measure, const double* thresholds, uint32_t nthr, uint32_t flags,
+                               double* out_sse, uint64_t* out_count, void* ws, size_t ws_bytes,
+                               binsketch_stream_t stream);
 
 /* Workspace bytes needed by op (BINSKETCH_OP_*) for na (queries) x nb (db)
  * rows of N-bit sketches and top-k size k (ignored for other ops). Pure

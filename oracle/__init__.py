@@ -12,6 +12,7 @@ pure-Python oracle for tiny inputs that pins it.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 
@@ -62,6 +63,7 @@ def _lib_():
         L.orc_bcs_table.argtypes = [u32, u64, vp]; L.orc_bcs_table.restype = None
         L.orc_bcs_estimate_pair.argtypes = [i32, i32, i32, u64, vp, vp]; L.orc_bcs_estimate_pair.restype = None
         L.orc_bcs_estimate.argtypes = [vp, u64, vp, u64, u32, u64, u32, vp]; L.orc_bcs_estimate.restype = None
+        L.orc_mse.argtypes = [vp, u64, u32, u64, vp, vp, u32, vp, u32, u32, vp, vp]; L.orc_mse.restype = None
         L.orc_enumerate.argtypes = [u32, u32, vp, i64, vp, i64, vp, vp]
         L.orc_enumerate.restype = ctypes.c_int
         _lib = L
@@ -255,6 +257,34 @@ def bcs_estimate(A: np.ndarray, B: np.ndarray, N: int, d: int, measure: int) -> 
     planes = bin(measure & 15).count("1")
     out = np.empty((planes, A.shape[0], B.shape[0]), dtype=np.float32)
     _lib_().orc_bcs_estimate(_p(A), A.shape[0], _p(B), B.shape[0], N, d, measure, _p(out))
+    return out
+
+
+def mse(S: np.ndarray, N: int, d: int, indptr, indices, measure: int, thresholds, bcs: bool = False):
+    """Experiment 1 sums (R-M1): (sse float64[nthr], count uint64[nthr]) over pairs
+    i < j whose exact similarity reaches each threshold; est from the sketches S (BCS if bcs)."""
+    S = np.ascontiguousarray(S, dtype=np.uint32)
+    thr = np.ascontiguousarray(np.atleast_1d(np.asarray(thresholds, dtype=np.float64)))
+    sse = np.empty(len(thr), dtype=np.float64)
+    cnt = np.empty(len(thr), dtype=np.uint64)
+    _lib_().orc_mse(_p(S), S.shape[0], N, d, _p(np.ascontiguousarray(indptr, dtype=np.int64)),
+                    _p(np.ascontiguousarray(indices, dtype=np.int32)), measure, _p(thr), len(thr),
+                    1 if bcs else 0, _p(sse), _p(cnt))
+    return sse, cnt
+
+
+def mse_report(sse: np.ndarray, count: np.ndarray, measure: int) -> list[dict]:
+    """MSE per threshold and, for JS / COS, -ln(MSE); empty sets -> absent."""
+    out = []
+    for s, c in zip(sse, count):
+        if c == 0:
+            out.append(None)
+            continue
+        v = float(s) / float(c)
+        r = {"pairs": int(c), "mse": v}
+        if measure in (JS, COS):
+            r["neg_log_mse"] = -math.log(v) if v > 0 else math.inf
+        out.append(r)
     return out
 
 

@@ -485,6 +485,51 @@ void orc_bcs_estimate(const uint32_t* A, uint64_t na, const uint32_t* Bm, uint64
 }
 
 // ---------------------------------------------------------------------------
+// Experiment 1, fidelity of the estimate: over every unordered pair
+// i < j of one corpus whose TRUE similarity is at least the threshold ("we considered
+// only those pairs whose similarities are higher than 0.95"; reading R-M1: >=, and for
+// Hamming a distance <= t), the squared difference between the estimate and the truth:
+//   count[t] = #{i<j : true(i,j) selects t},  sse[t] = sum (est(i,j) - true(i,j))^2
+// (MSE = sse / count, reported as -ln MSE for JS / COS and as is for IP).
+// est: the canonical BinSketch recipe from the sketches (flags & 1: BCS estimates from
+// BCS sketches, R-B2); true: exact similarities of the CSR rows (orc_exact). Sums are
+// plain sequential fp64 in (i, j) order.
+// ---------------------------------------------------------------------------
+void orc_mse(const uint32_t* S, uint64_t n, uint32_t N, uint64_t d, const int64_t* indptr, const int32_t* indices,
+             uint32_t measure, const double* thr, uint32_t nthr, uint32_t flags, double* sse, uint64_t* count) {
+  const uint64_t W = orc_words(N);
+  int m = 0;
+  while (m < 4 && measure != (1u << m)) ++m;
+  for (uint32_t t = 0; t < nthr; ++t) { sse[t] = 0.0; count[t] = 0; }
+  if (m == 4) return;
+  std::vector<double> T(N + 1);
+  if (flags & 1u) orc_bcs_table(N, d, T.data()); else orc_card_table(N, d, T.data());
+  std::vector<int32_t> pc(n);
+  for (uint64_t i = 0; i < n; ++i) pc[i] = popcount_row(S + i * W, W);
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint64_t j = i + 1; j < n; ++j) {
+      double tr[4], es[4];
+      orc_exact(indices + (indptr[i] - indptr[0]), indptr[i + 1] - indptr[i], indices + (indptr[j] - indptr[0]),
+                indptr[j + 1] - indptr[j], tr);
+      int pab = 0, px = 0;
+      for (uint64_t w = 0; w < W; ++w) {
+        pab += popc_fast(S[i * W + w] & S[j * W + w]);
+        px += popc_fast(S[i * W + w] ^ S[j * W + w]);
+      }
+      if (flags & 1u) orc_bcs_estimate_pair(pc[i], pc[j], px, d, T.data(), es);
+      else orc_estimate_pair(pc[i], pc[j], pab, N, T.data(), es);
+      for (uint32_t t = 0; t < nthr; ++t) {
+        const bool sel = (m == 1) ? (tr[m] <= thr[t]) : (tr[m] >= thr[t]);
+        if (sel) {
+          const double e = es[m] - tr[m];
+          sse[t] += e * e;
+          count[t] += 1;
+        }
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Exhaustive enumeration of Lemma 1's expectations: the
 // mean of |a_s| and of <a_s,b_s> over ALL N^d maps pi, computed by sketching
 // with every map (orc_sketch) and counting bits. a, b are sorted supports in

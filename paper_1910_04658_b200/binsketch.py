@@ -20,7 +20,8 @@ IP, HAM, JS, COS = 1, 2, 4, 8
 MEASURES = {"ip": IP, "ham": HAM, "js": JS, "cos": COS}
 TOPK_EXCLUDE_SELF = 1
 MAX_K = 256
-OP_ANDPOPC, OP_ESTIMATE, OP_TOPK, OP_JOIN, OP_JOIN_LIST, OP_BCS_ESTIMATE = 1, 2, 3, 4, 5, 6
+OP_ANDPOPC, OP_ESTIMATE, OP_TOPK, OP_JOIN, OP_JOIN_LIST, OP_BCS_ESTIMATE, OP_MSE = 1, 2, 3, 4, 5, 6, 7
+MSE_BCS = 1
 JOIN_EXCLUDE_SELF, JOIN_EXACT = 1, 2
 MAX_THRESHOLDS = 16
 
@@ -47,6 +48,7 @@ SIGNATURES = {
     "binsketch_join_list": (_int, [_vp, _vp, _u64, _vp, _u64, _u32, _u64, _u32, _u32, _vp, _vp, _vp, _u64, _vp, _sz,
                                    _vp]),
     "binsketch_join_confusion": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),
+    "binsketch_mse": (_int, [_vp, _vp, _u64, _u32, _u64, _u32, _vp, _u32, _u32, _vp, _vp, _vp, _sz, _vp]),
     "binsketch_workspace_bytes": (_sz, [_int, _u64, _u64, _u32, _u32]),
     "binsketch_card_table": (_int, [_u32, _u64, _vp]),
     "binsketch_device_status": (_int, [_vp]),
@@ -301,6 +303,20 @@ def join_confusion(bits_est: torch.Tensor, bits_true: torch.Tensor, ndb: int) ->
             _words_tensor(bits_true, "bits_true") if bits_true.numel() else None, nq, ndb,
             _dev(out, torch.int64, "out"), _stream()))
     return out
+
+
+def mse(S: torch.Tensor, X: torch.Tensor, N: int, d: int, measure: int, thresholds, bcs: bool = False, ws=None):
+    """Experiment 1 sums (binsketch_mse): device (sse float64[nthr], count int64[nthr])."""
+    n = S.shape[0]
+    thr = (ctypes.c_double * len(thresholds))(*[float(t) for t in thresholds])
+    sse = torch.empty(len(thresholds), dtype=torch.float64, device="cuda")
+    cnt = torch.empty(len(thresholds), dtype=torch.int64, device="cuda")
+    ws, wp, wn = _workspace(OP_MSE, n, d, N, 0, ws)
+    _check("binsketch_mse", _lib().binsketch_mse(
+        _words_tensor(S, "sketches") if n else None, _words_tensor(X, "exact") if n else None, n, N, d, measure,
+        ctypes.cast(thr, ctypes.c_void_p), len(thresholds), MSE_BCS if bcs else 0,
+        _dev(sse, torch.float64, "out_sse"), _dev(cnt, torch.int64, "out_count"), wp, wn, _stream()))
+    return sse, cnt
 
 
 def card_table(N: int, d: int):

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -88,7 +89,7 @@ TableCache& cache() {
 
 struct Layout {
   size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, qperm = 0, qspb = 0,
-         ctr = 0, done = 0, pab = 0, cnt = 0, total = 0;
+         ctr = 0, done = 0, pab = 0, cnt = 0, x8 = 0, px = 0, pabx = 0, part = 0, total = 0;
   uint32_t splits = 1;
 };
 
@@ -111,9 +112,25 @@ bool use_tc_pab(uint32_t N, uint64_t nq, uint64_t ndb, uint32_t k) {
   return !engine_cuda() && !use_tc(BINSKETCH_OP_TOPK, N, k) && nq * ndb * 4 <= kPabBudget;
 }
 
+constexpr uint64_t kMseRows = 4096;   // Experiment-1 row block (two [rows][n] int32 tables)
+
 Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
   Layout l;
   size_t off = 0;
+  if (op == BINSKETCH_OP_MSE) {   // na = n rows, nb = d (width of the exact rows)
+    const uint64_t n = na, d = nb, R = std::min<uint64_t>(n, kMseRows);
+    l.L = off; off += align_up((size_t)(N + 1) * 8);
+    l.pa = off; off += align_up((size_t)n * 4);
+    l.px = off; off += align_up((size_t)n * 4);
+    l.ctr = off; off += kAlign;
+    l.a8 = off; off += align_up((size_t)n * bsk::tc_kpad(N));
+    l.x8 = off; off += align_up((size_t)n * bsk::tc_kpad((uint32_t)std::min<uint64_t>(d, 0xffffff80ull)));
+    l.pab = off; off += align_up((size_t)R * n * 4);
+    l.pabx = off; off += align_up((size_t)R * n * 4);
+    l.part = off; off += align_up(bsk::mse_partial_bytes());
+    l.total = off;
+    return l;
+  }
   if (op == BINSKETCH_OP_ANDPOPC) {   // only the tensor-core engine needs scratch: expanded operands
     l.ctr = off; off += kAlign;
     l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
@@ -505,6 +522,54 @@ binsketch_status binsketch_bcs_table(uint32_t N, uint64_t d, double* host_out) {
   if (!t) return BINSKETCH_ECUDA;
   for (uint32_t k = 0; k <= N; ++k) host_out[k] = t[k];
   return BINSKETCH_OK;
+}
+
+binsketch_status binsketch_mse(const uint32_t* sketches, const uint32_t* exact, uint64_t n, uint32_t N, uint64_t d,
+                               uint32_t measure, const double* thresholds, uint32_t nthr, uint32_t flags,
+                               double* out_sse, uint64_t* out_count, void* ws, size_t ws_bytes,
+                               binsketch_stream_t stream) {
+  if (N < 2 || !one_bit(measure) || (flags & ~1u) || d == 0) return BINSKETCH_EINVAL;
+  if (nthr == 0 || nthr > BINSKETCH_MAX_THRESHOLDS || !thresholds || !out_sse || !out_count) return BINSKETCH_EINVAL;
+  for (uint32_t t = 0; t < nthr; ++t)
+    if (std::isnan(thresholds[t])) return BINSKETCH_EINVAL;
+  if (n > 0 && (!sketches || !exact)) return BINSKETCH_EINVAL;
+  if (n > 0x7fffffffull || d > 0xffffff80ull) return BINSKETCH_EUNSUPPORTED;
+  const Layout l = layout(BINSKETCH_OP_MSE, n, d, N, 0);
+  if (!ws || ws_bytes < l.total) return BINSKETCH_EWORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  const bool bcs = (flags & BINSKETCH_MSE_BCS) != 0;
+  double* part_sse = reinterpret_cast<double*>(w + l.part);
+  unsigned long long* part_cnt = reinterpret_cast<unsigned long long*>(w + l.part + bsk::mse_partial_bytes() / 2);
+  cudaError_t e = cudaMemsetAsync(w + l.part, 0, bsk::mse_partial_bytes(), s);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (n >= 2) {
+    binsketch_status st = upload_table(N, d, ws, l, s, bcs ? 1 : 0);
+    if (st != BINSKETCH_OK) return st;
+    int32_t* ps = reinterpret_cast<int32_t*>(w + l.pa);
+    int32_t* px = reinterpret_cast<int32_t*>(w + l.px);
+    uint8_t* a8 = reinterpret_cast<uint8_t*>(w + l.a8);
+    uint8_t* x8 = reinterpret_cast<uint8_t*>(w + l.x8);
+    const uint32_t Dw = (uint32_t)d;
+    e = bsk::launch_popcount(sketches, n, binsketch_words(N), ps, s);
+    if (e == cudaSuccess) e = bsk::launch_popcount(exact, n, binsketch_words(Dw), px, s);
+    if (e == cudaSuccess) e = bsk::launch_expand(sketches, n, N, a8, s);
+    if (e == cudaSuccess) e = bsk::launch_expand(exact, n, Dw, x8, s);
+    int32_t* pab = reinterpret_cast<int32_t*>(w + l.pab);
+    int32_t* pabx = reinterpret_cast<int32_t*>(w + l.pabx);
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(w + l.ctr);
+    for (uint64_t r0 = 0; e == cudaSuccess && r0 + 1 < n; r0 += kMseRows) {
+      const uint64_t rows = std::min<uint64_t>(kMseRows, n - r0);
+      e = bsk::launch_tc_andpopc(a8 + r0 * bsk::tc_kpad(N), rows, a8, n, N, pab, ctr, s);
+      if (e == cudaSuccess) e = bsk::launch_tc_andpopc(x8 + r0 * bsk::tc_kpad(Dw), rows, x8, n, Dw, pabx, ctr, s);
+      if (e == cudaSuccess)
+        e = bsk::launch_mse_block(pab, pabx, r0, rows, n, ps, px, reinterpret_cast<const double*>(w + l.L), N,
+                                  (double)d, measure, bcs, thresholds, nthr, part_sse, part_cnt, s);
+    }
+  }
+  if (e == cudaSuccess)
+    e = bsk::launch_mse_final(part_sse, part_cnt, nthr, out_sse, reinterpret_cast<unsigned long long*>(out_count), s);
+  return cuda_status(e);
 }
 
 binsketch_status binsketch_card_table(uint32_t N, uint64_t d, double* host_out) {

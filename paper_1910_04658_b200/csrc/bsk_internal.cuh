@@ -104,5 +104,15 @@ cudaError_t launch_join_list(const uint32_t* bits, uint64_t nq, uint64_t ndb, co
                              cudaStream_t s);
 cudaError_t launch_join_confusion(const uint32_t* est, const uint32_t* tru, uint64_t nq, uint64_t ndb, int64_t* out,
                                   cudaStream_t s);
+// Experiment 1: partial sums (mse_partial_bytes() of workspace, zeroed by the caller) over the
+// row block [r0, r0 + rows) x all n rows (j > i) from its two AND-popcount tables [rows][n];
+// thr: HOST double[nthr], nthr <= 16.
+uint32_t mse_partial_bytes();
+cudaError_t launch_mse_block(const int32_t* pab_s, const int32_t* pab_x, uint64_t r0, uint64_t rows, uint64_t n,
+                             const int32_t* ps, const int32_t* px, const double* L, uint32_t N, double dcap,
+                             uint32_t measure, bool bcs, const double* thr, uint32_t nthr, double* part_sse,
+                             unsigned long long* part_cnt, cudaStream_t s);
+cudaError_t launch_mse_final(const double* part_sse, const unsigned long long* part_cnt, uint32_t nthr, double* sse,
+                             unsigned long long* cnt, cudaStream_t s);
 
 }  // namespace bsk

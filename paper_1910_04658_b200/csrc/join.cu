@@ -1,8 +1,10 @@
-// join.cu — threshold-join post-processing (Experiment 2): the
-// per-query match list (CSR, db index ascending, with scores) from a match bitmap, and
-// the per-query confusion counts |O'|, |O|, |O ∩ O'| of two bitmaps, from which the
-// paper's accuracy / precision / recall / F1 follow.
-// The bitmaps themselves come from the tensor-core join (tc.cu, kTcJoin).
+// join.cu — kernels of the paper's two experiments beyond the pair engine:
+//  * Experiment 2 post-processing: the per-query match list (CSR, db
+//    index ascending, with scores) from a join bitmap, and the per-query confusion counts
+//    |O'|, |O|, |O ∩ O'| from which accuracy / precision / recall / F1 follow
+//    (PAPER.md:700-705). The bitmaps come from the tensor-core join (tc.cu, kTcJoin).
+//  * Experiment 1: the squared-error reduction over the pairs whose exact
+//    similarity reaches each threshold, from two AND-popcount tables (sketches, exact rows).
 // Compiled with -fmad=false (the list scores use the canonical fp64 recipe, R-C3).
 #include <cuda_runtime.h>
 
@@ -131,6 +133,99 @@ cudaError_t launch_join_confusion(const uint32_t* est, const uint32_t* tru, uint
   if (nq == 0) return cudaSuccess;
   const uint64_t blocks = std::min<uint64_t>((nq * 32 + 255) / 256, (uint64_t)num_sms() * 16);
   join_confusion_kernel<<<(unsigned)blocks, 256, 0, s>>>(est, tru, nq, (ndb + 31) / 32, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---- Experiment 1 -------------------------------------------------------------------------
+// Fixed grid (kMseBlocks, device independent) so that every partial sum has a fixed owner and
+// a fixed order: block b owns rows r0 + b, r0 + b + G, ... of the row block; thread t strides
+// over j > i; thread sums -> warp shuffle tree -> warps in order -> partial[b][t] (+=, the
+// block is its only writer; row blocks run in stream order). Result: bit-identical run to run.
+constexpr uint32_t kMseBlocks = 1024, kMseThreads = 256, kMseMaxThr = 16;
+struct MseThr { double v[kMseMaxThr]; };   // thresholds by value (kernel parameter space)
+
+__global__ void __launch_bounds__(kMseThreads)
+mse_block_kernel(const int32_t* __restrict__ pab_s, const int32_t* __restrict__ pab_x, uint64_t r0, uint64_t rows,
+                 uint64_t n, const int32_t* __restrict__ ps, const int32_t* __restrict__ px,
+                 const double* __restrict__ L, uint32_t N, double dcap, uint32_t m, uint32_t bcs,
+                 const MseThr thr, uint32_t nthr, double* __restrict__ part_sse,
+                 unsigned long long* __restrict__ part_cnt) {
+  __shared__ double s_sse[kMseThreads / 32][kMseMaxThr];
+  __shared__ unsigned long long s_cnt[kMseThreads / 32][kMseMaxThr];
+  double sse[kMseMaxThr];
+  unsigned long long cnt[kMseMaxThr];
+#pragma unroll
+  for (uint32_t t = 0; t < kMseMaxThr; ++t) { sse[t] = 0.0; cnt[t] = 0ull; }
+  for (uint64_t li = blockIdx.x; li < rows; li += gridDim.x) {
+    const uint64_t i = r0 + li;
+    const int pa = __ldg(ps + i), xa = __ldg(px + i);
+    const int32_t* rs = pab_s + li * n;
+    const int32_t* rx = pab_x + li * n;
+    for (uint64_t j = i + 1 + threadIdx.x; j < n; j += blockDim.x) {
+      const int pb = __ldg(ps + j), xb = __ldg(px + j);
+      const double key = exact_key(xa, xb, __ldg(rx + j), m);
+      const double tru = m == 2u ? -key : key;
+      const Est e = bcs ? bcs_estimate_pair(pa, pb, __ldg(rs + j), dcap, L, m)
+                        : estimate_pair(pa, pb, __ldg(rs + j), (int)N, L, m);
+      const double est = m == 1u ? e.ip : m == 2u ? e.ham : m == 4u ? e.js : e.cs;
+      const double df = __dsub_rn(est, tru);
+      const double sq = __dmul_rn(df, df);
+#pragma unroll
+      for (uint32_t t = 0; t < kMseMaxThr; ++t) {
+        if (t < nthr && (m == 2u ? tru <= thr.v[t] : tru >= thr.v[t])) { sse[t] = __dadd_rn(sse[t], sq); cnt[t] += 1ull; }
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (uint32_t t = 0; t < kMseMaxThr; ++t) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sse[t] = __dadd_rn(sse[t], __shfl_down_sync(0xffffffffu, sse[t], o));
+      cnt[t] += __shfl_down_sync(0xffffffffu, cnt[t], o);
+    }
+    if (lane == 0) { s_sse[warp][t] = sse[t]; s_cnt[warp][t] = cnt[t]; }
+  }
+  __syncthreads();
+  if (threadIdx.x < nthr) {
+    double a = 0.0;
+    unsigned long long c = 0ull;
+    for (int w = 0; w < (int)(kMseThreads / 32); ++w) { a = __dadd_rn(a, s_sse[w][threadIdx.x]); c += s_cnt[w][threadIdx.x]; }
+    part_sse[blockIdx.x * kMseMaxThr + threadIdx.x] = __dadd_rn(part_sse[blockIdx.x * kMseMaxThr + threadIdx.x], a);
+    part_cnt[blockIdx.x * kMseMaxThr + threadIdx.x] += c;
+  }
+}
+
+__global__ void mse_final_kernel(const double* __restrict__ part_sse, const unsigned long long* __restrict__ part_cnt,
+                                 uint32_t nthr, double* __restrict__ sse, unsigned long long* __restrict__ cnt) {
+  const uint32_t t = threadIdx.x;
+  if (t >= nthr) return;
+  double a = 0.0;
+  unsigned long long c = 0ull;
+  for (uint32_t b = 0; b < kMseBlocks; ++b) { a = __dadd_rn(a, part_sse[b * kMseMaxThr + t]); c += part_cnt[b * kMseMaxThr + t]; }
+  sse[t] = a;
+  cnt[t] = c;
+}
+
+uint32_t mse_partial_bytes() { return kMseBlocks * kMseMaxThr * 16; }
+
+cudaError_t launch_mse_block(const int32_t* pab_s, const int32_t* pab_x, uint64_t r0, uint64_t rows, uint64_t n,
+                             const int32_t* ps, const int32_t* px, const double* L, uint32_t N, double dcap,
+                             uint32_t measure, bool bcs, const double* thr, uint32_t nthr, double* part_sse,
+                             unsigned long long* part_cnt, cudaStream_t s) {
+  if (nthr > kMseMaxThr) return cudaErrorInvalidValue;
+  MseThr t = {};
+  for (uint32_t k = 0; k < nthr; ++k) t.v[k] = thr[k];   // host array
+  mse_block_kernel<<<kMseBlocks, kMseThreads, 0, s>>>(pab_s, pab_x, r0, rows, n, ps, px, L, N, dcap, measure,
+                                                      bcs ? 1u : 0u, t, nthr, part_sse, part_cnt);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mse_final(const double* part_sse, const unsigned long long* part_cnt, uint32_t nthr, double* sse,
+                             unsigned long long* cnt, cudaStream_t s) {
+  mse_final_kernel<<<1, 32, 0, s>>>(part_sse, part_cnt, nthr, sse, cnt);
   count_launch();
   return cudaGetLastError();
 }
