@@ -246,6 +246,24 @@ binsketch_status binsketch_mse(const uint32_t* sketches, const uint32_t* exact, 
                                double* out_sse, uint64_t* out_count, void* ws, size_t ws_bytes,
                                binsketch_stream_t stream);
 
+/* Categorical extension: label-encoded features -> the one-hot binary rows
+ * BinSketch compresses ("label-encoding followed by one-hot-encoding").
+ * codes: device int32[n][c], codes[r][k] in [0, m_k); offsets: device int64[c+1], offsets[0] = 0,
+ * offsets[k+1] - offsets[k] = m_k (so d = offsets[c]). Writes the CSR indptr (device int64[n+1],
+ * indptr[r] = r*c) and indices (device int32[n*c], offsets[k] + codes[r][k]) for binsketch_build.
+ * Latched EINDEX: a code outside [0, m_k) or an index >= 2^31 (the entry is then offsets[k]). */
+binsketch_status binsketch_onehot(const int32_t* codes, uint64_t n, uint32_t c, const int64_t* offsets,
+                                  int64_t* indptr, int32_t* indices, binsketch_stream_t stream);
+
+/* Estimated categorical distance D(u,v) = #{k : u[k] != v[k]} from the one-hot
+ * rows' sketches: D^ = HAM^/2 with HAM^ the Hamming estimate of binsketch_estimate (the one-hot
+ * Hamming distance is exactly 2 D; reading R-C1, SPEC.md:307 — the paper writes "equal").
+ * out: device float[na][nb] = (float)(HAM^ * 0.5). ws: >= binsketch_workspace_bytes(
+ * BINSKETCH_OP_BCS_ESTIMATE, na, nb, N, 0) (the tensor-core estimate layout). */
+binsketch_status binsketch_categorical_estimate(const uint32_t* sketches_a, uint64_t na, const uint32_t* sketches_b,
+                                                uint64_t nb, uint32_t N, uint64_t d, float* out, void* ws,
+                                                size_t ws_bytes, binsketch_stream_t stream);
+
 /* Workspace bytes needed by op (BINSKETCH_OP_*) for na (queries) x nb (db)
  * rows of N-bit sketches and top-k size k (ignored for other ops). Pure
  * function of its arguments (and of the BINSKETCH_ENGINE=cuda|tc A/B override,

@@ -64,6 +64,10 @@ def _lib_():
         L.orc_bcs_estimate_pair.argtypes = [i32, i32, i32, u64, vp, vp]; L.orc_bcs_estimate_pair.restype = None
         L.orc_bcs_estimate.argtypes = [vp, u64, vp, u64, u32, u64, u32, vp]; L.orc_bcs_estimate.restype = None
         L.orc_mse.argtypes = [vp, u64, u32, u64, vp, vp, u32, vp, u32, u32, vp, vp]; L.orc_mse.restype = None
+        L.orc_onehot.argtypes = [vp, u64, u32, vp, vp, vp]; L.orc_onehot.restype = ctypes.c_int
+        L.orc_categorical_distance.argtypes = [vp, u64, vp, u64, u32, vp]; L.orc_categorical_distance.restype = None
+        L.orc_categorical_estimate.argtypes = [vp, u64, vp, u64, u32, u64, vp]
+        L.orc_categorical_estimate.restype = None
         L.orc_enumerate.argtypes = [u32, u32, vp, i64, vp, i64, vp, vp]
         L.orc_enumerate.restype = ctypes.c_int
         _lib = L
@@ -285,6 +289,35 @@ def mse_report(sse: np.ndarray, count: np.ndarray, measure: int) -> list[dict]:
         if measure in (JS, COS):
             r["neg_log_mse"] = -math.log(v) if v > 0 else math.inf
         out.append(r)
+    return out
+
+
+def onehot(codes: np.ndarray, cards) -> tuple:
+    """Categorical extension: label codes [n][c] -> one-hot CSR.
+    Returns (indptr, indices, d, status)."""
+    codes = np.ascontiguousarray(codes, dtype=np.int32)
+    n, c = codes.shape
+    offsets = np.zeros(c + 1, dtype=np.int64)
+    offsets[1:] = np.cumsum(np.asarray(cards, dtype=np.int64))
+    indptr = np.empty(n + 1, dtype=np.int64)
+    indices = np.empty(n * c, dtype=np.int32)
+    st = _lib_().orc_onehot(_p(codes), n, c, _p(offsets), _p(indptr), _p(indices))
+    return indptr, indices, int(offsets[-1]), int(st)
+
+
+def categorical_distance(U: np.ndarray, V: np.ndarray) -> np.ndarray:
+    U = np.ascontiguousarray(U, dtype=np.int32)
+    V = np.ascontiguousarray(V, dtype=np.int32)
+    out = np.empty((U.shape[0], V.shape[0]), dtype=np.int32)
+    _lib_().orc_categorical_distance(_p(U), U.shape[0], _p(V), V.shape[0], U.shape[1], _p(out))
+    return out
+
+
+def categorical_estimate(A: np.ndarray, B: np.ndarray, N: int, d: int) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.uint32)
+    B = np.ascontiguousarray(B, dtype=np.uint32)
+    out = np.empty((A.shape[0], B.shape[0]), dtype=np.float32)
+    _lib_().orc_categorical_estimate(_p(A), A.shape[0], _p(B), B.shape[0], N, d, _p(out))
     return out
 
 

@@ -530,6 +530,56 @@ void orc_mse(const uint32_t* S, uint64_t n, uint32_t N, uint64_t d, const int64_
 }
 
 // ---------------------------------------------------------------------------
+// Categorical extension: label-encoded features (codes[r][k] in
+// [0, m_k)) are one-hot encoded as the binary vector with ones at offsets[k] + codes[r][k],
+// offsets = prefix sums of the cardinalities m_k (d = offsets[c]); the distance
+// D(u, v) = #{k : u[k] != v[k]}. Returns 1 on a code outside [0, m_k).
+// ---------------------------------------------------------------------------
+int orc_onehot(const int32_t* codes, uint64_t n, uint32_t c, const int64_t* offsets, int64_t* indptr,
+               int32_t* indices) {
+  int status = 0;
+  for (uint64_t r = 0; r <= n; ++r) indptr[r] = (int64_t)(r * c);
+  for (uint64_t r = 0; r < n; ++r)
+    for (uint32_t k = 0; k < c; ++k) {
+      const int64_t v = codes[r * c + k];
+      if (v < 0 || v >= offsets[k + 1] - offsets[k]) { status = 1; indices[r * c + k] = (int32_t)offsets[k]; continue; }
+      indices[r * c + k] = (int32_t)(offsets[k] + v);
+    }
+  return status;
+}
+
+// D(u, v) for all pairs (the categorical distance, literally).
+void orc_categorical_distance(const int32_t* U, uint64_t nu, const int32_t* V, uint64_t nv, uint32_t c, int32_t* out) {
+  for (uint64_t i = 0; i < nu; ++i)
+    for (uint64_t j = 0; j < nv; ++j) {
+      int32_t dd = 0;
+      for (uint32_t k = 0; k < c; ++k) dd += U[i * c + k] != V[j * c + k] ? 1 : 0;
+      out[i * nv + j] = dd;
+    }
+}
+
+// Estimated categorical distance (reading R-C1): D^ = HAM^ / 2 with HAM^ the canonical
+// recipe's Hamming estimate from the one-hot sketches (the one-hot Hamming distance is
+// exactly 2 D); out float[na][nb] = (float)(HAM^ * 0.5).
+void orc_categorical_estimate(const uint32_t* A, uint64_t na, const uint32_t* B, uint64_t nb, uint32_t N, uint64_t d,
+                              float* out) {
+  const uint64_t W = orc_words(N);
+  std::vector<double> L(N + 1);
+  orc_card_table(N, d, L.data());
+  for (uint64_t i = 0; i < na; ++i) {
+    const int pa = popcount_row(A + i * W, W);
+    for (uint64_t j = 0; j < nb; ++j) {
+      const int pb = popcount_row(B + j * W, W);
+      int pab = 0;
+      for (uint64_t w = 0; w < W; ++w) pab += popc_fast(A[i * W + w] & B[j * W + w]);
+      double e[4];
+      orc_estimate_pair(pa, pb, pab, N, L.data(), e);
+      out[i * nb + j] = (float)(e[1] * 0.5);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Exhaustive enumeration of Lemma 1's expectations: the
 // mean of |a_s| and of <a_s,b_s> over ALL N^d maps pi, computed by sketching
 // with every map (orc_sketch) and counting bits. a, b are sorted supports in

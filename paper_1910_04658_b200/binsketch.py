@@ -49,6 +49,8 @@ SIGNATURES = {
                                    _vp]),
     "binsketch_join_confusion": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),
     "binsketch_mse": (_int, [_vp, _vp, _u64, _u32, _u64, _u32, _vp, _u32, _u32, _vp, _vp, _vp, _sz, _vp]),
+    "binsketch_onehot": (_int, [_vp, _u64, _u32, _vp, _vp, _vp, _vp]),
+    "binsketch_categorical_estimate": (_int, [_vp, _u64, _vp, _u64, _u32, _u64, _vp, _vp, _sz, _vp]),
     "binsketch_workspace_bytes": (_sz, [_int, _u64, _u64, _u32, _u32]),
     "binsketch_card_table": (_int, [_u32, _u64, _vp]),
     "binsketch_device_status": (_int, [_vp]),
@@ -317,6 +319,32 @@ def mse(S: torch.Tensor, X: torch.Tensor, N: int, d: int, measure: int, threshol
         ctypes.cast(thr, ctypes.c_void_p), len(thresholds), MSE_BCS if bcs else 0,
         _dev(sse, torch.float64, "out_sse"), _dev(cnt, torch.int64, "out_count"), wp, wn, _stream()))
     return sse, cnt
+
+
+def onehot(codes: torch.Tensor, offsets: torch.Tensor):
+    """Categorical extension (binsketch_onehot): label codes int32 [n][c] + offsets int64 [c+1]
+    (device) -> one-hot CSR (indptr int64 [n+1], indices int32 [n*c])."""
+    n, c = codes.shape
+    indptr = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    indices = torch.empty(n * c, dtype=torch.int32, device="cuda")
+    _check("binsketch_onehot", _lib().binsketch_onehot(
+        _dev(codes, torch.int32, "codes") if codes.numel() else None, n, c,
+        _dev(offsets, torch.int64, "offsets") if c else None, _dev(indptr, torch.int64, "indptr"),
+        _dev(indices, torch.int32, "indices") if indices.numel() else None, _stream()))
+    return indptr, indices
+
+
+def categorical_estimate(A: torch.Tensor, B: torch.Tensor, N: int, d: int, out: torch.Tensor | None = None,
+                         ws=None) -> torch.Tensor:
+    """Estimated categorical distance HAM^/2 (binsketch_categorical_estimate): float [na][nb]."""
+    na, nb = A.shape[0], B.shape[0]
+    if out is None:
+        out = torch.empty((na, nb), dtype=torch.float32, device="cuda")
+    ws, wp, wn = _workspace(OP_BCS_ESTIMATE, na, nb, N, 0, ws)
+    _check("binsketch_categorical_estimate", _lib().binsketch_categorical_estimate(
+        _words_tensor(A, "A") if na else None, na, _words_tensor(B, "B") if nb else None, nb, N, d,
+        _dev(out, torch.float32, "out") if out.numel() else None, wp, wn, _stream()))
+    return out
 
 
 def card_table(N: int, d: int):

@@ -572,6 +572,44 @@ binsketch_status binsketch_mse(const uint32_t* sketches, const uint32_t* exact, 
   return cuda_status(e);
 }
 
+binsketch_status binsketch_onehot(const int32_t* codes, uint64_t n, uint32_t c, const int64_t* offsets,
+                                  int64_t* indptr, int32_t* indices, binsketch_stream_t stream) {
+  if (n > 0 && (!indptr || (c > 0 && (!codes || !offsets || !indices)))) return BINSKETCH_EINVAL;
+  if (!bsk::status_ptr()) return BINSKETCH_ECUDA;
+  if (n == 0) return BINSKETCH_OK;
+  if (c == 0) return cuda_status(cudaMemsetAsync(indptr, 0, (n + 1) * 8, reinterpret_cast<cudaStream_t>(stream)));
+  return cuda_status(bsk::launch_onehot(codes, n, c, offsets, indptr, indices, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+binsketch_status binsketch_categorical_estimate(const uint32_t* sketches_a, uint64_t na, const uint32_t* sketches_b,
+                                                uint64_t nb, uint32_t N, uint64_t d, float* out, void* ws,
+                                                size_t ws_bytes, binsketch_stream_t stream) {
+  if (N < 2) return BINSKETCH_EINVAL;
+  if (na == 0 || nb == 0) return BINSKETCH_OK;
+  if (!sketches_a || !sketches_b || !out || d == 0) return BINSKETCH_EINVAL;
+  const Layout l = layout(BINSKETCH_OP_BCS_ESTIMATE, na, nb, N, 0);   // the tensor-core estimate layout
+  if (!ws || ws_bytes < l.total) return BINSKETCH_EWORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  binsketch_status st = upload_table(N, d, ws, l, s, 0);
+  if (st != BINSKETCH_OK) return st;
+  const uint32_t W = binsketch_words(N);
+  int32_t* pa = reinterpret_cast<int32_t*>(w + l.pa);
+  int32_t* pb = reinterpret_cast<int32_t*>(w + l.pb);
+  uint8_t* a8 = reinterpret_cast<uint8_t*>(w + l.a8);
+  const bool self = sketches_a == sketches_b && na == nb;
+  uint8_t* b8 = self ? a8 : reinterpret_cast<uint8_t*>(w + l.b8);
+  cudaError_t e = bsk::launch_popcount(sketches_a, na, W, pa, s);
+  if (e == cudaSuccess) e = self ? cudaMemcpyAsync(pb, pa, na * 4, cudaMemcpyDeviceToDevice, s)
+                                 : bsk::launch_popcount(sketches_b, nb, W, pb, s);
+  if (e == cudaSuccess) e = bsk::launch_expand(sketches_a, na, N, a8, s);
+  if (e == cudaSuccess && !self) e = bsk::launch_expand(sketches_b, nb, N, b8, s);
+  if (e == cudaSuccess)
+    e = bsk::launch_tc_estimate(a8, na, b8, nb, N, BINSKETCH_HAM, pa, pb, reinterpret_cast<const double*>(w + l.L), out,
+                                reinterpret_cast<unsigned long long*>(w + l.ctr), s, false, 0.0, 0.5);
+  return cuda_status(e);
+}
+
 binsketch_status binsketch_card_table(uint32_t N, uint64_t d, double* host_out) {
   if (N < 2 || !host_out) return BINSKETCH_EINVAL;
   const double* t = cache().get(N, d);

@@ -37,6 +37,10 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
 
 cudaError_t launch_popcount(const uint32_t* sk, uint64_t n, uint32_t W, int32_t* out, cudaStream_t s);
 
+// Categorical extension: label codes [n][c] + offsets[c+1] (device) -> one-hot CSR (n*c entries).
+cudaError_t launch_onehot(const int32_t* codes, uint64_t n, uint32_t c, const int64_t* offsets, int64_t* indptr,
+                          int32_t* indices, cudaStream_t s);
+
 enum PairsMode { kAndPopc = 0, kEstimate = 1 };
 // All-pairs kernel: A[na][W] x B[nb][W]. mode kAndPopc writes int32 out[na][nb];
 // mode kEstimate reads pa/pb/L (device) and writes float planes.
@@ -64,10 +68,12 @@ cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* o
 // ctr: one 8-byte device word of workspace (dynamic tile scheduler; reset by the launcher).
 cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
                               int32_t* out, unsigned long long* ctr, cudaStream_t s);
-// bcs: BCS parity sketches, L = the BCS table, dcap = d (bcs_estimate_pair).
+// bcs: BCS parity sketches, L = the BCS table, dcap = d (bcs_estimate_pair). ham_scale multiplies
+// the fp64 Hamming estimate before rounding (0.5: categorical distance, exact power-of-two scaling).
 cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
                                uint32_t measure, const int32_t* pa, const int32_t* pb, const double* L, float* out,
-                               unsigned long long* ctr, cudaStream_t s, bool bcs = false, double dcap = 0.0);
+                               unsigned long long* ctr, cudaStream_t s, bool bcs = false, double dcap = 0.0,
+                               double ham_scale = 1.0);
 // Fused top-k on the tensor-core engine for k <= tc_topk_max_k(); partial lists
 // [nq][tc_topk_splits][k] in the workspace, then the merge kernel. `prefilter` enables
 // the integer L[pab] bound (valid when L is non-decreasing and convex).

@@ -704,6 +704,39 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------- one-hot ----
+// Categorical extension: label codes [n][c] -> the one-hot CSR that K1
+// sketches: indptr[r] = r*c, indices[r*c+k] = offsets[k] + codes[r][k]. A code outside
+// [0, offsets[k+1]-offsets[k]) or an index >= 2^31 latches kStatusIndex (the entry is then
+// offsets[k], so the CSR stays well formed).
+__global__ void onehot_kernel(const int32_t* __restrict__ codes, uint64_t n, uint32_t c,
+                              const int64_t* __restrict__ offsets, int64_t* __restrict__ indptr,
+                              int32_t* __restrict__ indices, unsigned int* status) {
+  unsigned bad = 0;
+  const uint64_t total = n * c;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = e / c;
+    const uint32_t k = (uint32_t)(e - r * c);
+    const int64_t o = __ldg(offsets + k), m = __ldg(offsets + k + 1) - o;
+    const int64_t v = __ldg(codes + e);
+    int64_t idx = o + v;
+    if (v < 0 || v >= m || idx > 0x7fffffffll || o < 0) { bad = 1; idx = o >= 0 && o <= 0x7fffffffll ? o : 0; }
+    indices[e] = (int32_t)idx;
+    if (k == 0) indptr[r] = (int64_t)(r * c);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) indptr[n] = (int64_t)(n * c);
+  if (bad) latch(status, kStatusIndex);
+}
+
+cudaError_t launch_onehot(const int32_t* codes, uint64_t n, uint32_t c, const int64_t* offsets, int64_t* indptr,
+                          int32_t* indices, cudaStream_t s) {
+  const uint64_t total = n * c;
+  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, (uint64_t)num_sms() * 8));
+  onehot_kernel<<<(unsigned)blocks, 256, 0, s>>>(codes, n, c, offsets, indptr, indices, status_ptr());
+  count_launch();
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ K2 ----
 // Algorithm 1 line 1: one warp per row, lanes over words.
 __global__ void popcount_kernel(const uint32_t* __restrict__ sk, uint64_t n, uint32_t W,

@@ -272,6 +272,7 @@ struct TcParams {
   uint32_t nthr, exact;   // kTcJoin: threshold count; exact similarities (L = identity) instead of estimates
   uint32_t bcs;           // kTcEstimate: BCS parity sketches (L = the BCS table B, dcap = d)
   double dcap;
+  double ham_scale;       // kTcEstimate: Hamming plane = fp64 HAM x ham_scale (1, or 0.5 categorical)
   double tkey[kTcMaxThr];     // kTcJoin: threshold keys, descending
   uint32_t tslot[kTcMaxThr];  // kTcJoin: bitmap plane of each key
 };
@@ -868,7 +869,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                     : estimate_pair(pa, pb, (int)v[j], (int)p.N, L, m);
                 uint32_t q = 0;
                 if (m & 1u) tr[(q++) * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.ip));
-                if (m & 2u) tr[(q++) * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.ham));
+                if (m & 2u) tr[(q++) * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(__dmul_rn(e.ham, p.ham_scale)));
                 if (m & 4u) tr[(q++) * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.js));
                 if (m & 8u) tr[q * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.cs));
               }
@@ -1031,11 +1032,11 @@ cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8,
 
 cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
                                uint32_t measure, const int32_t* pa, const int32_t* pb, const double* L, float* out,
-                               unsigned long long* ctr, cudaStream_t s, bool bcs, double dcap) {
+                               unsigned long long* ctr, cudaStream_t s, bool bcs, double dcap, double ham_scale) {
   if (na == 0 || nb == 0) return cudaSuccess;
   TcParams p = {};
   p.na = na; p.nb = nb; p.N = N; p.measure = measure; p.pa = pa; p.pb = pb; p.L = L; p.out_f32 = out;
-  p.bcs = bcs ? 1u : 0u; p.dcap = dcap;
+  p.bcs = bcs ? 1u : 0u; p.dcap = dcap; p.ham_scale = ham_scale;
   p.item_ctr = ctr;
   const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
   p.l_smem = (lb <= 64 * 1024) ? lb : 0;

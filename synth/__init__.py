@@ -168,3 +168,20 @@ EXP2_DUP_FRAC = 0.3
 EXP2_DUP_SEED = 8
 EXP2_SPLIT_SEED = 9
 EXP2_THRESHOLDS = (0.95, 0.9, 0.85, 0.8, 0.6, 0.5, 0.2, 0.1)
+
+
+# --- categorical inputs: label-encoded table [n][c] ---
+def make_categorical(n: int, cards, seed: int, dup_frac: float = 0.3, flip: float = 0.2):
+    """Seeded label-encoded table: column k uniform over [0, cards[k]) (Zipf-free), with a
+    fraction of rows copied from an earlier row with each column re-drawn w.p. ``flip``
+    (so small categorical distances occur). Input preparation only."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    cards = np.asarray(cards, dtype=np.int64)
+    n = int(n)
+    X = (rng.random((n, len(cards))) * cards[None, :]).astype(np.int32)
+    for i in range(1, n):
+        if rng.random() < dup_frac:
+            s = int(rng.integers(0, i))
+            re = rng.random(len(cards)) < flip
+            X[i] = np.where(re, X[i], X[s])
+    return X
