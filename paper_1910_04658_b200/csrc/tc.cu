@@ -277,6 +277,25 @@ struct TcParams {
   uint32_t tslot[kTcMaxThr];  // kTcJoin: bitmap plane of each key
 };
 
+// Max of 32 values as a depth-4 tree of 3-input maxima (VIMNMX3), not a 31-deep chain: the
+// epilogue runs one warp per scheduler, so dependent-latency chains are what it waits on.
+__device__ __forceinline__ uint32_t max32(const uint32_t (&v)[32]) {
+  uint32_t a[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) a[i] = __vimax3_u32(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  a[10] = max(v[30], v[31]);
+  const uint32_t b0 = __vimax3_u32(a[0], a[1], a[2]), b1 = __vimax3_u32(a[3], a[4], a[5]);
+  const uint32_t b2 = __vimax3_u32(a[6], a[7], a[8]), b3 = max(a[9], a[10]);
+  return max(__vimax3_u32(b0, b1, b2), b3);
+}
+// Bit j set iff v[j] >= t, built in four independent partial masks.
+__device__ __forceinline__ uint32_t ge_mask32(const uint32_t (&v)[32], uint32_t t) {
+  uint32_t m[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int j = 0; j < 32; ++j) m[j & 3] |= (v[j] >= t ? 1u : 0u) << j;
+  return (m[0] | m[1]) | (m[2] | m[3]);
+}
+
 template <int MODE, int KC>
 __global__ void __launch_bounds__(TcRoles<MODE>::kThreads, 1)
 tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
@@ -563,15 +582,11 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         auto chunk = [&](const uint32_t c, uint32_t (&v)[32]) {
           if (c >= nval) return;
           const uint32_t left = nval - c;
-          uint32_t mx = 0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) mx = max(mx, v[j]);
+          const uint32_t mx = max32(v);
           const bool pass = valid && mx >= pmin;
           if (!__any_sync(0xffffffffu, pass)) return;
           // survivor mask of this lane
-          uint32_t sm = 0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) sm |= ((pass && v[j] >= pmin && (uint32_t)j < left) ? 1u : 0u) << j;
+          const uint32_t sm = pass ? ge_mask32(v, pmin) & (left >= 32 ? 0xffffffffu : ((1u << left) - 1u)) : 0u;
           const uint32_t ns = __popc(sm);
           uint32_t off = ns;
 #pragma unroll
@@ -758,14 +773,10 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         auto chunk = [&](const uint32_t c, uint32_t (&v)[32]) {
           if (c >= nval) return;
           const uint32_t left = nval - c;
-          uint32_t mx = 0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) mx = max(mx, v[j]);
+          const uint32_t mx = max32(v);
           const bool pass = valid && mx >= pmin;
           if (!__any_sync(0xffffffffu, pass)) return;
-          uint32_t sm = 0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) sm |= ((pass && v[j] >= pmin && (uint32_t)j < left) ? 1u : 0u) << j;
+          const uint32_t sm = pass ? ge_mask32(v, pmin) & (left >= 32 ? 0xffffffffu : ((1u << left) - 1u)) : 0u;
           const uint32_t ns = __popc(sm);
           uint32_t off = ns;
 #pragma unroll
