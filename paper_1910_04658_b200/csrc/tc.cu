@@ -19,6 +19,7 @@
 //                   (2 x 256 int32 columns) so the epilogue of tile t overlaps
 //                   the MMAs of tile t+1.
 #include <cuda.h>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -53,10 +54,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "r"(0x100000u)   // suspend-time hint (ns): sleep, do not spin
         : "memory");
   } while (!done);
 }
@@ -855,6 +856,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const int pa = (MODE == kTcEstimate && valid) ? __ldg(p.pa + r) : 0;
       const uint64_t r0 = mt * kTcM + lb;             // first row of this warp's quadrant
       const uint32_t nrows = r0 < p.na ? (uint32_t)min((uint64_t)32, p.na - r0) : 0u;
+      const bool vec_rows = (p.nb & 3u) == 0 && (reinterpret_cast<uintptr_t>(p.out_f32) & 15u) == 0;
       for (uint32_t nt = nt0; nt < nt1; ++nt) {
         const uint64_t n0 = (uint64_t)nt * kTcN;
         tc::mbar_wait(tfull(acc), aphase);
@@ -872,19 +874,52 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int j = 0; j < CW; ++j) tr[lane * (CW + 1) + j] = v[j];
           } else {
             const int32_t pbl = lane < (int)left ? __ldg(p.pb + cb + lane) : 0;
+            // all four planes of BinSketch (the common call) compiled with the mask constant;
+            // with 16-B aligned rows each lane stores its row's CW = 8 values per plane as two
+            // 16-B stores (no transpose)
+            auto planes = [&](auto mtag) -> bool {
+              constexpr uint32_t MM = decltype(mtag)::value;
+              const uint32_t mm = MM ? MM : m;
+              float val[4][CW];
 #pragma unroll
-            for (int j = 0; j < CW; ++j) {
-              const int pb = __shfl_sync(0xffffffffu, pbl, j);
-              if (valid && (uint32_t)j < left) {
-                const Est e = p.bcs ? bcs_estimate_pair(pa, pb, (int)v[j], p.dcap, L, m)
-                                    : estimate_pair(pa, pb, (int)v[j], (int)p.N, L, m);
-                uint32_t q = 0;
-                if (m & 1u) tr[(q++) * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.ip));
-                if (m & 2u) tr[(q++) * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(__dmul_rn(e.ham, p.ham_scale)));
-                if (m & 4u) tr[(q++) * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.js));
-                if (m & 8u) tr[q * kTr + lane * (CW + 1) + j] = __float_as_uint(__double2float_rn(e.cs));
+              for (int j = 0; j < CW; ++j) {
+                const int pb = __shfl_sync(0xffffffffu, pbl, j);
+                Est e;
+                if (MM == 0u && p.bcs) e = bcs_estimate_pair(pa, pb, (int)v[j], p.dcap, L, mm);
+                else e = estimate_pair(pa, pb, (int)v[j], (int)p.N, L, mm);
+                // val[measure id][j] (static indices; the output plane of id is popc(mm & ((1<<id)-1)))
+                val[0][j] = __double2float_rn(e.ip);
+                val[1][j] = __double2float_rn(MM ? e.ham : __dmul_rn(e.ham, p.ham_scale));
+                val[2][j] = __double2float_rn(e.js);
+                val[3][j] = __double2float_rn(e.cs);
               }
-            }
+              if (CW == 8 && vec_rows && left == (uint32_t)CW) {
+                if (valid) {
+                  const uint64_t plane = p.na * p.nb;
+                  float* o = p.out_f32 + r * p.nb + cb;
+#pragma unroll
+                  for (uint32_t id = 0; id < 4; ++id) {
+                    if (mm & (1u << id)) {
+                      float* oq = o + (uint64_t)__popc(mm & ((1u << id) - 1u)) * plane;
+                      __stcs(reinterpret_cast<float4*>(oq), make_float4(val[id][0], val[id][1], val[id][2], val[id][3]));
+                      __stcs(reinterpret_cast<float4*>(oq + 4), make_float4(val[id][4], val[id][5], val[id][6], val[id][7]));
+                    }
+                  }
+                }
+                return true;
+              }
+#pragma unroll
+              for (int j = 0; j < CW; ++j)
+                if (valid && (uint32_t)j < left)
+#pragma unroll
+                  for (uint32_t id = 0; id < 4; ++id)
+                    if (mm & (1u << id))
+                      tr[(uint32_t)__popc(mm & ((1u << id) - 1u)) * kTr + lane * (CW + 1) + j] = __float_as_uint(val[id][j]);
+              return false;
+            };
+            const bool done = (m == 15u && !p.bcs && p.ham_scale == 1.0) ? planes(std::integral_constant<uint32_t, 15u>{})
+                                                                         : planes(std::integral_constant<uint32_t, 0u>{});
+            if (done) continue;                            // warp-uniform (left, vec_rows uniform)
           }
           __syncwarp();
           {
