@@ -169,6 +169,12 @@ template <bool XOR>
 __device__ __forceinline__ void put_bit(uint32_t a, uint32_t v) {
   if (XOR) red_xor_shared(a, v); else red_or_shared(a, v);
 }
+// 1 << (x mod 32) in one funnel shift (shf.l.wrap takes the shift amount mod 32).
+__device__ __forceinline__ uint32_t bit_of(uint32_t x) {
+  uint32_t r;
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(0u), "r"(1u), "r"(x));
+  return r;
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -460,8 +466,8 @@ build_kernel(const BuildParams p) {
               addr[4 * h + k] = pb.y + (POW2 ? ((uint32_t)__popc(pb.x & mle[k]) << wsh)
                                             : (uint32_t)__popc(pb.x & mle[k]) * Wb);
           }
-          maxidx = max(maxidx, max(max(max(cur[0], cur[1]), max(cur[2], cur[3])),
-                                   max(max(cur[4], cur[5]), max(cur[6], cur[7]))));
+          maxidx = __vimax3_u32(maxidx, __vimax3_u32(cur[0], cur[1], cur[2]),
+                                __vimax3_u32(__vimax3_u32(cur[3], cur[4], cur[5]), cur[6], cur[7]));
           uint32_t bit[8];   // 1 << (j & 31)
           if (MODE == kPiSeeded && POW2) {
             // word offset from j & ~31 (LEA.HI); x & 31 = j & 31 since N >= 32
@@ -469,7 +475,7 @@ build_kernel(const BuildParams p) {
             for (int u = 0; u < 8; ++u) {
               const uint32_t x = pi_pow2_raw(seed1, cur[u]);
               j[u] = x & wmask;                         // = (j >> 5) << 5
-              bit[u] = 1u << (x & 31u);
+              bit[u] = bit_of(x);
             }
           } else if (MODE == kPiSeeded) {
 #pragma unroll
@@ -509,7 +515,7 @@ build_kernel(const BuildParams p) {
           }
           if (!(MODE == kPiSeeded && POW2)) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) { bit[u] = 1u << (j[u] & 31u); j[u] &= ~31u; }
+            for (int u = 0; u < 8; ++u) { bit[u] = bit_of(j[u]); j[u] &= ~31u; }
           }
           if (FULL) {
 #pragma unroll
