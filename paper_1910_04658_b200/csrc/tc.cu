@@ -620,11 +620,13 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const int owner = (int)(e.y >> 24);
             const int pa_o = __shfl_sync(0xffffffffu, pa, owner);
             const double T_o = __shfl_sync(0xffffffffu, T, owner);
+            const int32_t Ti_o = __shfl_sync(0xffffffffu, Ti, owner);
             double key = -__longlong_as_double(0x7ff0000000000000LL);
             if (has) key = measure_key(estimate_pair(pa_o, tpb[e.x], (int)(e.y & 0xFFFFFFu), (int)p.N, Ls, m), m);
-            // candidates (key >= owner's threshold; ties resolved by the owner) go back to
-            // their owner lanes: every lane then inserts its own rows' candidates, in parallel
-            const bool cand = has && key >= T_o;
+            // candidates — those that would enter the owner's heap at its current threshold
+            // (key, then the tie order of R-G17 on the db index, checked here lane-parallel:
+            // rows with tiny sketches tie with thousands of db rows) — go back to their owners
+            const bool cand = has && before(key, tpm[e.x], T_o, Ti_o);
             const uint32_t bal = __ballot_sync(0xffffffffu, cand);
             if (bal) {
               __syncwarp();
