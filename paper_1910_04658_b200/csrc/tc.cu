@@ -440,6 +440,8 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                (size_t)(warp - 2) * kQCap;
     uint4* cq = reinterpret_cast<uint4*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 +
                                          4 * kQCap * 8) + (size_t)(warp - 2) * 32;   // per-warp candidate list
+    uint32_t* own = reinterpret_cast<uint32_t*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 +
+                                                4 * kQCap * 8 + 4 * 32 * 16) + (size_t)(warp - 2) * 32;   // per-owner candidate masks
     auto hkey = [&](uint32_t i) -> double& { return hk[i * kTcM + rt]; };
     auto hidx = [&](uint32_t i) -> int32_t& { return hi[i * kTcM + rt]; };
     uint32_t aphase = 0;
@@ -629,17 +631,23 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const bool cand = has && before(key, tpm[e.x], T_o, Ti_o);
             const uint32_t bal = __ballot_sync(0xffffffffu, cand);
             if (bal) {
+              // owner-parallel insertion: candidate of evaluating lane e sits in cq[e]; the
+              // lowest lane of each same-owner group publishes the group's mask to its owner,
+              // and every owner walks its own candidates (rounds = max candidates per owner)
+              const uint32_t grp = __match_any_sync(0xffffffffu, cand ? (uint32_t)owner : 32u + (uint32_t)lane);
               __syncwarp();
-              if (cand) {
-                const uint32_t slot = __popc(bal & ((1u << lane) - 1u));
-                cq[slot] = make_uint4(e.x, (uint32_t)owner, __double2loint(key), __double2hiint(key));
+              own[lane] = 0u;
+              if (cand) cq[lane] = make_uint4(e.x, (uint32_t)owner, __double2loint(key), __double2hiint(key));
+              __syncwarp();
+              if (cand && (grp & ((1u << lane) - 1u)) == 0u) own[owner] = grp;
+              __syncwarp();
+              uint32_t mine = own[lane];
+              while (mine) {
+                const uint32_t ee = __ffs(mine) - 1; mine &= mine - 1;
+                const uint4 c4 = cq[ee];
+                offer(__hiloint2double((int)c4.w, (int)c4.z), tpm[c4.x]);
               }
               __syncwarp();
-              const uint32_t nc = __popc(bal);
-              for (uint32_t t = 0; t < nc; ++t) {
-                const uint4 c4 = cq[t];
-                if (c4.y == (uint32_t)lane) offer(__hiloint2double((int)c4.w, (int)c4.z), tpm[c4.x]);
-              }
             }
           }
           __syncwarp();
@@ -1131,7 +1139,7 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
   p.lc = std::log1p(-1.0 / (double)N);
   p.prefilter = (prefilter && perm) ? 1u : 0u;   // the per-tile bound needs the popcount-sorted db
   p.part_key = part_key; p.part_idx = part_idx;
-  p.heap_smem = k * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 + 4 * 256 * 8 + 4 * 32 * 16;   // heaps, scratch, tile staging, queues, candidates
+  p.heap_smem = k * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 + 4 * 256 * 8 + 4 * 32 * 16 + 4 * 32 * 4;   // heaps, scratch, tile staging, queues, candidates, owner masks
   const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
   if (lb > 48 * 1024) return cudaErrorInvalidValue;   // caller keeps N <= tc_topk_max_n()
   p.l_topk_smem = lb;
