@@ -550,8 +550,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // result is made exact by the table refinement below
         const float pr = -(float)p.N * expm1f((float)((La + Llo - t) * p.lc));
         const float q0 = (float)pa + (float)lo - fminf(floorf(pr) + 2.0f, (float)p.N);
+        // q0 is a lower bound of the exact answer (the fp32 error of pr is < 0.01, far below the
+        // 2-step margin), so only the upward refinement is needed
         uint32_t qq = q0 <= 0.0f ? 0u : min((uint32_t)q0, pmax);
-        while (qq > 0 && key_bound(qq - 1, lo, hi_) >= g) --qq;     // (margin makes this rare)
         while (qq <= pmax && key_bound(qq, lo, hi_) < g) ++qq;
         c_lo = lo; c_hi = hi_; c_T = T; c_pmin = qq;
         return qq;
@@ -602,10 +603,22 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
               for (int j = 0; j < 32; ++j) scr[j * kTcM + rt] = v[j];
               uint32_t mm = sm;
-              while (mm) {
-                const uint32_t j = __ffs(mm) - 1; mm &= mm - 1;
-                const double key = measure_key(estimate_pair(pa, tpb[c + j], (int)scr[j * kTcM + rt], (int)p.N, Ls, m), m);
-                if (cnt < K || key >= T) offer(key, tpm[c + j]);
+              while (mm) {   // four independent fp64 evaluations in flight, then the offers
+                double kk[4];
+                int32_t ix[4];
+                uint32_t nk = 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  if (mm) {
+                    const uint32_t j = __ffs(mm) - 1; mm &= mm - 1;
+                    kk[u] = measure_key(estimate_pair(pa, tpb[c + j], (int)scr[j * kTcM + rt], (int)p.N, Ls, m), m);
+                    ix[u] = tpm[c + j];
+                    nk = (uint32_t)u + 1;
+                  }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  if ((uint32_t)u < nk && (cnt < K || kk[u] >= T)) offer(kk[u], ix[u]);
               }
             }
             __syncwarp();
