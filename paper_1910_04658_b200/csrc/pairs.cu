@@ -196,6 +196,34 @@ __device__ void block_bitonic_sort(double* key, int* idx, int n) {
 
 constexpr int kTBN = 64, kTKC = 32;
 
+// Necessary condition for measure_key(estimate_pair(...)) >= t (t finite), evaluated without
+// the division / square root of the JS and COS keys; the 1e-9 relative margins absorb every
+// rounding difference, so a pair it rejects is certainly below t.
+__device__ __forceinline__ bool pretest_keep(int pa, int pb, int pab, int N, const double* __restrict__ L, uint32_t m,
+                                             double t) {
+  const int pu = pa + pb - pab;
+  const double La = L[pa], Lb = L[pb];
+  const double S = La + Lb;
+  double ip;
+  if (pu == N && pa < N && pb < N) {
+    ip = 0.0;
+  } else {
+    ip = S - L[pu];
+    ip = ip > 0.0 ? ip : 0.0;
+    ip = fmin(ip, fmin(La, Lb));
+  }
+  const double eps = 1e-9;
+  if (m == 1u) return ip >= t - eps * fmax(1.0, fabs(t));
+  if (m == 2u) return 2.0 * ip - S >= t - eps * fmax(1.0, fabs(t));
+  if (t <= 0.0) return true;
+  if (m == 4u) {
+    if (pa == 0 && pb == 0) return true;
+    return ip * (1.0 + t) * (1.0 + eps) >= t * S;        // JS = ip/(S-ip) >= t
+  }
+  if (pa == 0 || pb == 0) return true;
+  return ip * ip * (1.0 + eps) >= t * t * (La * Lb);      // COS = ip/sqrt(La Lb) >= t
+}
+
 template <int TQ, int CAP>
 struct TopkCfg {
   static constexpr int TM = TQ / 16;   // 16 thread rows
@@ -285,7 +313,12 @@ topk_kernel(const uint32_t* __restrict__ Q, uint64_t nq, const uint32_t* __restr
         const uint64_t c = n0 + tx + j * C::kThreadsX;
         if (c >= c_end) continue;
         if ((flags & 1u) && c == r) continue;
-        const Est e = estimate_pair(pqr[i], pd[c], (int)acc[i][j], (int)N, L, measure);
+        const int pbc = pd[c];
+        // division-free pre-test against the row's threshold: the IP part of the recipe, then a
+        // conservative (1e-9 relative margin) necessary condition for key >= t; only pairs that
+        // pass pay for the exact key (division / square root)
+        if (t > -1e300 && !pretest_keep(pqr[i], pbc, (int)acc[i][j], (int)N, L, measure, t)) continue;
+        const Est e = estimate_pair(pqr[i], pbc, (int)acc[i][j], (int)N, L, measure);
         const double key = measure_key(e, measure);
         if (before(key, (int)c, t, ti)) {
           const int pos = atomicAdd(cnt + ql, 1);
@@ -379,6 +412,142 @@ uint32_t topk_splits(uint64_t nq, uint64_t ndb, uint32_t k) {
   return (uint32_t)std::max<uint64_t>(1, s);
 }
 
+// Top-k from a precomputed AND-popcount table pab[nq][ndb] (tensor cores): one warp per
+// (query row, db split) streams its pab row (16-B loads, 128 columns per step), keeps a running
+// threshold (its current k-th best), screens every pair with the division-free pre-test, scores
+// the rest exactly and appends those that beat the threshold to a per-warp buffer, which is
+// sorted (warp bitonic) and cut back to k when it could overflow. No block-level barriers.
+template <int CAPW>
+__global__ void __launch_bounds__(256)
+topk_pab_kernel(const int32_t* __restrict__ pab, uint64_t nq, uint64_t ndb, uint32_t N, uint32_t measure, uint32_t k,
+                uint32_t flags, const int32_t* __restrict__ pq, const int32_t* __restrict__ pd,
+                const double* __restrict__ Lg, uint32_t splits, double* __restrict__ part_key,
+                int32_t* __restrict__ part_idx, int32_t* __restrict__ out_idx, float* __restrict__ out_score) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const bool l_in_smem = N + 1 <= kMaxSmemL;
+  const size_t lbytes = l_in_smem ? (((size_t)(N + 1) * 8 + 15) & ~(size_t)15) : 0;
+  double* Ls = reinterpret_cast<double*>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* ckey = reinterpret_cast<double*>(smem + lbytes) + warp * CAPW;
+  int* cidx = reinterpret_cast<int*>(smem + lbytes + (size_t)8 * CAPW * 8) + warp * CAPW;
+  if (l_in_smem)
+    for (uint32_t i = threadIdx.x; i <= N; i += blockDim.x) Ls[i] = Lg[i];
+  __syncthreads();
+  const double* L = l_in_smem ? Ls : Lg;
+  const uint64_t gw = (uint64_t)blockIdx.x * 8 + warp;
+  if (gw >= nq * splits) return;
+  const uint64_t r = gw / splits;
+  const uint32_t sp = (uint32_t)(gw - r * splits);
+  const uint64_t per = ((ndb + splits - 1) / splits + 127) / 128 * 128;
+  const uint64_t c_begin = min((uint64_t)sp * per, ndb), c_end = min(c_begin + per, ndb);
+  const double kNegInf = -__longlong_as_double(0x7ff0000000000000LL);
+  for (int i = lane; i < CAPW; i += 32) { ckey[i] = kNegInf; cidx[i] = kSentinelIdx; }
+  __syncwarp();
+  double t = kNegInf;
+  int ti = kSentinelIdx;
+  uint32_t cnt = 0;                                     // buffered candidates beyond the first k
+  const int pa = pq[r];
+  const int32_t* prow = pab + r * ndb;
+  const bool vec = (ndb & 3u) == 0 && (reinterpret_cast<uintptr_t>(pab) & 15u) == 0 &&
+                   (reinterpret_cast<uintptr_t>(pd) & 15u) == 0;
+  auto flush = [&]() {
+    warp_bitonic_sort(ckey, cidx, CAPW);
+    for (int i = (int)k + lane; i < CAPW; i += 32) { ckey[i] = kNegInf; cidx[i] = kSentinelIdx; }
+    __syncwarp();
+    t = ckey[k - 1];
+    ti = cidx[k - 1];
+    cnt = 0;
+  };
+  for (uint64_t c0 = c_begin; c0 < c_end; c0 += 128) {
+    const uint64_t cl = c0 + 4 * (uint64_t)lane;
+    int v[4], b[4];
+    if (vec && cl + 3 < c_end) {
+      const int4 a4 = __ldcs(reinterpret_cast<const int4*>(prow + cl));
+      const int4 p4 = __ldg(reinterpret_cast<const int4*>(pd + cl));
+      v[0] = a4.x; v[1] = a4.y; v[2] = a4.z; v[3] = a4.w;
+      b[0] = p4.x; b[1] = p4.y; b[2] = p4.z; b[3] = p4.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        v[u] = cl + u < c_end ? __ldcs(prow + cl + u) : 0;
+        b[u] = cl + u < c_end ? __ldg(pd + cl + u) : 0;
+      }
+    }
+    double key[4];
+    bool keep[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t c = cl + u;
+      keep[u] = c < c_end && !((flags & 1u) && c == r);
+      if (keep[u] && t > kNegInf) keep[u] = pretest_keep(pa, b[u], v[u], (int)N, L, measure, t);
+      key[u] = kNegInf;
+      if (keep[u]) {
+        key[u] = measure_key(estimate_pair(pa, b[u], v[u], (int)N, L, measure), measure);
+        keep[u] = before(key[u], (int)c, t, ti);
+      }
+    }
+    const uint32_t mine = (keep[0] ? 1u : 0u) + (keep[1] ? 1u : 0u) + (keep[2] ? 1u : 0u) + (keep[3] ? 1u : 0u);
+    uint32_t off = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, off, o); if (lane >= o) off += y; }
+    const uint32_t total = __shfl_sync(0xffffffffu, off, 31);
+    if (total == 0) continue;
+    if (cnt + total > (uint32_t)CAPW - k) {
+      flush();   // frees CAPW - k >= 128 slots; re-screen this step's picks against the new threshold
+#pragma unroll
+      for (int u = 0; u < 4; ++u) keep[u] = keep[u] && before(key[u], (int)(cl + u), t, ti);
+      const uint32_t m2 = (keep[0] ? 1u : 0u) + (keep[1] ? 1u : 0u) + (keep[2] ? 1u : 0u) + (keep[3] ? 1u : 0u);
+      off = m2;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, off, o); if (lane >= o) off += y; }
+      const uint32_t tot2 = __shfl_sync(0xffffffffu, off, 31);
+      off -= m2;
+      uint32_t pos = k + cnt + off;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (keep[u]) { ckey[pos] = key[u]; cidx[pos] = (int)(cl + u); ++pos; }
+      cnt += tot2;
+    } else {
+      off -= mine;
+      uint32_t pos = k + cnt + off;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (keep[u]) { ckey[pos] = key[u]; cidx[pos] = (int)(cl + u); ++pos; }
+      cnt += total;
+    }
+    __syncwarp();
+  }
+  if (cnt > 0 || t == kNegInf) flush();
+  for (uint32_t q = lane; q < k; q += 32) {
+    const double kq = ckey[q];
+    const int id = cidx[q];
+    if (splits == 1) {
+      const bool valid = id != kSentinelIdx;
+      out_idx[r * k + q] = valid ? id : -1;
+      out_score[r * k + q] = valid ? key_to_score(kq, measure) : __int_as_float(0x7fc00000);
+    } else {
+      part_key[(r * splits + sp) * k + q] = kq;
+      part_idx[(r * splits + sp) * k + q] = id;
+    }
+  }
+}
+
+template <int CAPW>
+static cudaError_t launch_topk_pab_t(const int32_t* pab, uint64_t nq, uint64_t ndb, uint32_t N, uint32_t measure,
+                                     uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* pd, const double* L,
+                                     uint32_t splits, double* part_key, int32_t* part_idx, int32_t* out_idx,
+                                     float* out_score, cudaStream_t s) {
+  const bool l_in_smem = N + 1 <= kMaxSmemL;
+  const size_t smem = (l_in_smem ? (((size_t)(N + 1) * 8 + 15) & ~(size_t)15) : 0) + (size_t)8 * CAPW * 12;
+  cudaError_t e = cudaFuncSetAttribute(topk_pab_kernel<CAPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint64_t warps = nq * splits;
+  topk_pab_kernel<CAPW><<<(unsigned)((warps + 7) / 8), 256, smem, s>>>(pab, nq, ndb, N, measure, k, flags, pq, pd, L,
+                                                                       splits, part_key, part_idx, out_idx, out_score);
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <int TQ, int CAP, bool FROMPAB>
 static cudaError_t launch_topk_t2(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint64_t ndb, uint32_t N,
                                   uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq,
@@ -417,6 +586,14 @@ cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint6
   if (nq == 0 || k == 0) return cudaSuccess;
   const uint32_t splits = topk_splits(nq, ndb, k);
   cudaError_t e;
+  if (pab) {
+    e = k <= 128 ? launch_topk_pab_t<256>(pab, nq, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx,
+                                          out_idx, out_score, s)
+                 : launch_topk_pab_t<512>(pab, nq, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx,
+                                          out_idx, out_score, s);
+    if (e != cudaSuccess || splits == 1) return e;
+    return launch_topk_merge(nq, splits, k, measure, part_key, part_idx, out_idx, out_score, s);
+  }
   if (k <= 128 - kTBN)       e = launch_topk_t<32, 128>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, pab, s);
   else if (k <= 256 - kTBN)  e = launch_topk_t<16, 256>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, pab, s);
   else                       e = launch_topk_t<16, 512>(Q, nq, D, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx, out_idx, out_score, pab, s);
