@@ -99,9 +99,17 @@ bool engine_cuda() {
   const char* e = std::getenv("BINSKETCH_ENGINE");
   return e && !std::strcmp(e, "cuda");
 }
+bool engine_tc() {
+  const char* e = std::getenv("BINSKETCH_ENGINE");
+  return e && !std::strcmp(e, "tc");
+}
 bool use_tc(int op, uint32_t N, uint32_t k = 0) {
   if (engine_cuda()) return false;
   if (op == BINSKETCH_OP_TOPK) return k <= bsk::tc_topk_max_k() && N <= bsk::tc_topk_max_n();
+  // all-pairs estimate: the epilogue (fp64 recipe, 16 B of planes per pair) dominates; at W <= 32
+  // the CUDA-core kernel's 32 POPCs per pair are cheaper than the tensor-core pipeline around it
+  // (Medium, 1e8 pairs x 4 planes: N = 1000 1.28 vs 1.49 ms; N = 2000 1.87 vs 1.56 ms)
+  if (op == BINSKETCH_OP_ESTIMATE && !engine_tc()) return (N + 31) / 32 > 32;
   return true;
 }
 // Top-k beyond the fused kernel's limits (k > 64 or N > 6143): tensor-core AND-popcount into a
