@@ -211,6 +211,7 @@ __global__ void pb_scatter_kernel(const int32_t* __restrict__ pb, uint64_t n, ui
 // (SWIZZLE_128B) for the plain AND-popcount, KC = 64 (SWIZZLE_64B, half-size stages, so
 // deeper rings fit next to the estimator table / per-row top-k heaps) otherwise.
 constexpr int kTcM = 128, kTcN = 256;
+constexpr int kTcAcc = 512 / kTcN;   // TMEM accumulators (512 columns)
 constexpr uint32_t kTcSmemMax = 227 * 1024;
 // instruction descriptor: D s32, A/B u8, K-major, N = 256, M = 128
 constexpr uint32_t kTcIdesc = (2u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
@@ -311,19 +312,19 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   auto full = [&](uint32_t s) { return bars + 8u * s; };
   auto empty = [&](uint32_t s) { return bars + 8u * (S + s); };
   auto tfull = [&](int a) { return bars + 8u * (2 * S + a); };
-  auto tempty = [&](int a) { return bars + 8u * (2 * S + 2 + a); };
-  const uint32_t tmem_slot = bars + 8u * (2 * S + 4);
+  auto tempty = [&](int a) { return bars + 8u * (2 * S + kTcAcc + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * S + 2 * kTcAcc);
   // dynamic item schedule: the producer takes items from a global counter (heaviest query
   // tiles first) and publishes them through a 4-slot ring read by the MMA and epilogue roles
-  auto ifull = [&](uint32_t k) { return bars + 8u * (2 * S + 5 + k); };
-  auto iempty = [&](uint32_t k) { return bars + 8u * (2 * S + 9 + k); };
-  const uint32_t iring = bars + 8u * (2 * S + 13);   // 4 x u64 item ids
+  auto ifull = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 1 + k); };
+  auto iempty = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 5 + k); };
+  const uint32_t iring = bars + 8u * (2 * S + 2 * kTcAcc + 9);   // 4 x u64 item ids
   uint8_t* extra = smem + S * G::kStageBytes + 1024;        // estimator table or top-k heaps
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     for (uint32_t s = 0; s < S; ++s) { tc::mbar_init(full(s), 1); tc::mbar_init(empty(s), 1); }
-    for (int a = 0; a < 2; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), 32 * TcRoles<MODE>::kEpi); }
+    for (int a = 0; a < kTcAcc; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), 32 * TcRoles<MODE>::kEpi); }
     for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(ifull(k), 1); tc::mbar_init(iempty(k), 1 + TcRoles<MODE>::kEpi); }   // MMA + epilogue warps
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -414,7 +415,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             if (++stage == S) { stage = 0; phase ^= 1u; }
           }
           tc::commit(tfull(acc));                  // accumulator ready for the epilogue
-          if (++acc == 2) { acc = 0; aphase ^= 1u; }
+          if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
         }
       }
     }
@@ -559,10 +560,10 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       };
       // per-tile staging of the db popcounts / original indices (8 columns per lane),
       // loaded one tile ahead into registers, published to this warp's buffer
-      int32_t pf_pb[8], pf_pm[8];
+      int32_t pf_pb[kTcN / 32], pf_pm[kTcN / 32];
       auto prefetch = [&](uint32_t nt) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kTcN / 32; ++u) {
           const uint64_t col = (uint64_t)nt * kTcN + 32 * u + lane;
           const bool in = nt < nt1 && col < p.nb;
           pf_pb[u] = in ? __ldg(p.pb + col) : 0;
@@ -574,7 +575,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint64_t n0 = (uint64_t)nt * kTcN;
         __syncwarp();
 #pragma unroll
-        for (int u = 0; u < 8; ++u) { tpb[32 * u + lane] = pf_pb[u]; tpm[32 * u + lane] = pf_pm[u]; }
+        for (int u = 0; u < kTcN / 32; ++u) { tpb[32 * u + lane] = pf_pb[u]; tpm[32 * u + lane] = pf_pm[u]; }
         __syncwarp();
         prefetch(nt + 1);                                     // in flight during this tile
         const uint32_t nval = (uint32_t)min((uint64_t)kTcN, p.nb - n0);
@@ -681,7 +682,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
         tc::fence_before();
         tc::mbar_arrive(tempty(acc));
-        if (++acc == 2) { acc = 0; aphase ^= 1u; }
+        if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
       }
       if (valid) {   // partial list of this (row, chunk) — or the row's running heap when chained
         const uint64_t slot = p.chain ? rq : rq * p.splits + sp;
@@ -772,10 +773,10 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         c_lo = lo; c_hi = hi_; c_pmin = qq;
         return qq;
       };
-      int32_t pf_pb[8], pf_pm[8];
+      int32_t pf_pb[kTcN / 32], pf_pm[kTcN / 32];
       auto prefetch = [&](uint32_t nt) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kTcN / 32; ++u) {
           const uint64_t col = (uint64_t)nt * kTcN + 32 * u + lane;
           const bool in = nt < nt1 && col < p.nb;
           pf_pb[u] = in ? __ldg(p.pb + col) : 0;
@@ -787,7 +788,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint64_t n0 = (uint64_t)nt * kTcN;
         __syncwarp();
 #pragma unroll
-        for (int u = 0; u < 8; ++u) { tpb[32 * u + lane] = pf_pb[u]; tpm[32 * u + lane] = pf_pm[u]; }
+        for (int u = 0; u < kTcN / 32; ++u) { tpb[32 * u + lane] = pf_pb[u]; tpm[32 * u + lane] = pf_pm[u]; }
         __syncwarp();
         prefetch(nt + 1);
         const uint32_t nval = (uint32_t)min((uint64_t)kTcN, p.nb - n0);
@@ -847,7 +848,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
         tc::fence_before();
         tc::mbar_arrive(tempty(acc));
-        if (++acc == 2) { acc = 0; aphase ^= 1u; }
+        if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
       }
     }
   } else {             // ---- andpopc / estimate epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
@@ -964,7 +965,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
         tc::fence_before();
         tc::mbar_arrive(tempty(acc));
-        if (++acc == 2) { acc = 0; aphase ^= 1u; }
+        if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
       }
     }
   }
