@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "bsk_device.cuh"
 #include "bsk_estimator.cuh"
@@ -103,27 +104,34 @@ pairs_kernel(const uint32_t* __restrict__ A, uint64_t na, const uint32_t* __rest
 
   const int tx = threadIdx.x % PCfg::kThreadsX, ty = threadIdx.x / PCfg::kThreadsX;
   const uint64_t plane = na * nb;
+  // the all-planes call (the common one) is compiled with the measure mask as a constant
+  auto epilogue = [&](auto mtag) {
+    constexpr uint32_t MM = decltype(mtag)::value;
+    const uint32_t mm = MM ? MM : measure;
 #pragma unroll
-  for (int i = 0; i < kPTM; ++i) {
-    const uint64_t r = m0 + ty + i * PCfg::kThreadsY;
-    if (r >= na) continue;
-    const int par = (MODE == kEstimate) ? pa[r] : 0;
+    for (int i = 0; i < kPTM; ++i) {
+      const uint64_t r = m0 + ty + i * PCfg::kThreadsY;
+      if (r >= na) continue;
+      const int par = (MODE == kEstimate) ? pa[r] : 0;
 #pragma unroll
-    for (int j = 0; j < kPTN; ++j) {
-      const uint64_t c = n0 + tx + j * PCfg::kThreadsX;
-      if (c >= nb) continue;
-      if (MODE == kAndPopc) {
-        static_cast<int32_t*>(out)[r * nb + c] = (int32_t)acc[i][j];
-      } else {
-        const Est e = estimate_pair(par, pb[c], (int)acc[i][j], (int)N, L, measure);
-        float* o = static_cast<float*>(out) + r * nb + c;
-        if (measure & 1u) { __stcs(o, __double2float_rn(e.ip)); o += plane; }
-        if (measure & 2u) { __stcs(o, __double2float_rn(e.ham)); o += plane; }
-        if (measure & 4u) { __stcs(o, __double2float_rn(e.js)); o += plane; }
-        if (measure & 8u) { __stcs(o, __double2float_rn(e.cs)); }
+      for (int j = 0; j < kPTN; ++j) {
+        const uint64_t c = n0 + tx + j * PCfg::kThreadsX;
+        if (c >= nb) continue;
+        if (MODE == kAndPopc) {
+          static_cast<int32_t*>(out)[r * nb + c] = (int32_t)acc[i][j];
+        } else {
+          const Est e = estimate_pair(par, pb[c], (int)acc[i][j], (int)N, L, mm);
+          float* o = static_cast<float*>(out) + r * nb + c;
+          if (mm & 1u) { __stcs(o, __double2float_rn(e.ip)); o += plane; }
+          if (mm & 2u) { __stcs(o, __double2float_rn(e.ham)); o += plane; }
+          if (mm & 4u) { __stcs(o, __double2float_rn(e.js)); o += plane; }
+          if (mm & 8u) { __stcs(o, __double2float_rn(e.cs)); }
+        }
       }
     }
-  }
+  };
+  if (MODE == kEstimate && measure == 15u) epilogue(std::integral_constant<uint32_t, 15u>{});
+  else epilogue(std::integral_constant<uint32_t, 0u>{});
 }
 
 cudaError_t launch_pairs(int mode, const uint32_t* A, uint64_t na, const uint32_t* B, uint64_t nb,
