@@ -528,11 +528,12 @@ build_kernel(const BuildParams p) {
           }
         };
         if (ws + kStage <= span) {
-          half_step(0, std::true_type{});
-          if (kStage > kIter) half_step(1, std::true_type{});
+#pragma unroll
+          for (int h = 0; h < kStage / kIter; ++h) half_step(h, std::true_type{});
         } else {
-          half_step(0, std::false_type{});
-          if (kStage > kIter && ws + kIter < span) half_step(1, std::false_type{});
+#pragma unroll 1
+          for (int h = 0; h < kStage / kIter; ++h)
+            if (ws + kIter * h < span) half_step(h, std::false_type{});
         }
       }
     }
