@@ -492,8 +492,8 @@ void orc_bcs_estimate(const uint32_t* A, uint64_t na, const uint32_t* Bm, uint64
 //   count[t] = #{i<j : true(i,j) selects t},  sse[t] = sum (est(i,j) - true(i,j))^2
 // (MSE = sse / count, reported as -ln MSE for JS / COS and as is for IP).
 // est: the canonical BinSketch recipe from the sketches (flags & 1: BCS estimates from
-// BCS sketches, R-B2); true: exact similarities of the CSR rows (orc_exact). Sums are
-// plain sequential fp64 in (i, j) order.
+// BCS sketches, R-B2); true: exact similarities of the CSR rows (orc_exact). Sums: per row i
+// sequentially over j, then over i in order (fp64, independent of the thread count).
 // ---------------------------------------------------------------------------
 void orc_mse(const uint32_t* S, uint64_t n, uint32_t N, uint64_t d, const int64_t* indptr, const int32_t* indices,
              uint32_t measure, const double* thr, uint32_t nthr, uint32_t flags, double* sse, uint64_t* count) {
@@ -506,7 +506,13 @@ void orc_mse(const uint32_t* S, uint64_t n, uint32_t N, uint64_t d, const int64_
   if (flags & 1u) orc_bcs_table(N, d, T.data()); else orc_card_table(N, d, T.data());
   std::vector<int32_t> pc(n);
   for (uint64_t i = 0; i < n; ++i) pc[i] = popcount_row(S + i * W, W);
-  for (uint64_t i = 0; i < n; ++i)
+  // per-row partial sums (each a sequential sum over j), then a sequential sum over i: the
+  // same fixed order whatever the thread count
+  std::vector<double> rs((size_t)n * nthr, 0.0);
+  std::vector<uint64_t> rc((size_t)n * nthr, 0);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t ii = 0; ii < (int64_t)n; ++ii) {
+    const uint64_t i = (uint64_t)ii;
     for (uint64_t j = i + 1; j < n; ++j) {
       double tr[4], es[4];
       orc_exact(indices + (indptr[i] - indptr[0]), indptr[i + 1] - indptr[i], indices + (indptr[j] - indptr[0]),
@@ -522,11 +528,14 @@ void orc_mse(const uint32_t* S, uint64_t n, uint32_t N, uint64_t d, const int64_
         const bool sel = (m == 1) ? (tr[m] <= thr[t]) : (tr[m] >= thr[t]);
         if (sel) {
           const double e = es[m] - tr[m];
-          sse[t] += e * e;
-          count[t] += 1;
+          rs[i * nthr + t] += e * e;
+          rc[i * nthr + t] += 1;
         }
       }
     }
+  }
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint32_t t = 0; t < nthr; ++t) { sse[t] += rs[i * nthr + t]; count[t] += rc[i * nthr + t]; }
 }
 
 // ---------------------------------------------------------------------------

@@ -1,8 +1,8 @@
 """Pins for the oracle's Experiment-1 sums (fidelity of the estimate; CPU only).
 
 Independent of oracle.cpp: a pure-Python pass (set intersections for the truth, definitional
-per-bit popcounts + canonical recipe for the estimate) in the same (i, j) order; pair counts
-against a dense numpy matmul; SPEC.md:413's worked arithmetic; near-exactness at huge N;
+per-bit popcounts + canonical recipe for the estimate) summed in the same order (per row, then
+over rows); pair counts against a dense numpy matmul; SPEC.md:413's worked arithmetic; near-exactness at huge N;
 and SPEC.md:484's trend (MSE non-increasing in N, averaged over seeds).
 """
 import math
@@ -41,6 +41,7 @@ def test_mse_vs_python(measure, bcs):
     want_s = [0.0] * len(thr)
     want_c = [0] * len(thr)
     for i in range(n):
+        row_s = [0.0] * len(thr)              # summation order: per row over j, then over rows
         for j in range(i + 1, n):
             a, b = rows[i], rows[j]
             inter = len(a & b)
@@ -54,8 +55,10 @@ def test_mse_vs_python(measure, bcs):
                 est = D.estimate_canonical(pa, pb, D.and_popcount_bits(bits[i], bits[j]), N, T)[k]
             for t, th in enumerate(thr):
                 if (tru <= th) if measure == 2 else (tru >= th):
-                    want_s[t] += (est - tru) * (est - tru)
+                    row_s[t] += (est - tru) * (est - tru)
                     want_c[t] += 1
+        for t in range(len(thr)):
+            want_s[t] += row_s[t]
     assert list(cnt) == want_c
     assert all(s == w for s, w in zip(sse, want_s)), (sse, want_s)
     assert want_c[0] > 0
