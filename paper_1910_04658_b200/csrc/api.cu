@@ -433,15 +433,12 @@ binsketch_status binsketch_join(const uint32_t* queries, uint64_t nq, const uint
   const bool self = queries == db && nq == ndb;
   if (e == cudaSuccess) e = self ? cudaMemcpyAsync(pd, pq, nq * 4, cudaMemcpyDeviceToDevice, s)
                                  : bsk::launch_popcount(db, ndb, W, pd, s);
-  int32_t* perm = reinterpret_cast<int32_t*>(w + l.perm);
-  int32_t* spb = reinterpret_cast<int32_t*>(w + l.spb);
+  // db in its own order: every output word is then owned by one lane and written once with a
+  // plain store (no memset, no atomics; K11)
   uint8_t* q8 = reinterpret_cast<uint8_t*>(w + l.a8);
-  uint8_t* d8 = reinterpret_cast<uint8_t*>(w + l.b8);
-  if (e == cudaSuccess) e = bsk::launch_sort_by_popcount(pd, ndb, N, reinterpret_cast<uint32_t*>(w + l.bins), perm, spb, s);
+  uint8_t* d8 = self ? q8 : reinterpret_cast<uint8_t*>(w + l.b8);
   if (e == cudaSuccess) e = bsk::launch_expand(queries, nq, N, q8, s);
-  if (e == cudaSuccess) e = bsk::launch_expand(db, ndb, N, d8, s, perm);
-  const uint64_t wpr = (ndb + 31) / 32;
-  if (e == cudaSuccess) e = cudaMemsetAsync(out_bits, 0, (size_t)nthr * nq * wpr * 4, s);
+  if (e == cudaSuccess && !self) e = bsk::launch_expand(db, ndb, N, d8, s);
   if (e != cudaSuccess) return cuda_status(e);
   // threshold keys (R-J1), descending; tslot maps each back to its output plane
   double tkey[BINSKETCH_MAX_THRESHOLDS];
@@ -449,9 +446,8 @@ binsketch_status binsketch_join(const uint32_t* queries, uint64_t nq, const uint
   for (uint32_t t = 0; t < nthr; ++t) { tslot[t] = t; tkey[t] = measure == BINSKETCH_HAM ? -thresholds[t] : thresholds[t]; }
   for (uint32_t a = 1; a < nthr; ++a)
     for (uint32_t b = a; b > 0 && tkey[b] > tkey[b - 1]; --b) { std::swap(tkey[b], tkey[b - 1]); std::swap(tslot[b], tslot[b - 1]); }
-  const bool prefilter = exact || cache().convex(N, d);
   e = bsk::launch_tc_join(q8, nq, d8, ndb, N, measure, tkey, tslot, nthr, flags & BINSKETCH_JOIN_EXCLUDE_SELF, exact, pq,
-                          spb, perm, reinterpret_cast<const double*>(w + l.L), prefilter, out_bits,
+                          pd, nullptr, reinterpret_cast<const double*>(w + l.L), false, out_bits,
                           reinterpret_cast<unsigned long long*>(w + l.ctr), s);
   return cuda_status(e);
 }

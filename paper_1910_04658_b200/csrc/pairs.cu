@@ -204,34 +204,6 @@ __device__ void block_bitonic_sort(double* key, int* idx, int n) {
 
 constexpr int kTBN = 64, kTKC = 32;
 
-// Necessary condition for measure_key(estimate_pair(...)) >= t (t finite), evaluated without
-// the division / square root of the JS and COS keys; the 1e-9 relative margins absorb every
-// rounding difference, so a pair it rejects is certainly below t.
-__device__ __forceinline__ bool pretest_keep(int pa, int pb, int pab, int N, const double* __restrict__ L, uint32_t m,
-                                             double t) {
-  const int pu = pa + pb - pab;
-  const double La = L[pa], Lb = L[pb];
-  const double S = La + Lb;
-  double ip;
-  if (pu == N && pa < N && pb < N) {
-    ip = 0.0;
-  } else {
-    ip = S - L[pu];
-    ip = ip > 0.0 ? ip : 0.0;
-    ip = fmin(ip, fmin(La, Lb));
-  }
-  const double eps = 1e-9;
-  if (m == 1u) return ip >= t - eps * fmax(1.0, fabs(t));
-  if (m == 2u) return 2.0 * ip - S >= t - eps * fmax(1.0, fabs(t));
-  if (t <= 0.0) return true;
-  if (m == 4u) {
-    if (pa == 0 && pb == 0) return true;
-    return ip * (1.0 + t) * (1.0 + eps) >= t * S;        // JS = ip/(S-ip) >= t
-  }
-  if (pa == 0 || pb == 0) return true;
-  return ip * ip * (1.0 + eps) >= t * t * (La * Lb);      // COS = ip/sqrt(La Lb) >= t
-}
-
 template <int TQ, int CAP>
 struct TopkCfg {
   static constexpr int TM = TQ / 16;   // 16 thread rows

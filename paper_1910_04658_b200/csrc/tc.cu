@@ -223,9 +223,9 @@ constexpr uint32_t kTcMaxThr = 16;   // thresholds per join launch
 // recipe per pair, latency-bound) runs 16 warps reading 8-column chunks; the others 4 warps.
 template <int MODE>
 struct TcRoles {
-  static constexpr int kEpi = MODE == kTcEstimate ? 16 : 4;
+  static constexpr int kEpi = (MODE == kTcEstimate || MODE == kTcJoin) ? 16 : 4;
   static constexpr uint32_t kThreads = 64 + 32 * kEpi;
-  static constexpr int kCW = MODE == kTcEstimate ? 8 : 32;   // columns per TMEM load (andpopc / estimate)
+  static constexpr int kCW = (MODE == kTcEstimate || MODE == kTcJoin) ? 8 : 32;   // columns per TMEM load
 };
 
 template <int KC>
@@ -700,23 +700,31 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
     }
   } else if (MODE == kTcJoin) {
-    // ---- threshold-join epilogue (Exp. 2; R-J1): thread = one query row
-    // (TMEM lane). Per 256-column tile the prefilter bound of the top-k epilogue, taken at
-    // the LOWEST threshold key, gives pmin; 32-column chunks whose max pab < pmin are skipped
-    // with one compare. Survivors go through a per-warp queue and are scored lane-parallel
-    // (canonical fp64 recipe, or the exact key); a match sets its bit in every plane whose
-    // threshold it reaches (bit = original db index, so the bitmap is order independent).
+    // ---- threshold-join epilogue (Exp. 2; R-J1). The db is in its own order,
+    // so each lane (one query row, its TMEM lane) owns whole output words: the kEpi/4 warps of a
+    // lane quadrant split the tile's columns (64 each, 8-column TMEM chunks), every pair is
+    // screened by the division-free necessary condition against the LOWEST threshold key
+    // (pretest_keep), the rest are scored exactly (canonical fp64 recipe, or the exact key) and
+    // set their bit in every plane whose threshold they reach; each lane then stores its row's
+    // two words per plane with plain stores (every output word written exactly once: no memset,
+    // no atomics).
+    constexpr int CW = TcRoles<MODE>::kCW, NG = TcRoles<MODE>::kEpi / 4;
+    constexpr uint32_t kWC = kTcN / NG;               // columns per warp (64)
+    const int ew = warp - 2;
     const uint32_t lb = 32u * (uint32_t)(warp & 3);
     const uint32_t rt = lb + (uint32_t)lane;
-    const uint32_t m = p.measure;
+    const uint32_t cg0 = (uint32_t)(ew >> 2) * kWC;
+    const uint32_t m = p.measure, nthr = p.nthr;
     const bool exact = p.exact != 0u;
-    constexpr uint32_t kJQ = 1024;                    // per-warp queue: one chunk of 32 x 32 always fits
-    int32_t* tpb = reinterpret_cast<int32_t*>(extra) + (size_t)(warp - 2) * 2 * kTcN;
-    int32_t* tpm = tpb + kTcN;
-    uint2* q = reinterpret_cast<uint2*>(extra + 4 * 2 * kTcN * 4) + (size_t)(warp - 2) * kJQ;
-    const double g = p.tkey[p.nthr - 1] - 1e-9 * fmax(1.0, fabs(p.tkey[p.nthr - 1]));   // lowest key, with slack
+    const double tlo = p.tkey[nthr - 1];
     const uint64_t plane = p.na * p.wpr;
-    auto Lv = [&](uint32_t x) -> double { return exact ? (double)x : L[x]; };
+    // per-warp scratch after the (optionally staged) table: output words [32 lanes][16][2],
+    // the chunk's pab values [32][CW+1] and db popcounts [CW]
+    uint8_t* jscr = extra + p.l_topk_smem + (size_t)ew * (32 * nthr * 2 * 4 + 32 * (CW + 1) * 4 + 64);
+    uint32_t* jw = reinterpret_cast<uint32_t*>(jscr);
+    uint32_t* sv = jw + 32 * nthr * 2;
+    int32_t* spb_s = reinterpret_cast<int32_t*>(sv + 32 * (CW + 1));
+    const uint32_t rt_w = (uint32_t)lane;
     uint32_t aphase = 0;
     int acc = 0;
     for (uint32_t ii = 0;; ++ii) {
@@ -729,126 +737,59 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const uint64_t r = mt * kTcM + rt;
       const bool valid = r < p.na;
       const int pa = valid ? __ldg(p.pa + r) : 0;
-      const double La = Lv((uint32_t)pa);
-      // key bound over the tile's pb range [lo, hi] (see the top-k epilogue; L = identity when exact)
-      auto key_bound = [&](uint32_t pab, uint32_t lo, uint32_t hi_) -> double {
-        const uint32_t pu = min(pa + lo - min(pab, pa + lo), p.N);
-        const double Llo = Lv(lo);
-        double u = La + Llo - Lv(pu);
-        u = u > 0.0 ? u : 0.0;
-        u = fmin(u, fmin(La, Lv(hi_)));
-        if (m == 1u) return u;
-        if (m == 4u) { const double den = La + Llo - u; return den > 0.0 ? fmin(u / den, 1.0) : 1.0; }
-        if (m == 8u) return fmin(u / sqrt(La * Llo), 1.0);
-        return fmin(2.0 * u - La - Llo, 0.0);
-      };
-      uint32_t c_lo = 0xFFFFFFFFu, c_hi = 0, c_pmin = 0;
-      auto tile_pmin = [&](uint32_t lo, uint32_t hi_) -> uint32_t {
-        if (!p.prefilter || lo == 0) return 0u;
-        if (lo == c_lo && hi_ == c_hi) return c_pmin;
-        const uint32_t pmax = min((uint32_t)pa, hi_);
-        const double Llo = Lv(lo);
-        double t;
-        if (m == 1u) t = g;
-        else if (m == 4u) t = g > -1.0 ? g * (La + Llo) / (1.0 + g) : -1.0;
-        else if (m == 8u) t = g * sqrt(La * Llo);
-        else t = 0.5 * (g + La + Llo);
-        uint32_t qq;
-        if (t <= 0.0) {
-          qq = 0u;
-        } else if (fmin(La, Lv(hi_)) < t) {
-          qq = pmax + 1;
-        } else {
-          float q0;
-          if (exact) {
-            q0 = (float)t - 2.0f;
-          } else {
-            const float pr = -(float)p.N * expm1f((float)((La + Llo - t) * p.lc));
-            q0 = (float)pa + (float)lo - fminf(floorf(pr) + 2.0f, (float)p.N);
-          }
-          qq = q0 <= 0.0f ? 0u : min((uint32_t)q0, pmax);
-          while (qq > 0 && key_bound(qq - 1, lo, hi_) >= g) --qq;
-          while (qq <= pmax && key_bound(qq, lo, hi_) < g) ++qq;
-        }
-        c_lo = lo; c_hi = hi_; c_pmin = qq;
-        return qq;
-      };
-      int32_t pf_pb[kTcN / 32], pf_pm[kTcN / 32];
-      auto prefetch = [&](uint32_t nt) {
-#pragma unroll
-        for (int u = 0; u < kTcN / 32; ++u) {
-          const uint64_t col = (uint64_t)nt * kTcN + 32 * u + lane;
-          const bool in = nt < nt1 && col < p.nb;
-          pf_pb[u] = in ? __ldg(p.pb + col) : 0;
-          pf_pm[u] = in ? (p.perm ? __ldg(p.perm + col) : (int32_t)col) : -1;
-        }
-      };
-      prefetch(nt0);
       for (uint32_t nt = nt0; nt < nt1; ++nt) {
         const uint64_t n0 = (uint64_t)nt * kTcN;
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < kTcN / 32; ++u) { tpb[32 * u + lane] = pf_pb[u]; tpm[32 * u + lane] = pf_pm[u]; }
-        __syncwarp();
-        prefetch(nt + 1);
-        const uint32_t nval = (uint32_t)min((uint64_t)kTcN, p.nb - n0);
-        const uint32_t pmin = valid ? tile_pmin((uint32_t)tpb[nval - 1], (uint32_t)tpb[0]) : 0u;
         tc::mbar_wait(tfull(acc), aphase);
         tc::fence_after();
-        auto chunk = [&](const uint32_t c, uint32_t (&v)[32]) {
-          if (c >= nval) return;
-          const uint32_t left = nval - c;
-          const uint32_t mx = max32(v);
-          const bool pass = valid && mx >= pmin;
-          if (!__any_sync(0xffffffffu, pass)) return;
-          const uint32_t sm = pass ? ge_mask32(v, pmin) & (left >= 32 ? 0xffffffffu : ((1u << left) - 1u)) : 0u;
-          const uint32_t ns = __popc(sm);
-          uint32_t off = ns;
+        // this lane's output words for the tile: [plane][2] in shared memory (own lane only)
+        uint32_t* wb = jw + (size_t)rt_w * (nthr * (kWC / 32));
+#pragma unroll 1
+        for (uint32_t t = 0; t < nthr; ++t) { wb[2 * t] = 0u; wb[2 * t + 1] = 0u; }
+#pragma unroll 1
+        for (uint32_t c = 0; c < kWC; c += CW) {
+          uint32_t v[CW];
+          if constexpr (CW == 8) tc::tmem_ld8(tmem + (lb << 16) + (uint32_t)acc * kTcN + cg0 + c, v);
+          else tc::tmem_ld32(tmem + (lb << 16) + (uint32_t)acc * kTcN + cg0 + c, v);
+          const uint64_t cb = n0 + cg0 + c;
+          const int32_t pbl = (lane < CW && cb + lane < p.nb) ? __ldg(p.pb + cb + lane) : 0;
+          // 1) screen the 8 pairs (straight-line, no per-pair branches)
+          uint32_t keepm = 0;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, off, o); if (lane >= o) off += y; }
-          const uint32_t total = __shfl_sync(0xffffffffu, off, 31);
-          off -= ns;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if ((sm >> j) & 1u) q[off++] = make_uint2((c + (uint32_t)j) | ((uint32_t)lane << 16), v[j]);
+          for (int j = 0; j < CW; ++j) {
+            const int pb = __shfl_sync(0xffffffffu, pbl, j);
+            const uint64_t col = cb + j;
+            bool keep = valid && col < p.nb && !((p.flags & 1u) && col == r);
+            if (!exact) keep = keep && pretest_keep(pa, pb, (int)v[j], (int)p.N, L, m, tlo);
+            keepm |= (keep ? 1u : 0u) << j;
+            sv[lane * (CW + 1) + j] = v[j];
+          }
+          if (lane < CW) spb_s[lane] = pbl;
           __syncwarp();
-          for (uint32_t b = 0; b < total; b += 32) {
-            const bool has = b + lane < total;
-            const uint2 e = has ? q[b + lane] : make_uint2(0u, 0u);
-            const int owner = (int)(e.x >> 16);
-            const uint32_t col = e.x & 0xFFFFu;
-            const int pa_o = __shfl_sync(0xffffffffu, pa, owner);
-            const uint64_t r_o = __shfl_sync(0xffffffffu, r, owner);
-            if (has) {
-              const int32_t j = tpm[col];
-              if (!((p.flags & 1u) && (uint64_t)j == r_o)) {
-                const double key = exact ? exact_key(pa_o, tpb[col], (int)e.y, m)
-                                         : measure_key(estimate_pair(pa_o, tpb[col], (int)e.y, (int)p.N, L, m), m);
-                uint32_t* row = p.bits + r_o * p.wpr + ((uint32_t)j >> 5);
-                const uint32_t bit = 1u << ((uint32_t)j & 31u);
-                for (uint32_t t = 0; t < p.nthr; ++t)
-                  if (key >= p.tkey[t]) atomicOr(row + (uint64_t)p.tslot[t] * plane, bit);
-              }
-            }
+          // 2) the survivors: exact key, then the planes it reaches (thresholds descending)
+          while (keepm) {
+            const uint32_t j = __ffs(keepm) - 1; keepm &= keepm - 1;
+            const int pb = spb_s[j];
+            const int pab = (int)sv[lane * (CW + 1) + j];
+            const double key = exact ? exact_key(pa, pb, pab, m) : measure_key(estimate_pair(pa, pb, pab, (int)p.N, L, m), m);
+            uint32_t t0 = nthr;
+            while (t0 > 0 && key >= p.tkey[t0 - 1]) --t0;   // planes t >= t0 pass
+            const uint32_t h = (c + j) >> 5, bit = 1u << ((c + j) & 31u);
+            for (uint32_t t = t0; t < nthr; ++t) wb[2 * t + h] |= bit;
           }
           __syncwarp();
-        };
-        const uint32_t tb = tmem + (lb << 16) + (uint32_t)acc * kTcN;
-        uint32_t va[32], vb[32];
-        tc::tmem_ld32_issue(tb, va);
-        tc::tmem_ld_wait(va);
-#pragma unroll 1
-        for (uint32_t c = 0; c < (uint32_t)kTcN; c += 64) {
-          tc::tmem_ld32_issue(tb + c + 32, vb);
-          chunk(c, va);
-          tc::tmem_ld_wait(vb);
-          if (c + 64 < (uint32_t)kTcN) tc::tmem_ld32_issue(tb + c + 64, va);
-          chunk(c + 32, vb);
-          if (c + 64 < (uint32_t)kTcN) tc::tmem_ld_wait(va);
         }
         tc::fence_before();
         tc::mbar_arrive(tempty(acc));
         if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
+        if (valid) {
+          const uint64_t w0 = (n0 + cg0) >> 5;
+#pragma unroll 1
+          for (uint32_t t = 0; t < nthr; ++t) {
+            uint32_t* row = p.bits + (uint64_t)p.tslot[t] * plane + r * p.wpr;
+            if (w0 < p.wpr) __stcs(row + w0, wb[2 * t]);
+            if (w0 + 1 < p.wpr) __stcs(row + w0 + 1, wb[2 * t + 1]);
+          }
+        }
       }
     }
   } else {             // ---- andpopc / estimate epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
@@ -1182,10 +1123,11 @@ cudaError_t launch_tc_join(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
   for (uint32_t t = 0; t < nthr; ++t) { p.tkey[t] = tkey[t]; p.tslot[t] = tslot[t]; }
   p.lc = std::log1p(-1.0 / (double)N);
   p.prefilter = (prefilter && perm) ? 1u : 0u;
-  p.heap_smem = 4 * 2 * kTcN * 4 + 4 * 1024 * 8;        // tile staging + survivor queues
+  p.heap_smem = 0;
   const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
   p.l_topk_smem = (!exact && lb <= 64 * 1024) ? lb : 0u;   // else the table is read from global (L1)
-  return tc_launch<kTcJoin, 64>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, 0, s);
+  const uint32_t kJoinScratch = TcRoles<kTcJoin>::kEpi * (32 * nthr * 2 * 4 + 32 * (TcRoles<kTcJoin>::kCW + 1) * 4 + 64);
+  return tc_launch<kTcJoin, 64>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem + kJoinScratch, 0, s);
 }
 
 }  // namespace bsk
