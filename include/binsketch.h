@@ -171,8 +171,8 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
  *   bits 0), fully overwritten. The result is a set, so it is bit-identical run to run.
  * ws: >= binsketch_workspace_bytes(BINSKETCH_OP_JOIN, nq, ndb, N, 0).
  * Runs on the tensor-core engine (K11): AND-popcounts as in binsketch_andpopc,
- * a per-tile bound at the lowest threshold skips hopeless pairs, survivors are scored
- * exactly and their bits set. */
+ * a division-free necessary condition at the lowest threshold screens every pair, the
+ * rest are scored exactly, and each output word is written once. */
 binsketch_status binsketch_join(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb,
                                 uint32_t N, uint64_t d, uint32_t measure, const double* thresholds,
                                 uint32_t nthr, uint32_t flags, uint32_t* out_bits, void* ws, size_t ws_bytes,

@@ -149,13 +149,10 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
   l.L = off; off += align_up((size_t)(N + 1) * 8);
   l.pa = off; off += align_up((size_t)na * 4);
   l.pb = off; off += align_up((size_t)nb * 4);
-  if (op == BINSKETCH_OP_JOIN) {   // tensor-core join: widened operands, db sorted by popcount
+  if (op == BINSKETCH_OP_JOIN) {   // tensor-core join: widened operands
     l.ctr = off; off += kAlign;
     l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
     l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
-    l.bins = off; off += align_up((size_t)(N + 1) * 4);
-    l.perm = off; off += align_up((size_t)nb * 4);
-    l.spb = off; off += align_up((size_t)nb * 4);
     l.total = off;
     return l;
   }
@@ -447,7 +444,7 @@ binsketch_status binsketch_join(const uint32_t* queries, uint64_t nq, const uint
   for (uint32_t a = 1; a < nthr; ++a)
     for (uint32_t b = a; b > 0 && tkey[b] > tkey[b - 1]; --b) { std::swap(tkey[b], tkey[b - 1]); std::swap(tslot[b], tslot[b - 1]); }
   e = bsk::launch_tc_join(q8, nq, d8, ndb, N, measure, tkey, tslot, nthr, flags & BINSKETCH_JOIN_EXCLUDE_SELF, exact, pq,
-                          pd, nullptr, reinterpret_cast<const double*>(w + l.L), false, out_bits,
+                          pd, reinterpret_cast<const double*>(w + l.L), out_bits,
                           reinterpret_cast<unsigned long long*>(w + l.ctr), s);
   return cuda_status(e);
 }

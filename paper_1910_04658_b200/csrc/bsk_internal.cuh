@@ -93,14 +93,14 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
                            int32_t* part_idx, int32_t* out_idx, float* out_score, unsigned long long* ctr,
                            unsigned int* done, cudaStream_t s);   // done: ceil(nq/128) words of workspace
 
-// Threshold join on the tensor-core engine (Exp. 2): bits [nthr][nq][ceil(ndb/32)] (zeroed by the
-// caller); tkey descending with tslot[t] its bitmap plane; D8 rows in `perm` order (pd sorted
-// popcounts, descending) when prefilter is on. exact: L unused, keys from exact_key.
+// Threshold join on the tensor-core engine (Exp. 2): bits [nthr][nq][ceil(ndb/32)] (every word
+// written by the kernel); tkey descending with tslot[t] its bitmap plane; db rows in their own
+// order. exact: L unused, keys from exact_key.
 uint32_t tc_join_max_thresholds();
 cudaError_t launch_tc_join(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
                            uint32_t measure, const double* tkey, const uint32_t* tslot, uint32_t nthr, uint32_t flags,
-                           bool exact, const int32_t* pq, const int32_t* pd, const int32_t* perm, const double* L,
-                           bool prefilter, uint32_t* bits, unsigned long long* ctr, cudaStream_t s);
+                           bool exact, const int32_t* pq, const int32_t* pd, const double* L, uint32_t* bits,
+                           unsigned long long* ctr, cudaStream_t s);
 // join.cu: per-row counts (int32 scratch [nq]) -> row_ptr [nq+1]; list; confusion counts [3][nq].
 cudaError_t launch_join_rowptr(const uint32_t* bits, uint64_t nq, uint64_t ndb, int32_t* counts, int64_t* row_ptr,
                                cudaStream_t s);

@@ -1113,16 +1113,15 @@ uint32_t tc_join_max_thresholds() { return kTcMaxThr; }
 
 cudaError_t launch_tc_join(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
                            uint32_t measure, const double* tkey, const uint32_t* tslot, uint32_t nthr, uint32_t flags,
-                           bool exact, const int32_t* pq, const int32_t* pd, const int32_t* perm, const double* L,
-                           bool prefilter, uint32_t* bits, unsigned long long* ctr, cudaStream_t s) {
+                           bool exact, const int32_t* pq, const int32_t* pd, const double* L, uint32_t* bits,
+                           unsigned long long* ctr, cudaStream_t s) {
   if (nq == 0 || ndb == 0 || nthr == 0) return cudaSuccess;
   if (nthr > kTcMaxThr || (!exact && !L)) return cudaErrorInvalidValue;
   TcParams p = {};
   p.na = nq; p.nb = ndb; p.N = N; p.measure = measure; p.flags = flags; p.pa = pq; p.pb = pd; p.L = exact ? nullptr : L;
-  p.perm = perm; p.item_ctr = ctr; p.bits = bits; p.wpr = (ndb + 31) / 32; p.nthr = nthr; p.exact = exact ? 1u : 0u;
+  p.item_ctr = ctr; p.bits = bits; p.wpr = (ndb + 31) / 32; p.nthr = nthr; p.exact = exact ? 1u : 0u;
   for (uint32_t t = 0; t < nthr; ++t) { p.tkey[t] = tkey[t]; p.tslot[t] = tslot[t]; }
   p.lc = std::log1p(-1.0 / (double)N);
-  p.prefilter = (prefilter && perm) ? 1u : 0u;
   p.heap_smem = 0;
   const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
   p.l_topk_smem = (!exact && lb <= 64 * 1024) ? lb : 0u;   // else the table is read from global (L1)
