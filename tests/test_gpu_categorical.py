@@ -67,3 +67,10 @@ def test_categorical_estimate_bit_exact(na, nb, N):
     got = bs.categorical_estimate(dev(A.view(np.int32)), dev(B.view(np.int32)), N, d).cpu().numpy()
     assert np.all(np.abs(got.astype(np.float64) - want) <= 1e-4 * np.maximum(1.0, np.abs(want)))
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_onehot_zero_columns_and_zero_rows():
+    ip, ix = bs.onehot(torch.zeros((5, 0), dtype=torch.int32, device="cuda"), torch.zeros(1, dtype=torch.int64, device="cuda"))
+    assert ip.cpu().tolist() == [0] * 6 and ix.numel() == 0
+    ip, ix = bs.onehot(torch.zeros((0, 3), dtype=torch.int32, device="cuda"), dev(_offsets([2, 2, 2])))
+    assert ix.numel() == 0

@@ -188,3 +188,42 @@ def test_join_confusion_and_exp2_metrics():
         pc = lambda a: np.unpackbits(a.view(np.uint8), axis=1).sum(1)   # noqa: E731
         assert np.array_equal(conf[0], pc(est[k])) and np.array_equal(conf[1], pc(tru[k]))
         assert np.array_equal(conf[2], pc(est[k] & tru[k]))
+
+
+def test_join_list_capacity_truncation_and_exact_row_ptr():
+    (q, t) = _corpus(1500, seed=90)
+    d, N = synth.TINY.d, synth.TINY_N
+    pi = oracle.make_pi(synth.PI_SEED, d, N)
+    Qs, _ = oracle.sketch(pi, d, N, *q)
+    Ds, _ = oracle.sketch(pi, d, N, *t)
+    Qd, Dd = dev(Qs.view(np.int32)), dev(Ds.view(np.int32))
+    bits = bs.join(Qd, Dd, N, d, bs.JS, [0.2])[0]
+    row_ptr, cols, scores = bs.join_list(bits, Qd, Dd, N, d, bs.JS)
+    total = int(row_ptr[-1].item())
+    assert total > 10
+    # raw ABI call with a capacity below the total: row_ptr still exact, the first `cap` entries identical
+    cap = total // 3
+    rp = torch.empty(Qd.shape[0] + 1, dtype=torch.int64, device="cuda")
+    oj = torch.full((cap,), -7, dtype=torch.int32, device="cuda")
+    osc = torch.empty(cap, dtype=torch.float32, device="cuda")
+    nws = bs.workspace_bytes(bs.OP_JOIN_LIST, Qd.shape[0], Dd.shape[0], N)
+    ws = torch.empty(max(1, nws), dtype=torch.uint8, device="cuda")
+    code = bs._lib().binsketch_join_list(bs._words_tensor(bits, "b"), bs._words_tensor(Qd, "q"), Qd.shape[0],
+                                         bs._words_tensor(Dd, "d"), Dd.shape[0], N, d, bs.JS, 0,
+                                         bs._dev(rp, torch.int64, "rp"), bs._dev(oj, torch.int32, "oj"),
+                                         bs._dev(osc, torch.float32, "os"), cap, bs.ctypes.c_void_p(ws.data_ptr()),
+                                         ws.numel(), bs._stream())
+    assert code == 0
+    assert torch.equal(rp, row_ptr)
+    assert torch.equal(oj, cols[:cap]) and torch.equal(osc.view(torch.int32), scores[:cap].view(torch.int32))
+
+
+def test_join_sixteen_thresholds():
+    (q, t) = _corpus(1200, seed=91)
+    d, N = synth.TINY.d, 2048
+    pi = oracle.make_pi(synth.PI_SEED, d, N)
+    Qs, _ = oracle.sketch(pi, d, N, *q)
+    Ds, _ = oracle.sketch(pi, d, N, *t)
+    thr = list(np.linspace(0.02, 0.98, 16))
+    got = u32(bs.join(dev(Qs.view(np.int32)), dev(Ds.view(np.int32)), N, d, bs.COS, thr))
+    assert np.array_equal(got, oracle.join(Qs, Ds, N, d, bs.COS, thr))

@@ -80,3 +80,16 @@ def test_exp1_driver_matches_oracle():
     for r, w in zip(rows, rep):
         assert r["pairs"] == w["pairs"]
         assert abs(r["neg_log_mse"] - w["neg_log_mse"]) <= 1e-9 * abs(w["neg_log_mse"])
+
+
+def test_mse_sixteen_thresholds():
+    spec = synth.scaled(synth.TINY, 400, seed=77)
+    ip, ix = synth.make_csr(spec)
+    d, N = spec.d, 700
+    S, _ = oracle.sketch(oracle.make_pi(2, d, N), d, N, ip, ix)
+    X, _ = oracle.sketch(np.arange(d, dtype=np.uint32), d, d, ip, ix)
+    thr = list(np.linspace(0.0, 0.9, 16))
+    sse_ref, cnt_ref = oracle.mse(S, N, d, ip, ix, bs.COS, thr)
+    sse, cnt = bs.mse(dev(S.view(np.int32)), dev(X.view(np.int32)), N, d, bs.COS, thr)
+    assert np.array_equal(cnt.cpu().numpy().astype(np.uint64), cnt_ref)
+    assert np.all(np.abs(sse.cpu().numpy() - sse_ref) <= 1e-9 * np.maximum(1e-300, np.abs(sse_ref)))
