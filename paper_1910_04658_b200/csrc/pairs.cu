@@ -373,6 +373,37 @@ __global__ void topk_merge_kernel(uint64_t nq, uint32_t splits, uint32_t k, uint
   }
 }
 
+// Same merge with one warp per query row (8 rows per block) for short lists (P <= 256): the
+// chained tensor-core top-k hands over one k-list per row, and a 256-thread block per row
+// spent most of its time in block barriers.
+__global__ void topk_merge_warp_kernel(uint64_t nq, uint32_t splits, uint32_t k, uint32_t P, uint32_t measure,
+                                       const double* __restrict__ part_key, const int32_t* __restrict__ part_idx,
+                                       int32_t* __restrict__ out_idx, float* __restrict__ out_score) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* key = reinterpret_cast<double*>(smem) + (size_t)warp * P;
+  int* idx = reinterpret_cast<int*>(reinterpret_cast<double*>(smem) + 8 * (size_t)P) + (size_t)warp * P;
+  const uint64_t q = (uint64_t)blockIdx.x * 8 + warp;
+  if (q >= nq) return;
+  const uint32_t total = splits * k;
+  for (uint32_t i = lane; i < P; i += 32) {
+    if (i < total) {
+      key[i] = part_key[q * total + i];
+      idx[i] = part_idx[q * total + i];
+    } else {
+      key[i] = -__longlong_as_double(0x7ff0000000000000LL);
+      idx[i] = kSentinelIdx;
+    }
+  }
+  __syncwarp();
+  warp_bitonic_sort(key, idx, (int)P);
+  for (uint32_t t = lane; t < k; t += 32) {
+    const bool valid = idx[t] != kSentinelIdx;
+    out_idx[q * k + t] = valid ? idx[t] : -1;
+    out_score[q * k + t] = valid ? key_to_score(key[t], measure) : __int_as_float(0x7fc00000);
+  }
+}
+
 static uint32_t next_pow2(uint32_t v) {
   uint32_t p = 1;
   while (p < v) p <<= 1;
@@ -585,6 +616,15 @@ cudaError_t launch_topk_merge(uint64_t nq, uint32_t splits, uint32_t k, uint32_t
                               const int32_t* part_idx, int32_t* out_idx, float* out_score, cudaStream_t s) {
   if (nq == 0 || k == 0) return cudaSuccess;
   const uint32_t P = next_pow2(splits * k);
+  if (P <= 256) {
+    const size_t smem = (size_t)8 * P * 12;
+    cudaError_t e = cudaFuncSetAttribute(topk_merge_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    topk_merge_warp_kernel<<<(unsigned)((nq + 7) / 8), 256, smem, s>>>(nq, splits, k, P, measure, part_key, part_idx,
+                                                                     out_idx, out_score);
+    count_launch();
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)P * 12;
   cudaError_t e = cudaFuncSetAttribute(topk_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
