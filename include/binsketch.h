@@ -136,7 +136,9 @@ binsketch_status binsketch_andpopc(const uint32_t* A, uint64_t na, const uint32_
  * measure: nonzero mask of BINSKETCH_{IP,HAM,JS,COS}; out: device
  * float[popcount(measure)][na][nb], planes in the order IP, HAM, JS, COS, each
  * value the fp64 result rounded to nearest float.
- * d: ambient dimension (saturation cap). */
+ * d: ambient dimension (saturation cap).
+ * Engine (results identical either way): tensor cores (K10) when W > 32,
+ * the CUDA-core LOP3+POPC kernel (K3) otherwise. */
 binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, const uint32_t* sketches_b,
                                     uint64_t nb, uint32_t N, uint64_t d, uint32_t measure, float* out,
                                     void* ws, size_t ws_bytes, binsketch_stream_t stream);
@@ -149,7 +151,10 @@ binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, con
  * flags: BINSKETCH_TOPK_EXCLUDE_SELF skips j == i (self-join, R-G18).
  * out_idx: device int32[nq][k]; out_score: device float[nq][k] (the measure's
  * value, not the key). Slots beyond the number of eligible db rows hold
- * idx = -1 and score = NaN. */
+ * idx = -1 and score = NaN.
+ * Engine (results identical either way): k <= 64 and N <= 6143 — the fused tensor-core
+ * top-k (K10; per-row heaps in shared memory, db popcount-sorted for the bound);
+ * otherwise the tensor-core AND-popcount into a workspace table + the streaming top-k (K4b). */
 binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb,
                                 uint32_t N, uint64_t d, uint32_t measure, uint32_t k, uint32_t flags,
                                 int32_t* out_idx, float* out_score, void* ws, size_t ws_bytes,
