@@ -280,29 +280,36 @@ def run_ours(args):
 
     # --- e2e: host (pinned) CSR -> build -> top-k -> host results, through the public API ---
     e2e = None
-    if w["q"] is None:
-        ip_pin = torch.from_numpy(ip_h).pin_memory()
-        ix_pin = torch.from_numpy(ix_h).pin_memory()
-        pi_pin = torch.empty(d, dtype=torch.int32).pin_memory()
-        pi_pin.copy_(pi.cpu())
-        bufs = {}
-        for _ in range(max(1, args.warmup)):
-            bs.rank_from_host_csr(ip_pin, ix_pin, pi_pin, d, N, measure, k, exclude_self=w["exclude_self"], bufs=bufs)
-        torch.cuda.synchronize()
-        tsum = 0.0
-        h2d = d2h = 0
-        for _ in range(args.steps):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            _, _, h2d, d2h = bs.rank_from_host_csr(ip_pin, ix_pin, pi_pin, d, N, measure, k,
-                                                   exclude_self=w["exclude_self"], bufs=bufs)
-            b.record(stream)
-            b.synchronize()
-            tsum += a.elapsed_time(b) * 1e-3
-        tsum = max_over_ranks(tsum, ws)
-        e2e = {"value": aggregate_value(ws, pairs_per_step, args.steps, tsum), "unit": "pairs/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+    ip_pin = torch.from_numpy(ip_h).pin_memory()
+    ix_pin = torch.from_numpy(ix_h).pin_memory()
+    qp_pin = torch.from_numpy(qp_h).pin_memory() if qp_h is not None else None
+    qx_pin = torch.from_numpy(qx_h).pin_memory() if qx_h is not None else None
+    pi_pin = torch.empty(d, dtype=torch.int32).pin_memory()
+    pi_pin.copy_(pi.cpu())
+    bufs = {}
+    ms_e2e = w.get("measures", (measure,))
+
+    def e2e_step():
+        return bs.topk_from_host_csr(ip_pin, ix_pin, pi_pin, d, N, ms_e2e, k, q_indptr_h=qp_pin,
+                                     q_indices_h=qx_pin, exclude_self=w["exclude_self"], bufs=bufs)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    tsum = 0.0
+    h2d = d2h = 0
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _, h2d, d2h = e2e_step()
+        b.record(stream)
+        b.synchronize()
+        tsum += a.elapsed_time(b) * 1e-3
+    tsum = max_over_ranks(tsum, ws)
+    e2e = {"value": aggregate_value(ws, pairs_per_step, args.steps, tsum), "unit": "pairs/s",
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+    del bufs
 
     # --- roofline of the dominant kernel ---
     # Default engine: tensor cores (tc_pairs_kernel<kTcTopk>: tcgen05 kind::i8 on {0,1}-byte

@@ -401,3 +401,49 @@ def rank_from_host_csr(indptr_h: torch.Tensor, indices_h: torch.Tensor, pi_h: to
     h2d = indptr_h.numel() * 8 + indices_h.numel() * 4 + pi_h.numel() * 4
     d2h = nq * k * 8
     return b["idx_h"], b["score_h"], h2d, d2h
+
+
+def topk_from_host_csr(db_indptr_h: torch.Tensor, db_indices_h: torch.Tensor, pi_h: torch.Tensor, d: int, N: int,
+                       measures, k: int, q_indptr_h: torch.Tensor | None = None,
+                       q_indices_h: torch.Tensor | None = None, exclude_self: bool = False,
+                       bufs: dict | None = None):
+    """Host (pinned) CSR in, host top-k lists out, through the C ABI: H2D of the db CSR (and of a
+    separate query CSR, if given) and pi -> binsketch_build -> binsketch_topk per measure -> D2H of
+    every (idx, score) list. Without a query CSR the db rows are the queries (self-join).
+    Returns (list of (idx_host, score_host), h2d_bytes, d2h_bytes)."""
+    b = bufs if bufs is not None else {}
+    n = db_indptr_h.numel() - 1
+    sep = q_indptr_h is not None
+    nq = (q_indptr_h.numel() - 1) if sep else n
+    ms = list(measures)
+    if "db_ip" not in b:
+        b["db_ip"] = torch.empty_like(db_indptr_h, device="cuda")
+        b["db_ix"] = torch.empty_like(db_indices_h, device="cuda")
+        b["pi"] = torch.empty_like(pi_h, device="cuda")
+        b["db_sk"] = torch.empty((n, words(N)), dtype=torch.int32, device="cuda")
+        if sep:
+            b["q_ip"] = torch.empty_like(q_indptr_h, device="cuda")
+            b["q_ix"] = torch.empty_like(q_indices_h, device="cuda")
+            b["q_sk"] = torch.empty((nq, words(N)), dtype=torch.int32, device="cuda")
+        b["ws"] = torch.empty(max(1, workspace_bytes(OP_TOPK, nq, n, N, k)), dtype=torch.uint8, device="cuda")
+        b["out"] = [(torch.empty((nq, k), dtype=torch.int32, device="cuda"),
+                     torch.empty((nq, k), dtype=torch.float32, device="cuda")) for _ in ms]
+        b["out_h"] = [(torch.empty((nq, k), dtype=torch.int32, pin_memory=True),
+                       torch.empty((nq, k), dtype=torch.float32, pin_memory=True)) for _ in ms]
+    b["db_ip"].copy_(db_indptr_h, non_blocking=True)
+    b["db_ix"].copy_(db_indices_h, non_blocking=True)
+    b["pi"].copy_(pi_h, non_blocking=True)
+    h2d = db_indptr_h.numel() * 8 + db_indices_h.numel() * 4 + pi_h.numel() * 4
+    build(b["pi"], d, N, b["db_ip"], b["db_ix"], out=b["db_sk"])
+    if sep:
+        b["q_ip"].copy_(q_indptr_h, non_blocking=True)
+        b["q_ix"].copy_(q_indices_h, non_blocking=True)
+        h2d += q_indptr_h.numel() * 8 + q_indices_h.numel() * 4
+        build(b["pi"], d, N, b["q_ip"], b["q_ix"], out=b["q_sk"])
+    qs = b["q_sk"] if sep else b["db_sk"]
+    for m, (oi, osc), (hi, hs) in zip(ms, b["out"], b["out_h"]):
+        topk(qs, b["db_sk"], N, d, m, k, exclude_self=exclude_self, out_idx=oi, out_score=osc, ws=b["ws"])
+        hi.copy_(oi, non_blocking=True)
+        hs.copy_(osc, non_blocking=True)
+    d2h = len(ms) * nq * k * 8
+    return b["out_h"], h2d, d2h
