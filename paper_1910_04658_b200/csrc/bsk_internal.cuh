@@ -84,7 +84,7 @@ uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t N, uint32_t k);   //
 // sorted popcounts; bins: N+1 words of scratch). Top-k uses it for N <= 65536 (tc_sortable).
 bool tc_sortable(uint32_t N);
 cudaError_t launch_sort_by_popcount(const int32_t* pb, uint64_t n, uint32_t N, uint32_t* bins, int32_t* perm,
-                                    int32_t* spb, cudaStream_t s);
+                                    int32_t* spb, cudaStream_t s, bool descending = true);
 // Q8 rows in `qperm` order and D8 rows in `perm` order (nullptr: original order); pq / pd the
 // matching popcounts. Results land at the original query indices.
 cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,

@@ -169,13 +169,16 @@ __global__ void expand_kernel(const uint32_t* __restrict__ sk, uint64_t n, uint3
 }
 
 // ------------------------------------------------- db order for top-k ---
-// Counting sort of the db rows by popcount, descending (bin N - pb), so every 256-row
+// Counting sort of the db rows by popcount (descending: bin N - pb; or ascending), so every 256-row
 // tensor-core tile spans a narrow popcount range and the per-tile key bound is tight.
 // Order inside a bin is arbitrary: the top-k result is the unique top-k under
 // (key desc, original index asc), independent of processing order.
-__global__ void pb_hist_kernel(const int32_t* __restrict__ pb, uint64_t n, uint32_t N, uint32_t* __restrict__ bins) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    atomicAdd(bins + (N - (uint32_t)__ldg(pb + i)), 1u);
+__global__ void pb_hist_kernel(const int32_t* __restrict__ pb, uint64_t n, uint32_t N, uint32_t desc,
+                               uint32_t* __restrict__ bins) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = (uint32_t)__ldg(pb + i);
+    atomicAdd(bins + (desc ? N - v : v), 1u);
+  }
 }
 
 __global__ void pb_scan_kernel(uint32_t* __restrict__ bins, uint32_t nbins) {   // one block, exclusive, in place
@@ -196,11 +199,11 @@ __global__ void pb_scan_kernel(uint32_t* __restrict__ bins, uint32_t nbins) {   
   for (uint32_t i = b0; i < b1; ++i) { const uint32_t c = bins[i]; bins[i] = run; run += c; }
 }
 
-__global__ void pb_scatter_kernel(const int32_t* __restrict__ pb, uint64_t n, uint32_t N, uint32_t* __restrict__ cursor,
-                                  int32_t* __restrict__ perm, int32_t* __restrict__ spb) {
+__global__ void pb_scatter_kernel(const int32_t* __restrict__ pb, uint64_t n, uint32_t N, uint32_t desc,
+                                  uint32_t* __restrict__ cursor, int32_t* __restrict__ perm, int32_t* __restrict__ spb) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const int32_t v = __ldg(pb + i);
-    const uint32_t pos = atomicAdd(cursor + (N - (uint32_t)v), 1u);
+    const uint32_t pos = atomicAdd(cursor + (desc ? N - (uint32_t)v : (uint32_t)v), 1u);
     perm[pos] = (int32_t)i;
     spb[pos] = v;
   }
@@ -264,7 +267,7 @@ struct TcParams {
   int32_t* part_idx;
   uint32_t l_smem;        // kTcEstimate: table staged in shared memory (bytes, 0 = not staged)
   uint32_t heap_smem;     // kTcTopk: per-row heaps + survivor scratch in shared memory (bytes)
-  const int32_t* perm;    // kTcTopk: B row (sorted by |b_s| descending) -> original db index
+  const int32_t* perm;    // kTcTopk: B row (sorted by |b_s|, descending for IP, else ascending) -> original db index
   uint32_t l_topk_smem;   // kTcTopk: table staged after the heaps (bytes, 0 = global)
   double lc;              // log1p(-1/N): closed-form inverse of the table for the tile bound
   const int32_t* qperm;   // kTcTopk: A row (queries sorted by |a_s| descending) -> original query index
@@ -579,7 +582,8 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         __syncwarp();
         prefetch(nt + 1);                                     // in flight during this tile
         const uint32_t nval = (uint32_t)min((uint64_t)kTcN, p.nb - n0);
-        if (valid) pmin = tile_pmin((uint32_t)tpb[nval - 1], (uint32_t)tpb[0]);   // pb descending in the tile
+        // the tile's popcount range (the db is popcount-sorted, descending or ascending)
+        if (valid) pmin = tile_pmin(min((uint32_t)tpb[nval - 1], (uint32_t)tpb[0]), max((uint32_t)tpb[nval - 1], (uint32_t)tpb[0]));
         const bool direct = __any_sync(0xffffffffu, cnt < K);
         tc::mbar_wait(tfull(acc), aphase);
         tc::fence_after();
@@ -1062,14 +1066,14 @@ uint32_t tc_topk_max_n() { return 6143; }   // cardinality table (N+1 doubles) s
 bool tc_sortable(uint32_t N) { return N <= 65536; }
 
 cudaError_t launch_sort_by_popcount(const int32_t* pb, uint64_t n, uint32_t N, uint32_t* bins, int32_t* perm,
-                                    int32_t* spb, cudaStream_t s) {
+                                    int32_t* spb, cudaStream_t s, bool descending) {
   if (n == 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(bins, 0, (size_t)(N + 1) * 4, s);
   if (e != cudaSuccess) return e;
   const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms() * 8);
-  pb_hist_kernel<<<(unsigned)blocks, 256, 0, s>>>(pb, n, N, bins);
+  pb_hist_kernel<<<(unsigned)blocks, 256, 0, s>>>(pb, n, N, descending ? 1u : 0u, bins);
   pb_scan_kernel<<<1, 1024, 0, s>>>(bins, N + 1);
-  pb_scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(pb, n, N, bins, perm, spb);
+  pb_scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(pb, n, N, descending ? 1u : 0u, bins, perm, spb);
   count_launch(3);
   return cudaGetLastError();
 }
