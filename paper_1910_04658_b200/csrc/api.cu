@@ -359,16 +359,19 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
                                  : bsk::launch_popcount(db, ndb, W, pd, s);
   if (e != cudaSuccess) return cuda_status(e);
   if (ndb > 0 && use_tc(BINSKETCH_OP_TOPK, N, k)) {
-    // db in popcount-descending order (tight per-tile prefilter), queries in their own order
+    // db popcount-sorted (tight per-tile prefilter). Queries popcount-sorted too for JS / COS / HAM
+    // (a query tile then has a narrow |a_s| range, so its best candidates — pb near pa — arrive
+    // together; Large k = 50: HAM 90 -> 65, JS 214 -> 150, COS 158 -> 119 ms) but not for IP, where
+    // sorting clusters the heavy rows (large |a_s|, many candidates) into straggler tiles (53 -> 70 ms).
+    // BINSKETCH_TC_QSORT=0|1 overrides (dev A/B knob).
     uint8_t* q8 = reinterpret_cast<uint8_t*>(w + l.a8);
     uint8_t* d8 = reinterpret_cast<uint8_t*>(w + l.b8);
-    // Queries stay in their own order by default: sorting them too (BINSKETCH_TC_QSORT=1) clusters
-    // the heavy rows (large |a_s|, many candidates) into a few straggler tiles; measured 2.5x slower.
     const bool sorted = bsk::tc_sortable(N);
     int32_t* perm = sorted ? reinterpret_cast<int32_t*>(w + l.perm) : nullptr;
     int32_t* spb = sorted ? reinterpret_cast<int32_t*>(w + l.spb) : pd;
-    const char* qs = std::getenv("BINSKETCH_TC_QSORT");   // dev A/B knob
-    const bool qsort = sorted && qs && !std::strcmp(qs, "1");
+    const char* qs = std::getenv("BINSKETCH_TC_QSORT");
+    // (small query sets: the three extra sort launches would dominate a launch-bound call)
+    const bool qsort = sorted && (qs ? !std::strcmp(qs, "1") : (measure != BINSKETCH_IP && nq >= 16384));
     int32_t* qperm = qsort ? reinterpret_cast<int32_t*>(w + l.qperm) : nullptr;
     int32_t* qspb = qsort ? reinterpret_cast<int32_t*>(w + l.qspb) : pq;
     uint32_t* bins = reinterpret_cast<uint32_t*>(w + l.bins);

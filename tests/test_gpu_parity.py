@@ -399,3 +399,16 @@ def test_full_buildonly_sampled():
         assert np.array_equal(u32(sk[torch.from_numpy(rows).cuda()]), ref)
         bs.device_status()
         del sk
+
+
+@pytest.mark.parametrize("qsort", ["1", "0"])
+@pytest.mark.parametrize("measure", [1, 2, 4, 8])
+def test_topk_query_sort_paths(measure, qsort, monkeypatch):
+    """The fused top-k with queries popcount-sorted (default for JS / COS / HAM on >= 16384 queries)
+    and without, on both db sort directions (descending for IP, ascending otherwise): identical lists."""
+    monkeypatch.setenv("BINSKETCH_TC_QSORT", qsort)
+    N, d = 1024, 500_000
+    D = _sketches(synth.scaled(synth.LARGE, 2500), N)
+    D[300:340] = D[11]                   # ties across the sorted order
+    Q = D[:700].copy()
+    _check_topk(Q, D, N, d, measure, 50, exclude_self=True)
