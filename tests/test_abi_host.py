@@ -136,3 +136,26 @@ def test_product_shares_no_code_with_oracle():
                 assert not re.search(r"^\s*(import|from)\s+synth\b", src, re.M), f
     osrc = open(os.path.join(ROOT, "oracle", "oracle.cpp")).read()
     assert "#include \"binsketch.h\"" not in osrc and "bsk_" not in osrc
+
+
+def test_binding_fails_loudly_without_the_library(tmp_path):
+    """No CPU fallback: with the library absent every call raises (here: a fresh interpreter
+    pointed at a missing .so), and without a GPU a compute call raises instead of computing."""
+    import subprocess
+    import sys
+    code = ("import os, sys; sys.path.insert(0, %r); os.environ['BINSKETCH_LIB_VARIANT'] = %r\n"
+            "from paper_1910_04658_b200 import binsketch as bs\n"
+            "try:\n    bs.words(64)\nexcept ImportError as e:\n    print('raised', e)\n") % (ROOT, str(tmp_path / "missing.so"))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert "raised" in out.stdout and "no CPU fallback" in out.stdout
+
+
+def test_no_cpu_compute_path_in_the_binding():
+    """The binding only marshals arguments: it never imports numpy-based compute or the oracle,
+    and every public compute function ends in a libbinsketch call."""
+    src = open(os.path.join(ROOT, "paper_1910_04658_b200", "binsketch.py")).read()
+    assert "import oracle" not in src and "from oracle" not in src
+    for name in ("build", "build_seeded", "popcount", "andpopc", "estimate", "topk", "join", "mse",
+                 "bcs_build", "bcs_estimate", "onehot", "categorical_estimate"):
+        body = src.split(f"\ndef {name}(", 1)[1].split("\ndef ", 1)[0]
+        assert "_lib()." in body, name
