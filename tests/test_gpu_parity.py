@@ -313,10 +313,11 @@ def test_topk_padding_and_empty_db(engine):
     assert (gi.cpu().numpy() == -1).all() and np.isnan(gs.cpu().numpy()).all()
 
 
-# ------------------------------------------ full BASELINE sizes (sampled) --
+# ------------------------------------------------- full BASELINE sizes --
 @pytest.mark.slow
 def test_full_large_selfjoin_sampled():
-    """configs[4] at full size in the bench launch configuration; 256 sampled query rows vs the oracle."""
+    """configs[4] at full size in the bench launch configuration: all 2e5 sketches vs the oracle
+    (bit-exact), and 2000 sampled query rows' top-50 lists (IP, self excluded) vs the oracle."""
     spec, N, k = synth.LARGE, synth.LARGE_N, synth.LARGE_K
     indptr, indices = synth.make_csr(spec)
     pi = oracle.make_pi(synth.PI_SEED, spec.d, N)
@@ -325,28 +326,25 @@ def test_full_large_selfjoin_sampled():
     gi, gs = bs.topk(sk, sk, N, spec.d, bs.IP, k, exclude_self=True)
     torch.cuda.synchronize()
     skh = u32(sk)
-    rows = np.sort(np.random.default_rng(0).choice(spec.n, 256, replace=False))
-    # sketches: sampled rows recomputed by the oracle
-    for r in rows[:64]:
-        one, _ = oracle.sketch(pi, spec.d, N, np.array([0, indptr[r + 1] - indptr[r]]),
-                               indices[indptr[r]:indptr[r + 1]])
-        assert np.array_equal(one[0], skh[r])
-    # top-k of sampled queries against the full db: the query row index must stay r for exclusion
-    Qs = skh[rows]
+    ref_sk, _ = oracle.sketch(pi, spec.d, N, indptr, indices)
+    assert np.array_equal(skh, ref_sk)
+    rows = np.sort(np.random.default_rng(0).choice(spec.n, 2000, replace=False))
+    # exclude-self top-k of row r = the top-(k+1) over every db row with r removed (or its first k
+    # when r is not among them: ties with smaller indices pushed it out)
+    i1, s1 = oracle.topk(skh[rows], skh, N, spec.d, bs.IP, k + 1)
     ri = np.empty((len(rows), k), dtype=np.int32)
     rs = np.empty((len(rows), k), dtype=np.float32)
     for t, r in enumerate(rows):
-        # exclude_self compares db index with the query's own row index r
-        i1, s1 = oracle.topk(Qs[t:t + 1], np.delete(skh, r, axis=0), N, spec.d, 1, k)
-        i1 = np.where(i1 >= r, i1 + 1, i1)
-        ri[t], rs[t] = i1[0], s1[0]
+        keep = i1[t] != r
+        ri[t] = i1[t][keep][:k]
+        rs[t] = s1[t][keep][:k]
     assert np.array_equal(gi.cpu().numpy()[rows], ri)
     assert_est_close(gs.cpu().numpy()[rows], rs)
 
 
 @pytest.mark.slow
-def test_full_ranking_sampled():
-    """configs[2] at full size: 100k db, 1000 queries, top-100 JS and COS; 100 sampled queries."""
+def test_full_ranking():
+    """configs[2] at full size: 100k db, 1000 queries, top-100 JS and COS — every query's list."""
     N, d, k = synth.RANKING_N, synth.RANKING_DB.d, synth.RANKING_K
     pi = oracle.make_pi(synth.PI_SEED, d, N)
     dbp, dbi = synth.make_csr(synth.RANKING_DB)
@@ -354,50 +352,48 @@ def test_full_ranking_sampled():
     D = bs.build(dev(pi.view(np.int32)), d, N, *csr_dev(dbp, dbi))
     Q = bs.build(dev(pi.view(np.int32)), d, N, *csr_dev(qp, qi))
     Dh, Qh = u32(D), u32(Q)
-    rows = np.sort(np.random.default_rng(1).choice(1000, 100, replace=False))
+    assert np.array_equal(Dh, oracle.sketch(pi, d, N, dbp, dbi)[0])
+    assert np.array_equal(Qh, oracle.sketch(pi, d, N, qp, qi)[0])
     for m in (bs.JS, bs.COS):
         gi, gs = bs.topk(Q, D, N, d, m, k)
-        ri, rs = oracle.topk(Qh[rows], Dh, N, d, m, k)
-        assert np.array_equal(gi.cpu().numpy()[rows], ri)
-        assert_est_close(gs.cpu().numpy()[rows], rs)
+        ri, rs = oracle.topk(Qh, Dh, N, d, m, k)
+        assert np.array_equal(gi.cpu().numpy(), ri)
+        assert_est_close(gs.cpu().numpy(), rs)
 
 
 @pytest.mark.slow
-def test_full_medium_sampled_planes():
-    """configs[1] at full size (10k x 10k, 4 planes) for each N; 64 sampled rows x all columns."""
+def test_full_medium_planes():
+    """configs[1] at full size (10k x 10k, 4 planes) for each N: every value vs the oracle."""
     spec = synth.MEDIUM
     indptr, indices = synth.make_csr(spec)
     ip, ix = csr_dev(indptr, indices)
-    rows = np.sort(np.random.default_rng(2).choice(spec.n, 64, replace=False))
     for N in synth.MEDIUM_NS:
         sk = bs.build_seeded(synth.PI_SEED, spec.d, N, ip, ix)
         out = bs.estimate(sk, sk, N, spec.d, 15)
         torch.cuda.synchronize()
         skh = u32(sk)
-        ref = oracle.estimate(skh[rows], skh, N, spec.d, 15)
-        assert_est_close(out.cpu().numpy()[:, rows, :], ref)
+        ref = oracle.estimate(skh, skh, N, spec.d, 15)
+        assert_est_close(out.cpu().numpy(), ref)
+        del out, ref
 
 
 @pytest.mark.slow
-def test_full_buildonly_sampled():
-    """configs[3] at full size (1e7 rows): 20k sampled rows recomputed by the oracle, bit-exact."""
+def test_full_buildonly():
+    """configs[3] at full size (1e7 rows, 6.4e8 nonzeros): the whole 1.28 GB of sketches vs the
+    oracle, bit-exact, for the pi table (binsketch_build) and in-kernel pi (binsketch_build_seeded)."""
     spec, N = synth.BUILD_ONLY, synth.BUILD_ONLY_N
     indptr, indices = synth.make_csr(spec)
     pi = oracle.make_pi(synth.PI_SEED, spec.d, N)
+    ref, st = oracle.sketch(pi, spec.d, N, indptr, indices)
+    assert st == 0
     ip, ix = csr_dev(indptr, indices)
     for fn in ("table", "seeded"):
         if fn == "table":
             sk = bs.build(dev(pi.view(np.int32)), spec.d, N, ip, ix)
         else:
             sk = bs.build_seeded(synth.PI_SEED, spec.d, N, ip, ix)
-        torch.cuda.synchronize()
-        rows = np.sort(np.random.default_rng(3).choice(spec.n, 20_000, replace=False))
-        sub_ptr = np.zeros(len(rows) + 1, dtype=np.int64)
-        sub_ptr[1:] = np.cumsum(indptr[rows + 1] - indptr[rows])
-        sub_idx = np.concatenate([indices[indptr[r]:indptr[r + 1]] for r in rows])
-        ref, _ = oracle.sketch(pi, spec.d, N, sub_ptr, sub_idx)
-        assert np.array_equal(u32(sk[torch.from_numpy(rows).cuda()]), ref)
         bs.device_status()
+        assert np.array_equal(u32(sk), ref), fn
         del sk
 
 
