@@ -147,9 +147,12 @@ binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, con
  * query i, the k database rows with the best estimate under one measure,
  * ordered by (key descending, db index ascending) where key = the estimate
  * (IP, JS, COS) or -HAM; the fp64 key is computed by the recipe above.
- * measure: exactly one BINSKETCH_* bit; 1 <= k <= BINSKETCH_MAX_K (k = 0 is a no-op).
+ * measure: a nonzero mask of BINSKETCH_* bits; with several bits the lists of each measure are
+ * stacked in the order IP, HAM, JS, COS (out_idx / out_score: [popcount(measure)][nq][k]) and the
+ * tensor-core AND-popcount table, when that engine is used, is computed once for all of them.
+ * 1 <= k <= BINSKETCH_MAX_K (k = 0 is a no-op).
  * flags: BINSKETCH_TOPK_EXCLUDE_SELF skips j == i (self-join, R-G18).
- * out_idx: device int32[nq][k]; out_score: device float[nq][k] (the measure's
+ * out_idx: device int32[nq][k]; out_score: device float[nq][k] per measure (the measure's
  * value, not the key). Slots beyond the number of eligible db rows hold
  * idx = -1 and score = NaN.
  * Engine (results identical either way): k <= 64 and N <= 6143 — the fused tensor-core

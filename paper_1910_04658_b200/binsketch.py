@@ -241,10 +241,12 @@ def estimate(A: torch.Tensor, B: torch.Tensor, N: int, d: int, measure: int = 15
 def topk(Q: torch.Tensor, D: torch.Tensor, N: int, d: int, measure: int, k: int, exclude_self: bool = False,
          out_idx: torch.Tensor | None = None, out_score: torch.Tensor | None = None, ws=None):
     nq, ndb = Q.shape[0], D.shape[0]
+    planes = bin(measure & 15).count("1")   # several measures: lists stacked [measure][nq][k]
+    shape = (nq, k) if planes == 1 else (planes, nq, k)
     if out_idx is None:
-        out_idx = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+        out_idx = torch.empty(shape, dtype=torch.int32, device="cuda")
     if out_score is None:
-        out_score = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+        out_score = torch.empty(shape, dtype=torch.float32, device="cuda")
     ws, wp, wn = _workspace(OP_TOPK, nq, ndb, N, k, ws)
     _check("binsketch_topk", _lib().binsketch_topk(
         _words_tensor(Q, "queries") if nq else None, nq, _words_tensor(D, "db") if ndb else None, ndb, N, d,
@@ -410,7 +412,7 @@ def topk_from_host_csr(db_indptr_h: torch.Tensor, db_indices_h: torch.Tensor, pi
     """Host (pinned) CSR in, host top-k lists out, through the C ABI: H2D of the db CSR (and of a
     separate query CSR, if given) and pi -> binsketch_build -> binsketch_topk per measure -> D2H of
     every (idx, score) list. Without a query CSR the db rows are the queries (self-join).
-    Returns (list of (idx_host, score_host), h2d_bytes, d2h_bytes)."""
+    Returns ((idx_host, score_host) — [measure][nq][k] for several measures —, h2d_bytes, d2h_bytes)."""
     b = bufs if bufs is not None else {}
     n = db_indptr_h.numel() - 1
     sep = q_indptr_h is not None
@@ -426,10 +428,11 @@ def topk_from_host_csr(db_indptr_h: torch.Tensor, db_indices_h: torch.Tensor, pi
             b["q_ix"] = torch.empty_like(q_indices_h, device="cuda")
             b["q_sk"] = torch.empty((nq, words(N)), dtype=torch.int32, device="cuda")
         b["ws"] = torch.empty(max(1, workspace_bytes(OP_TOPK, nq, n, N, k)), dtype=torch.uint8, device="cuda")
-        b["out"] = [(torch.empty((nq, k), dtype=torch.int32, device="cuda"),
-                     torch.empty((nq, k), dtype=torch.float32, device="cuda")) for _ in ms]
-        b["out_h"] = [(torch.empty((nq, k), dtype=torch.int32, pin_memory=True),
-                       torch.empty((nq, k), dtype=torch.float32, pin_memory=True)) for _ in ms]
+        shape = (nq, k) if len(ms) == 1 else (len(ms), nq, k)
+        b["out"] = (torch.empty(shape, dtype=torch.int32, device="cuda"),
+                    torch.empty(shape, dtype=torch.float32, device="cuda"))
+        b["out_h"] = (torch.empty(shape, dtype=torch.int32, pin_memory=True),
+                      torch.empty(shape, dtype=torch.float32, pin_memory=True))
     b["db_ip"].copy_(db_indptr_h, non_blocking=True)
     b["db_ix"].copy_(db_indices_h, non_blocking=True)
     b["pi"].copy_(pi_h, non_blocking=True)
@@ -441,9 +444,12 @@ def topk_from_host_csr(db_indptr_h: torch.Tensor, db_indices_h: torch.Tensor, pi
         h2d += q_indptr_h.numel() * 8 + q_indices_h.numel() * 4
         build(b["pi"], d, N, b["q_ip"], b["q_ix"], out=b["q_sk"])
     qs = b["q_sk"] if sep else b["db_sk"]
-    for m, (oi, osc), (hi, hs) in zip(ms, b["out"], b["out_h"]):
-        topk(qs, b["db_sk"], N, d, m, k, exclude_self=exclude_self, out_idx=oi, out_score=osc, ws=b["ws"])
-        hi.copy_(oi, non_blocking=True)
-        hs.copy_(osc, non_blocking=True)
+    mask = 0
+    for m in ms:
+        mask |= m
+    (oi, osc), (hi, hs) = b["out"], b["out_h"]
+    topk(qs, b["db_sk"], N, d, mask, k, exclude_self=exclude_self, out_idx=oi, out_score=osc, ws=b["ws"])
+    hi.copy_(oi, non_blocking=True)
+    hs.copy_(osc, non_blocking=True)
     d2h = len(ms) * nq * k * 8
     return b["out_h"], h2d, d2h

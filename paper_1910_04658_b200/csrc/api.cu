@@ -339,10 +339,14 @@ binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, con
 binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb, uint32_t N,
                                 uint64_t d, uint32_t measure, uint32_t k, uint32_t flags, int32_t* out_idx,
                                 float* out_score, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
-  if (N < 2 || !one_bit(measure) || (flags & ~1u)) return BINSKETCH_EINVAL;
+  if (N < 2 || measure == 0 || (measure & ~15u) || (flags & ~1u)) return BINSKETCH_EINVAL;
   if (nq == 0 || k == 0) return BINSKETCH_OK;
   if (k > BINSKETCH_MAX_K) return BINSKETCH_EUNSUPPORTED;
   if (!queries || !out_idx || !out_score || d == 0 || (ndb > 0 && !db)) return BINSKETCH_EINVAL;
+  // several measures: lists stacked [measure][nq][k] in the order IP, HAM, JS, COS
+  uint32_t mlist[4], nm = 0;
+  for (uint32_t b = 1; b <= 8; b <<= 1)
+    if (measure & b) mlist[nm++] = b;
   if (ndb > 0x7fffffffull) return BINSKETCH_EUNSUPPORTED;   // int32 output indices
   const Layout l = layout(BINSKETCH_OP_TOPK, nq, ndb, N, k);
   if (!ws || ws_bytes < l.total) return BINSKETCH_EWORKSPACE;
@@ -359,6 +363,10 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
                                  : bsk::launch_popcount(db, ndb, W, pd, s);
   if (e != cudaSuccess) return cuda_status(e);
   if (ndb > 0 && use_tc(BINSKETCH_OP_TOPK, N, k)) {
+   for (uint32_t mi = 0; mi < nm; ++mi) {   // fused top-k: one pass per measure
+    const uint32_t measure_m = mlist[mi];
+    int32_t* out_idx_m = out_idx + (size_t)mi * nq * k;
+    float* out_score_m = out_score + (size_t)mi * nq * k;
     // db popcount-sorted (tight per-tile prefilter). Queries popcount-sorted too for JS / COS / HAM
     // (a query tile then has a narrow |a_s| range, so its best candidates — pb near pa — arrive
     // together; Large k = 50: HAM 90 -> 65, JS 214 -> 150, COS 158 -> 119 ms) but not for IP, where
@@ -371,24 +379,26 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
     int32_t* spb = sorted ? reinterpret_cast<int32_t*>(w + l.spb) : pd;
     const char* qs = std::getenv("BINSKETCH_TC_QSORT");
     // (small query sets: the three extra sort launches would dominate a launch-bound call)
-    const bool qsort = sorted && (qs ? !std::strcmp(qs, "1") : (measure != BINSKETCH_IP && nq >= 16384));
+    const bool qsort = sorted && (qs ? !std::strcmp(qs, "1") : (measure_m != BINSKETCH_IP && nq >= 16384));
     int32_t* qperm = qsort ? reinterpret_cast<int32_t*>(w + l.qperm) : nullptr;
     int32_t* qspb = qsort ? reinterpret_cast<int32_t*>(w + l.qspb) : pq;
     uint32_t* bins = reinterpret_cast<uint32_t*>(w + l.bins);
     // order that raises the heaps' thresholds fastest (measured, Large k = 50): IP's best
     // candidates have large pb (descending: 53 vs 262 ms); JS / COS / HAM favour pb close to pa,
     // reached earlier from below (ascending: JS 302 -> 214, COS 260 -> 158, HAM 870 -> 90 ms)
-    if (sorted) e = bsk::launch_sort_by_popcount(pd, ndb, N, bins, perm, spb, s, measure == BINSKETCH_IP);
+    if (sorted) e = bsk::launch_sort_by_popcount(pd, ndb, N, bins, perm, spb, s, measure_m == BINSKETCH_IP);
     if (qsort && e == cudaSuccess) e = bsk::launch_sort_by_popcount(pq, nq, N, bins, qperm, qspb, s);
     if (e == cudaSuccess) e = bsk::launch_expand(queries, nq, N, q8, s, qperm);
     if (e == cudaSuccess) e = bsk::launch_expand(db, ndb, N, d8, s, perm);
     if (e == cudaSuccess)
-      e = bsk::launch_tc_topk(q8, nq, d8, ndb, N, measure, k, flags, qspb, qperm, spb, perm,
+      e = bsk::launch_tc_topk(q8, nq, d8, ndb, N, measure_m, k, flags, qspb, qperm, spb, perm,
                               reinterpret_cast<const double*>(w + l.L), cache().convex(N, d),
-                              reinterpret_cast<double*>(w + l.pkey), reinterpret_cast<int32_t*>(w + l.pidx), out_idx,
-                              out_score, reinterpret_cast<unsigned long long*>(w + l.ctr),
+                              reinterpret_cast<double*>(w + l.pkey), reinterpret_cast<int32_t*>(w + l.pidx),
+                              out_idx_m, out_score_m, reinterpret_cast<unsigned long long*>(w + l.ctr),
                               reinterpret_cast<unsigned int*>(w + l.done), s);
-    return cuda_status(e);
+    if (e != cudaSuccess) return cuda_status(e);
+   }
+    return BINSKETCH_OK;
   }
   const int32_t* pab = nullptr;
   if (ndb > 0 && use_tc_pab(N, nq, ndb, k)) {
@@ -402,11 +412,13 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
     if (e != cudaSuccess) return cuda_status(e);
     pab = pabw;
   }
-  e = bsk::launch_topk(queries, nq, db, ndb, N, measure, k, flags, pq, pd,
+  // the AND-popcount table (when used) serves every requested measure
+  for (uint32_t mi = 0; mi < nm && e == cudaSuccess; ++mi)
+    e = bsk::launch_topk(queries, nq, db, ndb, N, mlist[mi], k, flags, pq, pd,
                          reinterpret_cast<const double*>(w + l.L),
                          l.splits > 1 ? reinterpret_cast<double*>(w + l.pkey) : nullptr,
-                         l.splits > 1 ? reinterpret_cast<int32_t*>(w + l.pidx) : nullptr, out_idx, out_score, s,
-                         pab);
+                         l.splits > 1 ? reinterpret_cast<int32_t*>(w + l.pidx) : nullptr,
+                         out_idx + (size_t)mi * nq * k, out_score + (size_t)mi * nq * k, s, pab);
   return cuda_status(e);
 }
 

@@ -99,7 +99,8 @@ def test_host_detected_errors(lib):
     assert lib.binsketch_estimate(None, 4, None, 4, 64, 10, 0, None, None, 0, None) == EINVAL   # measure 0
     assert lib.binsketch_estimate(None, 4, None, 4, 64, 10, 16, None, None, 0, None) == EINVAL  # bad bit
     assert lib.binsketch_estimate(None, 0, None, 4, 64, 10, 15, None, None, 0, None) == 0       # empty
-    assert lib.binsketch_topk(None, 4, None, 4, 64, 10, 3, 5, 0, None, None, None, 0, None) == EINVAL  # 2 bits
+    assert lib.binsketch_topk(None, 4, None, 4, 64, 10, 16, 5, 0, None, None, None, 0, None) == EINVAL  # bad bit
+    assert lib.binsketch_topk(None, 4, None, 4, 64, 10, 0, 5, 0, None, None, None, 0, None) == EINVAL   # no measure
     assert lib.binsketch_topk(None, 4, None, 4, 64, 10, 1, 5, 2, None, None, None, 0, None) == EINVAL  # flags
     assert lib.binsketch_topk(None, 4, None, 4, 64, 10, 1, 0, 0, None, None, None, 0, None) == 0       # k = 0
     assert lib.binsketch_topk(vp(8), 4, vp(8), 4, 64, 10, 1, 257, 0, vp(8), vp(8), None, 0, None) == EUNSUP

@@ -408,3 +408,19 @@ def test_topk_query_sort_paths(measure, qsort, monkeypatch):
     D[300:340] = D[11]                   # ties across the sorted order
     Q = D[:700].copy()
     _check_topk(Q, D, N, d, measure, 50, exclude_self=True)
+
+
+@pytest.mark.parametrize("k", [20, 100])
+def test_topk_several_measures_in_one_call(k, engine):
+    """measure mask with several bits: lists stacked in IP, HAM, JS, COS order, each identical to
+    the single-measure result (one AND-popcount table for all on the tensor-core pab path)."""
+    N, d = synth.RANKING_N, synth.RANKING_DB.d
+    D = _sketches(synth.scaled(synth.RANKING_DB, 3000), N)
+    Q = _sketches(synth.scaled(synth.RANKING_Q, 150), N)
+    Qd, Dd = dev(Q.view(np.int32)), dev(D.view(np.int32))
+    gi, gs = bs.topk(Qd, Dd, N, d, bs.IP | bs.JS | bs.COS, k)
+    assert gi.shape == (3, 150, k)
+    for t, m in enumerate((bs.IP, bs.JS, bs.COS)):
+        ri, rs = oracle.topk(Q, D, N, d, m, k)
+        assert np.array_equal(gi[t].cpu().numpy(), ri)
+        assert_est_close(gs[t].cpu().numpy(), rs)
