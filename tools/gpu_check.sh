@@ -5,6 +5,7 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/gpu.txt 2>&1
 nproc > gpurun_out/host.txt; lscpu | grep "Model name" >> gpurun_out/host.txt
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
+[ -x tools/microbench ] || nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench tools/microbench.cu
 timeout 120 ./tools/microbench > gpurun_out/microbench.jsonl 2>&1
 if [ -n "$PYTEST_K" ]; then timeout 1500 python -m pytest tests -m gpu -q -k "$PYTEST_K" > gpurun_out/pytest_gpu.log 2>&1; else timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; fi
 echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
