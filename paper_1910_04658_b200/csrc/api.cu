@@ -88,7 +88,7 @@ TableCache& cache() {
 }
 
 struct Layout {
-  size_t L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, qperm = 0, qspb = 0,
+  size_t tmeta = 0, L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, qperm = 0, qspb = 0,
          ctr = 0, done = 0, pab = 0, cnt = 0, x8 = 0, px = 0, pabx = 0, part = 0, total = 0;
   uint32_t splits = 1;
 };
@@ -187,6 +187,7 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
     l.spb = off; off += align_up((size_t)nb * 4);
     l.qperm = off; off += align_up((size_t)na * 4);
     l.qspb = off; off += align_up((size_t)na * 4);
+    l.tmeta = off; off += align_up((size_t)((nb + 255) / 256) * 256 * 8);   // per-tile db metadata
   }
   if (op == BINSKETCH_OP_TOPK) {
     l.splits = tc ? bsk::tc_topk_splits(na, nb, N, k) : bsk::topk_splits(na, nb, k);
@@ -395,7 +396,7 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
                               reinterpret_cast<const double*>(w + l.L), cache().convex(N, d),
                               reinterpret_cast<double*>(w + l.pkey), reinterpret_cast<int32_t*>(w + l.pidx),
                               out_idx_m, out_score_m, reinterpret_cast<unsigned long long*>(w + l.ctr),
-                              reinterpret_cast<unsigned int*>(w + l.done), s);
+                              reinterpret_cast<unsigned int*>(w + l.done), reinterpret_cast<int2*>(w + l.tmeta), s);
     if (e != cudaSuccess) return cuda_status(e);
    }
     return BINSKETCH_OK;

@@ -91,7 +91,7 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
                            uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* qperm,
                            const int32_t* pd, const int32_t* perm, const double* L, bool prefilter, double* part_key,
                            int32_t* part_idx, int32_t* out_idx, float* out_score, unsigned long long* ctr,
-                           unsigned int* done, cudaStream_t s);   // done: ceil(nq/128) words of workspace
+                           unsigned int* done, int2* meta, cudaStream_t s);   // done: ceil(nq/128) words of workspace
 
 // Threshold join on the tensor-core engine (Exp. 2): bits [nthr][nq][ceil(ndb/32)] (every word
 // written by the kernel); tkey descending with tslot[t] its bitmap plane; db rows in their own

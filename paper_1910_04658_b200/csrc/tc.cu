@@ -17,7 +17,10 @@
 //                   stages (A 16 KB + B 32 KB, 128B-swizzled by TMA) through a
 //                   4-deep mbarrier ring; accumulators double-buffered in TMEM
 //                   (2 x 256 int32 columns) so the epilogue of tile t overlaps
-//                   the MMAs of tile t+1.
+//                   the MMAs of tile t+1. With CG = 2 (long K) a CTA pair runs
+//                   cta_group::2 MMAs over a 256 x 256 tile, each CTA staging half
+//                   of the B rows. The fused top-k's per-tile db metadata comes
+//                   through a producer-filled bulk-copy ring.
 #include <cuda.h>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -67,6 +70,12 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
       : "memory");
 }
+// 1-D bulk copy global -> shared (16-B aligned, size a multiple of 16), completing on `bar`
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -91,6 +100,62 @@ __device__ __forceinline__ void mma_u8(uint32_t d_tmem, uint64_t a, uint64_t b, 
 }
 __device__ __forceinline__ void commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// ---- CTA pair (cta_group::2): one MMA over both SMs' shared memory, M = 256 ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// wait with cluster-scope acquire (the phase was completed by the peer CTA, data written remotely)
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "r"(0x100000u)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void st_cluster_u64(uint32_t cluster_addr, uint64_t v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(cluster_addr), "l"(v) : "memory");
+}
+// TMA into this CTA's shared memory, completing bytes on the pair leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int32_t x, int32_t y,
+                                                 uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_u8_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+// arrive on the barrier at this offset in every CTA of `mask` when the pair's MMAs complete
+__device__ __forceinline__ void commit_pair(uint32_t bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+               "h"(mask)
+               : "memory");
 }
 
 // 32 lanes x 32 consecutive columns of 32-bit TMEM -> 32 registers per thread. The wait
@@ -169,6 +234,14 @@ __global__ void expand_kernel(const uint32_t* __restrict__ sk, uint64_t n, uint3
 }
 
 // ------------------------------------------------- db order for top-k ---
+// Per-tile db metadata for the top-k epilogue: meta[i] = (|b_s|, original index) of B row i,
+// padded to whole 256-row tiles with (0, -1), so the producer bulk-loads 2 KB per tile.
+__global__ void tile_meta_kernel(const int32_t* __restrict__ pb, const int32_t* __restrict__ perm, uint64_t nb,
+                                 uint64_t npad, int2* __restrict__ meta) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < npad; i += (uint64_t)gridDim.x * blockDim.x)
+    meta[i] = i < nb ? make_int2(__ldg(pb + i), perm ? __ldg(perm + i) : (int32_t)i) : make_int2(0, -1);
+}
+
 // Counting sort of the db rows by popcount (descending: bin N - pb; or ascending), so every 256-row
 // tensor-core tile spans a narrow popcount range and the per-tile key bound is tight.
 // Order inside a bin is arbitrary: the top-k result is the unique top-k under
@@ -216,8 +289,6 @@ __global__ void pb_scatter_kernel(const int32_t* __restrict__ pb, uint64_t n, ui
 constexpr int kTcM = 128, kTcN = 256;
 constexpr int kTcAcc = 512 / kTcN;   // TMEM accumulators (512 columns)
 constexpr uint32_t kTcSmemMax = 227 * 1024;
-// instruction descriptor: D s32, A/B u8, K-major, N = 256, M = 128
-constexpr uint32_t kTcIdesc = (2u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
 enum TcMode { kTcAndPopc = 0, kTcEstimate = 1, kTcTopk = 2, kTcJoin = 3 };
 constexpr uint32_t kTcMaxThr = 16;   // thresholds per join launch
 
@@ -226,14 +297,18 @@ constexpr uint32_t kTcMaxThr = 16;   // thresholds per join launch
 // recipe per pair, latency-bound) runs 16 warps reading 8-column chunks; the others 4 warps.
 template <int MODE>
 struct TcRoles {
-  static constexpr int kEpi = (MODE == kTcEstimate || MODE == kTcJoin) ? 16 : 4;
+  static constexpr int kEpi = (MODE == kTcEstimate || MODE == kTcJoin) ? 16 : 4;   // TMEM-reading warps
   static constexpr uint32_t kThreads = 64 + 32 * kEpi;
   static constexpr int kCW = (MODE == kTcEstimate || MODE == kTcJoin) ? 8 : 32;   // columns per TMEM load
 };
 
-template <int KC>
+// CG = 1: one CTA per 128 x 256 tile. CG = 2: a CTA pair (cluster of 2, one TPC) computes a
+// 256 x 256 tile with cta_group::2 MMAs: each CTA stages its own 128 A rows and HALF of the
+// 256 B rows (the MMA reads both CTAs' shared memory), and receives its 128 rows x 256 columns
+// in its own TMEM. Same epilogue work per SM, two thirds of the operand bytes per MMA.
+template <int KC, int CG = 1>
 struct TcGeom {
-  static constexpr uint32_t kABytes = kTcM * KC, kBBytes = kTcN * KC, kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kABytes = kTcM * KC, kBBytes = (kTcN / CG) * KC, kStageBytes = kABytes + kBBytes;
 };
 
 // K-major operand tile of KC-byte rows, swizzled as TMA writes it: 8-row atoms of 8*KC
@@ -267,6 +342,7 @@ struct TcParams {
   int32_t* part_idx;
   uint32_t l_smem;        // kTcEstimate: table staged in shared memory (bytes, 0 = not staged)
   uint32_t heap_smem;     // kTcTopk: per-row heaps + survivor scratch in shared memory (bytes)
+  const int2* meta;       // kTcTopk: per db tile [256] (|b_s|, original index), padded to whole tiles
   const int32_t* perm;    // kTcTopk: B row (sorted by |b_s|, descending for IP, else ascending) -> original db index
   uint32_t l_topk_smem;   // kTcTopk: table staged after the heaps (bytes, 0 = global)
   double lc;              // log1p(-1/N): closed-form inverse of the table for the tile bound
@@ -301,13 +377,15 @@ __device__ __forceinline__ uint32_t ge_mask32(const uint32_t (&v)[32], uint32_t 
   return (m[0] | m[1]) | (m[2] | m[3]);
 }
 
-template <int MODE, int KC>
+template <int MODE, int KC, int CG>
 __global__ void __launch_bounds__(TcRoles<MODE>::kThreads, 1)
 tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
-  using G = TcGeom<KC>;
+  using G = TcGeom<KC, CG>;
+  constexpr int kEpi = TcRoles<MODE>::kEpi;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB alignment by pointer arithmetic on the shared array (keeps the shared address space,
-  // so heap / table accesses compile to LDS/STS, not generic LD/ST)
+  // so heap / table accesses compile to LDS/STS, not generic LD/ST). Both CTAs of a pair get
+  // the same offset (same kernel, same dynamic size), as the pair MMA requires.
   uint8_t* smem = smem_raw + ((1024u - (tc::saddr(smem_raw) & 1023u)) & 1023u);
   const uint32_t S = p.stages;
   const uint32_t base = tc::saddr(smem);
@@ -319,21 +397,38 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   const uint32_t tmem_slot = bars + 8u * (2 * S + 2 * kTcAcc);
   // dynamic item schedule: the producer takes items from a global counter (heaviest query
   // tiles first) and publishes them through a 4-slot ring read by the MMA and epilogue roles
+  // (CG = 2: the leader's producer publishes into both CTAs' rings)
   auto ifull = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 1 + k); };
   auto iempty = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 5 + k); };
   const uint32_t iring = bars + 8u * (2 * S + 2 * kTcAcc + 9);   // 4 x u64 item ids
+  // kTcTopk: 4-slot ring of per-tile db metadata, bulk-loaded by the producer
+  auto mfull = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 13 + k); };
+  auto mempty = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 17 + k); };
   uint8_t* extra = smem + S * G::kStageBytes + 1024;        // estimator table or top-k heaps
+  // kTcTopk: the metadata ring [4][256] int2 after the heaps and the survivor scratch
+  int2* meta_s = reinterpret_cast<int2*>(extra + (size_t)p.k * kTcM * 12 + 32 * kTcM * 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? tc::cluster_rank() : 0u;
+  const bool leader = rank == 0u;
 
   if (warp == 0 && lane == 0) {
+    // CG = 2 counts: tempty one arrival per epilogue warp of both CTAs; iempty the leader's MMA
+    // lane + epilogue warps and the peer's producer lane + epilogue warps (the leader's barriers)
     for (uint32_t s = 0; s < S; ++s) { tc::mbar_init(full(s), 1); tc::mbar_init(empty(s), 1); }
-    for (int a = 0; a < kTcAcc; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), 32 * TcRoles<MODE>::kEpi); }
-    for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(ifull(k), 1); tc::mbar_init(iempty(k), 1 + TcRoles<MODE>::kEpi); }   // MMA + epilogue warps
+    for (int a = 0; a < kTcAcc; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), CG == 1 ? 32 * kEpi : 2 * kEpi); }
+    constexpr int kTake = kEpi;   // item consumers besides the MMA / producer lanes
+    for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(ifull(k), 1); tc::mbar_init(iempty(k), CG == 1 ? 1 + kTake : 2 + 2 * kTake); }
+    for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(mfull(k), 1); tc::mbar_init(mempty(k), kEpi); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tmem_slot));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tmem_slot));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tmem_slot));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   const double* L = p.L;
   double* Ls = reinterpret_cast<double*>(extra + ((MODE == kTcTopk || MODE == kTcJoin) ? p.heap_smem : 0u));
@@ -342,59 +437,97 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     L = Ls;
   }
   tc::fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads();
+  else tc::cluster_sync();   // both CTAs' barriers initialised and TMEM allocated
   tc::fence_after();
   uint32_t tmem;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem) : "r"(tmem_slot));
 
-  auto publish_item = [&](uint32_t i) -> uint64_t {   // producer lane
+  auto publish_item = [&](uint32_t i) -> uint64_t {   // producer lane (the leader's when CG = 2)
     const uint32_t k = i & 3u, ph = (i >> 2) & 1u;
     tc::mbar_wait(iempty(k), ph ^ 1u);
     const uint64_t it = atomicAdd(p.item_ctr, 1ull);
     asm volatile("st.shared.u64 [%0], %1;" ::"r"(iring + 8u * k), "l"(it) : "memory");
     tc::mbar_arrive(ifull(k));
+    if constexpr (CG == 2) {
+      tc::st_cluster_u64(tc::mapa(iring + 8u * k, 1u), it);
+      tc::mbar_arrive_cluster(tc::mapa(ifull(k), 1u));   // release.cluster: orders the remote store
+    }
     return it;
   };
   auto take_item = [&](uint32_t i) -> uint64_t {      // one lane per consumer warp
     const uint32_t k = i & 3u, ph = (i >> 2) & 1u;
-    tc::mbar_wait(ifull(k), ph);
     uint64_t it;
-    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(it) : "r"(iring + 8u * k) : "memory");
-    tc::mbar_arrive(iempty(k));
+    if constexpr (CG == 1) {
+      tc::mbar_wait(ifull(k), ph);
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(it) : "r"(iring + 8u * k) : "memory");
+      tc::mbar_arrive(iempty(k));
+    } else {
+      tc::mbar_wait_cluster(ifull(k), ph);
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(it) : "r"(iring + 8u * k) : "memory");
+      tc::mbar_arrive_cluster(tc::mapa(iempty(k), 0u));
+    }
     return it;
   };
   // every role walks the same (item, n-tile) sequence
   // items are chunk-major: all query tiles against db chunk 0, then chunk 1, ... so the
-  // chunk's B operand (sized to stay L2-resident) is fetched from HBM about once
+  // chunk's B operand (sized to stay L2-resident) is fetched from HBM about once.
+  // mt = this CTA's 128-row A tile (item m-index x CG + rank)
   auto item_range = [&](uint64_t it, uint64_t& mt, uint32_t& sp, uint32_t& nt0, uint32_t& nt1) {
     sp = (uint32_t)(it / p.mtiles);
-    mt = it - (uint64_t)sp * p.mtiles;
+    mt = (it - (uint64_t)sp * p.mtiles) * CG + rank;
     nt0 = sp * p.per;
     nt1 = min(nt0 + p.per, p.tiles_n);
   };
+  // epilogue warp done with accumulator a (after its last TMEM load)
+  auto release_acc = [&](int a) {
+    tc::fence_before();
+    if constexpr (CG == 1) {
+      tc::mbar_arrive(tempty(a));
+    } else {
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(tc::mapa(tempty(a), 0u));
+    }
+  };
 
   if (warp == 0) {
-    if (lane == 0) {   // ---- TMA producer
-      uint32_t stage = 0, phase = 0;
+    if (lane == 0) {   // ---- TMA producer (both CTAs: own A rows, own half of the B rows)
+      uint32_t stage = 0, phase = 0, mcount = 0;
       for (uint32_t ii = 0;; ++ii) {
-        const uint64_t it = publish_item(ii);
+        const uint64_t it = (CG == 1 || leader) ? publish_item(ii) : take_item(ii);
         if (it >= p.nitems) break;
         uint64_t mt; uint32_t sp, nt0, nt1;
         item_range(it, mt, sp, nt0, nt1);
         for (uint32_t nt = nt0; nt < nt1; ++nt) {
+          if constexpr (MODE == kTcTopk) {   // the tile's db metadata for the epilogue
+            const uint32_t ms = mcount & 3u;
+            tc::mbar_wait(mempty(ms), ((mcount >> 2) & 1u) ^ 1u);
+            tc::mbar_expect_tx(mfull(ms), kTcN * 8u);
+            tc::bulk_load(tc::saddr(meta_s) + ms * kTcN * 8u, p.meta + (size_t)nt * kTcN, kTcN * 8u, mfull(ms));
+            ++mcount;
+          }
           for (uint32_t kc = 0; kc < p.nk; ++kc) {
             tc::mbar_wait(empty(stage), phase ^ 1u);
             const uint32_t sa = base + stage * G::kStageBytes;
-            tc::mbar_expect_tx(full(stage), G::kStageBytes);
-            tc::tma_load_2d(sa, &tmA, (int32_t)(kc * KC), (int32_t)(mt * kTcM), full(stage));
-            tc::tma_load_2d(sa + G::kABytes, &tmB, (int32_t)(kc * KC), (int32_t)(nt * kTcN), full(stage));
+            if constexpr (CG == 1) {
+              tc::mbar_expect_tx(full(stage), G::kStageBytes);
+              tc::tma_load_2d(sa, &tmA, (int32_t)(kc * KC), (int32_t)(mt * kTcM), full(stage));
+              tc::tma_load_2d(sa + G::kABytes, &tmB, (int32_t)(kc * KC), (int32_t)(nt * kTcN), full(stage));
+            } else {
+              if (leader) tc::mbar_expect_tx(full(stage), 2u * G::kStageBytes);   // both CTAs' bytes
+              const uint32_t fb = tc::mapa(full(stage), 0u);
+              tc::tma_load_2d_pair(sa, &tmA, (int32_t)(kc * KC), (int32_t)(mt * kTcM), fb);
+              tc::tma_load_2d_pair(sa + G::kABytes, &tmB, (int32_t)(kc * KC),
+                                   (int32_t)(nt * kTcN + rank * (kTcN / 2)), fb);
+            }
             if (++stage == S) { stage = 0; phase ^= 1u; }
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {   // ---- MMA issuer
+    if (lane == 0 && leader) {   // ---- MMA issuer (the leader's, for the pair when CG = 2)
+      constexpr uint32_t idesc = (2u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)((kTcM * CG) >> 4) << 24);
       uint32_t stage = 0, phase = 0, aphase = 0;
       int acc = 0;
       for (uint32_t ii = 0;; ++ii) {
@@ -412,12 +545,18 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const uint32_t sa = base + stage * G::kStageBytes;
             const uint64_t da = desc_sw<KC>(sa), db = desc_sw<KC>(sa + G::kABytes);
 #pragma unroll
-            for (int kk = 0; kk < KC / 32; ++kk)   // K = 32 bytes per MMA: +2 in 16-B units
-              tc::mma_u8(d, da + 2u * kk, db + 2u * kk, kTcIdesc, (kc | (uint32_t)kk) != 0u);
-            tc::commit(empty(stage));              // frees the smem stage when these MMAs finish
+            for (int kk = 0; kk < KC / 32; ++kk) {   // K = 32 bytes per MMA: +2 in 16-B units
+              if constexpr (CG == 1) tc::mma_u8(d, da + 2u * kk, db + 2u * kk, idesc, (kc | (uint32_t)kk) != 0u);
+              else tc::mma_u8_pair(d, da + 2u * kk, db + 2u * kk, idesc, (kc | (uint32_t)kk) != 0u);
+            }
+            // frees the smem stage (both CTAs' when CG = 2) when these MMAs finish
+            if constexpr (CG == 1) tc::commit(empty(stage));
+            else tc::commit_pair(empty(stage), (uint16_t)3u);
             if (++stage == S) { stage = 0; phase ^= 1u; }
           }
-          tc::commit(tfull(acc));                  // accumulator ready for the epilogue
+          // accumulator ready for the epilogue (of both CTAs)
+          if constexpr (CG == 1) tc::commit(tfull(acc));
+          else tc::commit_pair(tfull(acc), (uint16_t)3u);
           if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
         }
       }
@@ -438,8 +577,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     int32_t* hi = reinterpret_cast<int32_t*>(extra + (size_t)K * kTcM * 8);
     uint32_t* scr = reinterpret_cast<uint32_t*>(extra + (size_t)K * kTcM * 12);            // [32][128]
     // this warp's copy of the tile's db popcounts [256] and original indices [256]
-    int32_t* tpb = reinterpret_cast<int32_t*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4) + (size_t)(warp - 2) * 2 * kTcN;
-    int32_t* tpm = tpb + kTcN;
+    uint32_t mcount = 0;   // tiles seen: metadata ring slot / phase
     uint2* q = reinterpret_cast<uint2*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4) +
                (size_t)(warp - 2) * kQCap;
     uint4* cq = reinterpret_cast<uint4*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 +
@@ -470,9 +608,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // resume this row's heap from the previous chunk (chunk order per query tile is
         // enforced by the done counters: 4 epilogue warps finish each chunk)
         if (lane == 0) {
-          const unsigned int need = 4u * sp;
+          const unsigned int need = 4u * CG * sp;   // every epilogue warp of the CTA (pair)
           unsigned int v;
-          do { asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.done + mt) : "memory"); } while (v < need);
+          do { asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.done + mt / CG) : "memory"); } while (v < need);
         }
         __syncwarp();
         if (valid) {
@@ -561,29 +699,15 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         c_lo = lo; c_hi = hi_; c_T = T; c_pmin = qq;
         return qq;
       };
-      // per-tile staging of the db popcounts / original indices (8 columns per lane),
-      // loaded one tile ahead into registers, published to this warp's buffer
-      int32_t pf_pb[kTcN / 32], pf_pm[kTcN / 32];
-      auto prefetch = [&](uint32_t nt) {
-#pragma unroll
-        for (int u = 0; u < kTcN / 32; ++u) {
-          const uint64_t col = (uint64_t)nt * kTcN + 32 * u + lane;
-          const bool in = nt < nt1 && col < p.nb;
-          pf_pb[u] = in ? __ldg(p.pb + col) : 0;
-          pf_pm[u] = in ? (p.perm ? __ldg(p.perm + col) : (int32_t)col) : -1;
-        }
-      };
-      prefetch(nt0);
       for (uint32_t nt = nt0; nt < nt1; ++nt) {
         const uint64_t n0 = (uint64_t)nt * kTcN;
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < kTcN / 32; ++u) { tpb[32 * u + lane] = pf_pb[u]; tpm[32 * u + lane] = pf_pm[u]; }
-        __syncwarp();
-        prefetch(nt + 1);                                     // in flight during this tile
+        // this tile's db popcounts / original indices, bulk-loaded by the producer
+        const uint32_t ms = mcount & 3u;
+        tc::mbar_wait(mfull(ms), (mcount >> 2) & 1u);
+        const int2* tm = meta_s + ms * kTcN;
         const uint32_t nval = (uint32_t)min((uint64_t)kTcN, p.nb - n0);
         // the tile's popcount range (the db is popcount-sorted, descending or ascending)
-        if (valid) pmin = tile_pmin(min((uint32_t)tpb[nval - 1], (uint32_t)tpb[0]), max((uint32_t)tpb[nval - 1], (uint32_t)tpb[0]));
+        if (valid) pmin = tile_pmin(min((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x), max((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x));
         const bool direct = __any_sync(0xffffffffu, cnt < K);
         tc::mbar_wait(tfull(acc), aphase);
         tc::fence_after();
@@ -616,8 +740,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 for (int u = 0; u < 4; ++u) {
                   if (mm) {
                     const uint32_t j = __ffs(mm) - 1; mm &= mm - 1;
-                    kk[u] = measure_key(estimate_pair(pa, tpb[c + j], (int)scr[j * kTcM + rt], (int)p.N, Ls, m), m);
-                    ix[u] = tpm[c + j];
+                    const int2 mj = tm[c + j];
+                    kk[u] = measure_key(estimate_pair(pa, mj.x, (int)scr[j * kTcM + rt], (int)p.N, Ls, m), m);
+                    ix[u] = mj.y;
                     nk = (uint32_t)u + 1;
                   }
                 }
@@ -642,11 +767,12 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const double T_o = __shfl_sync(0xffffffffu, T, owner);
             const int32_t Ti_o = __shfl_sync(0xffffffffu, Ti, owner);
             double key = -__longlong_as_double(0x7ff0000000000000LL);
-            if (has) key = measure_key(estimate_pair(pa_o, tpb[e.x], (int)(e.y & 0xFFFFFFu), (int)p.N, Ls, m), m);
+            const int2 me = tm[e.x];
+            if (has) key = measure_key(estimate_pair(pa_o, me.x, (int)(e.y & 0xFFFFFFu), (int)p.N, Ls, m), m);
             // candidates — those that would enter the owner's heap at its current threshold
             // (key, then the tie order of R-G17 on the db index, checked here lane-parallel:
             // rows with tiny sketches tie with thousands of db rows) — go back to their owners
-            const bool cand = has && before(key, tpm[e.x], T_o, Ti_o);
+            const bool cand = has && before(key, me.y, T_o, Ti_o);
             const uint32_t bal = __ballot_sync(0xffffffffu, cand);
             if (bal) {
               // owner-parallel insertion: candidate of evaluating lane e sits in cq[e]; the
@@ -663,7 +789,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               while (mine) {
                 const uint32_t ee = __ffs(mine) - 1; mine &= mine - 1;
                 const uint4 c4 = cq[ee];
-                offer(__hiloint2double((int)c4.w, (int)c4.z), tpm[c4.x]);
+                offer(__hiloint2double((int)c4.w, (int)c4.z), tm[c4.x].y);
               }
               __syncwarp();
             }
@@ -684,8 +810,10 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           chunk(c + 32, vb);
           if (c + 64 < (uint32_t)kTcN) tc::tmem_ld_wait(va);
         }
-        tc::fence_before();
-        tc::mbar_arrive(tempty(acc));
+        release_acc(acc);
+        __syncwarp();   // every lane done with this tile's metadata
+        if (lane == 0) tc::mbar_arrive(mempty(ms));
+        ++mcount;
         if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
       }
       if (valid) {   // partial list of this (row, chunk) — or the row's running heap when chained
@@ -700,7 +828,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (p.chain) {
         __threadfence();
         __syncwarp();
-        if (lane == 0) atomicAdd(p.done + mt, 1u);
+        if (lane == 0) atomicAdd(p.done + mt / CG, 1u);
       }
     }
   } else if (MODE == kTcJoin) {
@@ -782,8 +910,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
           __syncwarp();
         }
-        tc::fence_before();
-        tc::mbar_arrive(tempty(acc));
+        release_acc(acc);
         if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
         if (valid) {
           const uint64_t w0 = (n0 + cg0) >> 5;
@@ -908,17 +1035,18 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
           __syncwarp();
         }
-        tc::fence_before();
-        tc::mbar_arrive(tempty(acc));
+        release_acc(acc);
         if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
       }
     }
   }
   tc::fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads();
+  else tc::cluster_sync();   // no CTA leaves while its peer may still signal its barriers / TMEM
   if (warp == 1) {
     tc::fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if constexpr (CG == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -990,24 +1118,33 @@ static TcSplit tc_split_rule(uint64_t na, uint64_t nb, uint32_t N, bool topk, ui
   return r;
 }
 
+// CTA-pair mode per launch. Pairs halve each SM's share of the B operand (shared-memory and L2
+// traffic per MMA), which pays when the K loop is long and the epilogue is negligible (exact join
+// over d-bit rows: 77.7 -> 68.2 ms, K10); with short K (sketch rows) the coupling of the
+// two epilogues costs more than it saves (Large top-k 52.9 -> 61.7 ms). BINSKETCH_TC_CG=1|2
+// overrides (dev A/B).
+static int tc_cg(uint32_t Kp) {
+  if (const char* e = std::getenv("BINSKETCH_TC_CG")) return std::atoi(e) == 2 ? 2 : 1;
+  return Kp >= 32768u ? 2 : 1;
+}
+
 // Shared launcher: pick ring depth from the shared memory left after `extra_bytes`, build
 // the TMA maps, size the work items (>= 2 per SM when the db can be split).
-template <int MODE, int KC>
-static cudaError_t tc_launch(const uint8_t* A8, const uint8_t* B8, TcParams& p, uint32_t N, uint32_t extra_bytes,
-                             uint32_t force_splits, cudaStream_t s) {
-  using G = TcGeom<KC>;
+template <int MODE, int KC, int CG>
+static cudaError_t tc_launch_cg(const uint8_t* A8, const uint8_t* B8, TcParams& p, uint32_t N, uint32_t extra_bytes,
+                                uint32_t force_splits, cudaStream_t s) {
+  using G = TcGeom<KC, CG>;
   const uint32_t Kp = tc_kpad(N);
   if (p.na > 0x7fffffffull || p.nb > 0x7fffffffull) return cudaErrorInvalidValue;
   const uint32_t fixed = 1024 /* align */ + 1024 /* barriers */ + extra_bytes;
   if (fixed + 2 * G::kStageBytes > kTcSmemMax) return cudaErrorInvalidConfiguration;
   p.stages = std::min<uint32_t>(8, (kTcSmemMax - fixed) / G::kStageBytes);
   alignas(64) CUtensorMap ma, mb;
-  if (!make_map(&ma, A8, p.na, Kp, kTcM, KC) || !make_map(&mb, B8, p.nb, Kp, kTcN, KC)) return cudaErrorNotSupported;
+  if (!make_map(&ma, A8, p.na, Kp, kTcM, KC) || !make_map(&mb, B8, p.nb, Kp, kTcN / CG, KC)) return cudaErrorNotSupported;
   cudaError_t e = cudaSuccess;
   p.nk = Kp / KC;
   p.tiles_n = (uint32_t)((p.nb + kTcN - 1) / kTcN);
-  const uint64_t mtiles = (p.na + kTcM - 1) / kTcM;
-  const uint64_t sms = (uint64_t)num_sms();
+  const uint64_t mtiles = (p.na + kTcM * CG - 1) / (kTcM * CG);   // items' m-index: 128 x CG rows
   if (force_splits) {
     p.splits = force_splits;
   } else {
@@ -1025,16 +1162,44 @@ static cudaError_t tc_launch(const uint8_t* A8, const uint8_t* B8, TcParams& p, 
     if (e != cudaSuccess) return e;
   }
   const uint32_t smem = p.stages * G::kStageBytes + fixed;
-  e = cudaFuncSetAttribute(tc_pairs_kernel<MODE, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = tc_pairs_kernel<MODE, KC, CG>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (!p.item_ctr) return cudaErrorInvalidValue;
   e = cudaMemsetAsync(p.item_ctr, 0, sizeof(unsigned long long), s);
   if (e != cudaSuccess) return e;
-  uint64_t grid = std::min<uint64_t>(p.nitems, sms);
-  if (const char* g = std::getenv("BINSKETCH_TC_GRID")) grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, std::strtoull(g, nullptr, 10)));
-  tc_pairs_kernel<MODE, KC><<<(unsigned)grid, TcRoles<MODE>::kThreads, smem, s>>>(ma, mb, p);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(TcRoles<MODE>::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // persistent: every CTA co-resident (the chained top-k waits on other CTAs' items)
+  uint64_t units = (uint64_t)num_sms() / CG;
+  if (CG > 1) {
+    int ncl = 0;
+    cfg.gridDim = dim3((unsigned)(units * CG));
+    if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl > 0) units = std::min<uint64_t>(units, (uint64_t)ncl);
+    (void)cudaGetLastError();
+  }
+  uint64_t grid = std::min<uint64_t>(p.nitems, units);
+  if (const char* g = std::getenv("BINSKETCH_TC_GRID"))
+    grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, std::strtoull(g, nullptr, 10) / CG));
+  cfg.gridDim = dim3((unsigned)(grid * CG));
+  e = cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
   count_launch();
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+template <int MODE, int KC>
+static cudaError_t tc_launch(const uint8_t* A8, const uint8_t* B8, TcParams& p, uint32_t N, uint32_t extra_bytes,
+                             uint32_t force_splits, cudaStream_t s) {
+  return tc_cg(tc_kpad(N)) == 2 ? tc_launch_cg<MODE, KC, 2>(A8, B8, p, N, extra_bytes, force_splits, s)
+                            : tc_launch_cg<MODE, KC, 1>(A8, B8, p, N, extra_bytes, force_splits, s);
 }
 
 cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
@@ -1089,7 +1254,7 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
                            uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* qperm,
                            const int32_t* pd, const int32_t* perm, const double* L, bool prefilter, double* part_key,
                            int32_t* part_idx, int32_t* out_idx, float* out_score, unsigned long long* ctr,
-                           unsigned int* done, cudaStream_t s) {
+                           unsigned int* done, int2* meta, cudaStream_t s) {
   if (nq == 0 || k == 0) return cudaSuccess;
   if (k > tc_topk_max_k()) return cudaErrorInvalidValue;
   TcParams p = {};
@@ -1098,7 +1263,7 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
   p.lc = std::log1p(-1.0 / (double)N);
   p.prefilter = (prefilter && perm) ? 1u : 0u;   // the per-tile bound needs the popcount-sorted db
   p.part_key = part_key; p.part_idx = part_idx;
-  p.heap_smem = k * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 + 4 * 256 * 8 + 4 * 32 * 16 + 4 * 32 * 4;   // heaps, scratch, tile staging, queues, candidates, owner masks
+  p.heap_smem = k * kTcM * 12 + 32 * kTcM * 4 + 4 * kTcN * 8 + 4 * 256 * 8 + 4 * 32 * 16 + 4 * 32 * 4;   // heaps, scratch, metadata ring, queues, candidates, owner masks
   const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
   if (lb > 48 * 1024) return cudaErrorInvalidValue;   // caller keeps N <= tc_topk_max_n()
   p.l_topk_smem = lb;
@@ -1106,6 +1271,13 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
   const TcSplit sc = tc_split_rule(nq, ndb, N, true, k);
   p.chain = sc.chain;
   p.done = done;
+  {
+    const uint64_t npad = ((ndb + kTcN - 1) / kTcN) * kTcN;
+    const uint64_t blocks = std::min<uint64_t>((npad + 255) / 256, (uint64_t)num_sms() * 8);
+    tile_meta_kernel<<<(unsigned)blocks, 256, 0, s>>>(pd, perm, ndb, npad, meta);
+    count_launch();
+    p.meta = meta;
+  }
   cudaError_t e = tc_launch<kTcTopk, 64>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, sc.splits, s);
   if (e != cudaSuccess) return e;
   const uint32_t lists = p.chain ? 1u : p.splits;

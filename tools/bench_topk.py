@@ -19,6 +19,7 @@ ap.add_argument("--config", default="large")
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--rows", type=int, default=0)
+ap.add_argument("--k", type=int, default=0, help="override k (top-k configs)")
 a = ap.parse_args()
 
 if a.config == "large":
@@ -34,6 +35,8 @@ if q is not None:
     Q = bs.build_seeded(synth.PI_SEED, db.d, N, qp, qx)
 else:
     Q = D
+if a.k and k:
+    k = a.k
 if a.rows:
     Q = Q[: a.rows]
 nq, ndb, W = Q.shape[0], D.shape[0], (N + 31) // 32
