@@ -1119,13 +1119,16 @@ static TcSplit tc_split_rule(uint64_t na, uint64_t nb, uint32_t N, bool topk, ui
 }
 
 // CTA-pair mode per launch. Pairs halve each SM's share of the B operand (shared-memory and L2
-// traffic per MMA), which pays when the K loop is long and the epilogue is negligible (exact join
-// over d-bit rows: 77.7 -> 68.2 ms, K10); with short K (sketch rows) the coupling of the
-// two epilogues costs more than it saves (Large top-k 52.9 -> 61.7 ms). BINSKETCH_TC_CG=1|2
-// overrides (dev A/B).
+// traffic per MMA), which pays when the K loop is long relative to the epilogue: the plain
+// AND-popcount from K = 4096 (8192^2 x 8192: 0.46 -> 0.38 ms; Exp.-1 exact rows, K = 28160:
+// 4.02 -> 3.60 ms; Ranking's table: 3.65 -> 3.59 ms) and every mode from K = 16384 (exact join,
+// K = 102784: 77.7 -> 67.7 ms). With sketch-length K the coupling of the two CTAs' epilogues costs
+// more than it saves (Large top-k 52.9 -> 61.7 ms; estimate / sketch join neutral to -2 %).
+// BINSKETCH_TC_CG=1|2 overrides (dev A/B; K10).
+template <int MODE>
 static int tc_cg(uint32_t Kp) {
   if (const char* e = std::getenv("BINSKETCH_TC_CG")) return std::atoi(e) == 2 ? 2 : 1;
-  return Kp >= 32768u ? 2 : 1;
+  return (Kp >= 16384u || (MODE == kTcAndPopc && Kp >= 4096u)) ? 2 : 1;
 }
 
 // Shared launcher: pick ring depth from the shared memory left after `extra_bytes`, build
@@ -1198,7 +1201,7 @@ static cudaError_t tc_launch_cg(const uint8_t* A8, const uint8_t* B8, TcParams& 
 template <int MODE, int KC>
 static cudaError_t tc_launch(const uint8_t* A8, const uint8_t* B8, TcParams& p, uint32_t N, uint32_t extra_bytes,
                              uint32_t force_splits, cudaStream_t s) {
-  return tc_cg(tc_kpad(N)) == 2 ? tc_launch_cg<MODE, KC, 2>(A8, B8, p, N, extra_bytes, force_splits, s)
+  return tc_cg<MODE>(tc_kpad(N)) == 2 ? tc_launch_cg<MODE, KC, 2>(A8, B8, p, N, extra_bytes, force_splits, s)
                             : tc_launch_cg<MODE, KC, 1>(A8, B8, p, N, extra_bytes, force_splits, s);
 }
 
