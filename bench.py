@@ -337,8 +337,15 @@ def run_ours(args):
         roofline = {"bound": "tensor", "kernel": "tc_pairs_kernel<kTcTopk> (tcgen05.mma kind::i8 + fused top-k)",
                     "achieved": ach, "peak": int8_peak, "unit": "TOPS (int8)", "frac": ach / int8_peak,
                     "peak_basis": "2 x MEASURED_PEAKS bf16_tflops_sustained (nominal int8:bf16 = 2:1)",
-                    "time_basis": "whole top-k stage (expand + popcount + MMA/top-k + merge)",
+                    "time_basis": "whole top-k stage (expand + popcount + MMA/top-k + merge; the kernel is 98.6 % "
+                                  "of it in profiles/r01_k10b/launches_large_v8_summary.txt)",
                     "traffic": None, "popc_equivalent": popc}
+        if args.workload == "large":
+            # DRAM bytes of one launch of this kernel at this workload, from `ncu --set full`
+            # (profiles/r01_tc_topk_large_v8_summary.txt: 4.076 GB read + 0.589 GB written); the
+            # contraction reads its operands from L2 (hit rate ~98 %), so this is not its bound
+            roofline["traffic"] = 4.0755e9 + 0.5891e9
+            roofline["traffic_unit"] = "DRAM bytes per launch (ncu)"
     elif engine != "cuda":
         int8_peak = 2.0 * pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1590.0))
         ach = 2.0 * pairs_per_step * N * args.steps / t_topk / 1e12
