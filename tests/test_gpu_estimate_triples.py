@@ -1,0 +1,63 @@
+"""All-pairs estimate planes over (|a_s|, |b_s|, |a_s AND b_s|) triples, both pair engines.
+
+The estimate epilogues store round32 of the canonical fp64 recipe (bsk_estimator.cuh). These
+tests feed sketches built so that the all-pairs table hits every feasible triple (A rows:
+prefixes of length pa; B rows: bit intervals [s, s + pb)), including empty and saturated
+sketches, and require bit-identical float planes vs the oracle's fp64 recipe rounded to fp32.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1910_04658_b200 import binsketch as bs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    bs._lib()
+    yield
+    torch.cuda.synchronize()
+
+
+def _rows(spans, N):
+    W = (N + 31) // 32
+    out = np.zeros((len(spans), W), dtype=np.uint32)
+    for r, (s, e) in enumerate(spans):
+        bits = np.zeros(W * 32, dtype=np.uint8)
+        bits[s:e] = 1
+        out[r] = np.packbits(bits.reshape(-1, 32)[:, ::-1], axis=1).view(">u4").ravel().astype(np.uint32)
+    return out
+
+
+def _check(N, d, pas, intervals, engine, monkeypatch):
+    monkeypatch.setenv("BINSKETCH_ENGINE", engine)
+    A = _rows([(0, p) for p in pas], N)
+    B = _rows(intervals, N)
+    assert np.array_equal(oracle.popcount(A, N), np.asarray(pas))
+    got = bs.estimate(torch.from_numpy(A.view(np.int32)).cuda(), torch.from_numpy(B.view(np.int32)).cuda(), N, d, 15)
+    ref = oracle.estimate(A, B, N, d, 15)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("engine", ["tc", "cuda"])
+def test_all_triples_small_N(engine, monkeypatch):
+    N = 64
+    pas = list(range(N + 1))
+    intervals = [(s, s + p) for p in range(N + 1) for s in range(0, N - p + 1)]   # every (pb, offset)
+    for d in (64, 1000, 1_000_000):
+        _check(N, d, pas, intervals, engine, monkeypatch)
+
+
+@pytest.mark.parametrize("engine", ["tc", "cuda"])
+@pytest.mark.parametrize("N", [1000, 2000])
+def test_triples_sampled_large_N(engine, N, monkeypatch):
+    rng = np.random.default_rng(N)
+    pas = sorted(set([0, 1, 2, N - 1, N] + rng.integers(0, N + 1, 250).tolist()))
+    pbs = [0, 1, 2, N - 1, N] + rng.integers(0, N + 1, 300).tolist()
+    intervals = [(s, s + p) for p in pbs for s in {0, N - p, int(rng.integers(0, N - p + 1))}]
+    _check(N, 28_102, pas, intervals, engine, monkeypatch)
