@@ -418,9 +418,14 @@ def test_topk_several_measures_in_one_call(k, engine):
     D = _sketches(synth.scaled(synth.RANKING_DB, 3000), N)
     Q = _sketches(synth.scaled(synth.RANKING_Q, 150), N)
     Qd, Dd = dev(Q.view(np.int32)), dev(D.view(np.int32))
-    gi, gs = bs.topk(Qd, Dd, N, d, bs.IP | bs.JS | bs.COS, k)
-    assert gi.shape == (3, 150, k)
-    for t, m in enumerate((bs.IP, bs.JS, bs.COS)):
-        ri, rs = oracle.topk(Q, D, N, d, m, k)
-        assert np.array_equal(gi[t].cpu().numpy(), ri)
-        assert_est_close(gs[t].cpu().numpy(), rs)
+    for ms in ((bs.IP, bs.JS, bs.COS), (bs.JS, bs.COS), (bs.IP, bs.HAM, bs.JS, bs.COS)):
+        # pab path: measures scored two per pass (pairs, plus a single for an odd count)
+        mask = 0
+        for m in ms:
+            mask |= m
+        gi, gs = bs.topk(Qd, Dd, N, d, mask, k, exclude_self=len(ms) == 2)
+        assert gi.shape == (len(ms), 150, k)
+        for t, m in enumerate(ms):
+            ri, rs = oracle.topk(Q, D, N, d, m, k, exclude_self=len(ms) == 2)
+            assert np.array_equal(gi[t].cpu().numpy(), ri)
+            assert_est_close(gs[t].cpu().numpy(), rs)
