@@ -20,6 +20,7 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--rows", type=int, default=0)
 ap.add_argument("--k", type=int, default=0, help="override k (top-k configs)")
+ap.add_argument("--measure", default="", help="override the measure: ip | ham | js | cos")
 a = ap.parse_args()
 
 if a.config == "large":
@@ -37,6 +38,8 @@ else:
     Q = D
 if a.k and k:
     k = a.k
+if a.measure:
+    m = {"ip": bs.IP, "ham": bs.HAM, "js": bs.JS, "cos": bs.COS}[a.measure]
 if a.rows:
     Q = Q[: a.rows]
 nq, ndb, W = Q.shape[0], D.shape[0], (N + 31) // 32
