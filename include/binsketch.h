@@ -117,7 +117,9 @@ binsketch_status binsketch_popcount(const uint32_t* sk, uint64_t n, uint32_t N, 
 
 /* Algorithm 1 line 2: out[i][j] = |A[i] AND B[j]|, computed on the
  * tensor cores as the exact u8 dot product of the sketches widened to {0,1}
- * bytes (tcgen05.mma kind::i8, int32 accumulation; K10).
+ * bytes (tcgen05.mma kind::i8, int32 accumulation; K10). From
+ * 128*ceil(N/128) >= 4096 the engine runs CTA pairs (cta_group::2, clusters of
+ * two); results are identical either way.
  * A: device uint32[na][W]; B: device uint32[nb][W]; out: device int32[na][nb].
  * ws: device workspace of ws_bytes >= binsketch_workspace_bytes(BINSKETCH_OP_ANDPOPC, ...). */
 binsketch_status binsketch_andpopc(const uint32_t* A, uint64_t na, const uint32_t* B, uint64_t nb,
@@ -277,7 +279,8 @@ binsketch_status binsketch_categorical_estimate(const uint32_t* sketches_a, uint
  * function of its arguments (and of the BINSKETCH_ENGINE=cuda|tc A/B override,
  * which must not change between this call and the op). The tensor-core
  * engine's scratch (K10) dominates: the sketches widened to {0,1}
- * bytes, (na + nb) x 128*ceil(N/128) bytes, plus top-k partial lists. */
+ * bytes, (na + nb) x 128*ceil(N/128) bytes, plus top-k partial lists and the
+ * fused top-k's per-tile db metadata (8 bytes per db row, padded to 256 rows). */
 size_t binsketch_workspace_bytes(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k);
 
 /* The cardinality table the library uploads (Alg. 1 line 3):
