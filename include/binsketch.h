@@ -139,8 +139,10 @@ binsketch_status binsketch_andpopc(const uint32_t* A, uint64_t na, const uint32_
  * float[popcount(measure)][na][nb], planes in the order IP, HAM, JS, COS, each
  * value the fp64 result rounded to nearest float.
  * d: ambient dimension (saturation cap).
- * Engine (results identical either way): tensor cores (K10) when W > 32,
- * the CUDA-core LOP3+POPC kernel (K3) otherwise. */
+ * Engine (results identical either way): when na*nb*4 bytes fit the 4 GB table
+ * budget, the tensor-core AND-popcount writes a pab table into the workspace and
+ * an elementwise kernel evaluates the recipe (K10 estimate); otherwise
+ * the fused tensor-core estimate (W > 32) or the CUDA-core LOP3+POPC kernel (K3). */
 binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, const uint32_t* sketches_b,
                                     uint64_t nb, uint32_t N, uint64_t d, uint32_t measure, float* out,
                                     void* ws, size_t ws_bytes, binsketch_stream_t stream);

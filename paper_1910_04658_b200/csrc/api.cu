@@ -120,6 +120,15 @@ bool use_tc_pab(uint32_t N, uint64_t nq, uint64_t ndb, uint32_t k) {
   return !engine_cuda() && !use_tc(BINSKETCH_OP_TOPK, N, k) && nq * ndb * 4 <= kPabBudget;
 }
 
+// All-pairs estimate planes through a pab table: tensor-core AND-popcount into pab[na][nb], then the
+// elementwise recipe kernel at full occupancy (K10 estimate). BINSKETCH_EST_PAB=0|1
+// overrides (dev A/B); the CUDA-core engine override disables it.
+bool use_est_pab(uint64_t na, uint64_t nb) {
+  if (engine_cuda()) return false;
+  if (const char* e = std::getenv("BINSKETCH_EST_PAB")) return std::strcmp(e, "0") != 0 && na * nb * 4 <= kPabBudget;
+  return na * nb * 4 <= kPabBudget;
+}
+
 constexpr uint64_t kMseRows = 4096;   // Experiment-1 row block (two [rows][n] int32 tables)
 
 Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
@@ -160,6 +169,7 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
     l.ctr = off; off += kAlign;
     l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
     l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
+    if (use_est_pab(na, nb)) { l.pab = off; off += align_up((size_t)na * nb * 4); }
     l.total = off;
     return l;
   }
@@ -168,8 +178,9 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
     l.total = off;
     return l;
   }
-  const bool tc = use_tc(op, N, k);
-  const bool tcp = op == BINSKETCH_OP_TOPK && use_tc_pab(N, na, nb, k);
+  const bool ep = op == BINSKETCH_OP_ESTIMATE && use_est_pab(na, nb);
+  const bool tc = !ep && use_tc(op, N, k);
+  const bool tcp = (op == BINSKETCH_OP_TOPK && use_tc_pab(N, na, nb, k)) || ep;
   if (tcp) {
     l.ctr = off; off += kAlign;
     l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
@@ -302,6 +313,23 @@ binsketch_status binsketch_andpopc(const uint32_t* A, uint64_t na, const uint32_
   return cuda_status(e);
 }
 
+// expand, tensor-core AND-popcount into the pab table, elementwise recipe (use_est_pab)
+binsketch_status estimate_via_pab(const uint32_t* A, uint64_t na, const uint32_t* B, uint64_t nb, uint32_t N,
+                                  uint32_t measure, const int32_t* pa, const int32_t* pb, const Layout& l, char* w,
+                                  float* out, cudaStream_t s, bool self, bool bcs, double dcap, double ham_scale) {
+  uint8_t* a8 = reinterpret_cast<uint8_t*>(w + l.a8);
+  uint8_t* b8 = self ? a8 : reinterpret_cast<uint8_t*>(w + l.b8);
+  int32_t* pab = reinterpret_cast<int32_t*>(w + l.pab);
+  cudaError_t e = bsk::launch_expand(A, na, N, a8, s);
+  if (e == cudaSuccess && !self) e = bsk::launch_expand(B, nb, N, b8, s);
+  if (e == cudaSuccess)
+    e = bsk::launch_tc_andpopc(a8, na, b8, nb, N, pab, reinterpret_cast<unsigned long long*>(w + l.ctr), s);
+  if (e == cudaSuccess)
+    e = bsk::launch_estimate_from_pab(pab, na, nb, N, measure, pa, pb, reinterpret_cast<const double*>(w + l.L), out,
+                                      s, bcs, dcap, ham_scale);
+  return cuda_status(e);
+}
+
 binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, const uint32_t* sketches_b,
                                     uint64_t nb, uint32_t N, uint64_t d, uint32_t measure, float* out, void* ws,
                                     size_t ws_bytes, binsketch_stream_t stream) {
@@ -322,6 +350,8 @@ binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, con
   if (e == cudaSuccess) e = self ? cudaMemcpyAsync(pb, pa, na * 4, cudaMemcpyDeviceToDevice, s)
                                  : bsk::launch_popcount(sketches_b, nb, W, pb, s);
   if (e != cudaSuccess) return cuda_status(e);
+  if (use_est_pab(na, nb))
+    return estimate_via_pab(sketches_a, na, sketches_b, nb, N, measure, pa, pb, l, w, out, s, self, false, 0.0, 1.0);
   if (use_tc(BINSKETCH_OP_ESTIMATE, N)) {
     uint8_t* a8 = reinterpret_cast<uint8_t*>(w + l.a8);
     uint8_t* b8 = self ? a8 : reinterpret_cast<uint8_t*>(w + l.b8);
@@ -528,7 +558,10 @@ binsketch_status binsketch_bcs_estimate(const uint32_t* sketches_a, uint64_t na,
   cudaError_t e = bsk::launch_popcount(sketches_a, na, W, pa, s);
   if (e == cudaSuccess) e = self ? cudaMemcpyAsync(pb, pa, na * 4, cudaMemcpyDeviceToDevice, s)
                                  : bsk::launch_popcount(sketches_b, nb, W, pb, s);
-  if (e == cudaSuccess) e = bsk::launch_expand(sketches_a, na, N, a8, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (use_est_pab(na, nb))
+    return estimate_via_pab(sketches_a, na, sketches_b, nb, N, measure, pa, pb, l, w, out, s, self, true, (double)d, 1.0);
+  e = bsk::launch_expand(sketches_a, na, N, a8, s);
   if (e == cudaSuccess && !self) e = bsk::launch_expand(sketches_b, nb, N, b8, s);
   if (e == cudaSuccess)
     e = bsk::launch_tc_estimate(a8, na, b8, nb, N, measure, pa, pb, reinterpret_cast<const double*>(w + l.L), out,
@@ -622,7 +655,10 @@ binsketch_status binsketch_categorical_estimate(const uint32_t* sketches_a, uint
   cudaError_t e = bsk::launch_popcount(sketches_a, na, W, pa, s);
   if (e == cudaSuccess) e = self ? cudaMemcpyAsync(pb, pa, na * 4, cudaMemcpyDeviceToDevice, s)
                                  : bsk::launch_popcount(sketches_b, nb, W, pb, s);
-  if (e == cudaSuccess) e = bsk::launch_expand(sketches_a, na, N, a8, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (use_est_pab(na, nb))
+    return estimate_via_pab(sketches_a, na, sketches_b, nb, N, BINSKETCH_HAM, pa, pb, l, w, out, s, self, false, 0.0, 0.5);
+  e = bsk::launch_expand(sketches_a, na, N, a8, s);
   if (e == cudaSuccess && !self) e = bsk::launch_expand(sketches_b, nb, N, b8, s);
   if (e == cudaSuccess)
     e = bsk::launch_tc_estimate(a8, na, b8, nb, N, BINSKETCH_HAM, pa, pb, reinterpret_cast<const double*>(w + l.L), out,

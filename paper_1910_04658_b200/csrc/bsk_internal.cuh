@@ -44,6 +44,10 @@ cudaError_t launch_onehot(const int32_t* codes, uint64_t n, uint32_t c, const in
 enum PairsMode { kAndPopc = 0, kEstimate = 1 };
 // All-pairs kernel: A[na][W] x B[nb][W]. mode kAndPopc writes int32 out[na][nb];
 // mode kEstimate reads pa/pb/L (device) and writes float planes.
+// Estimate planes from a precomputed AND-popcount table pab[na][nb] (elementwise recipe kernel).
+cudaError_t launch_estimate_from_pab(const int32_t* pab, uint64_t na, uint64_t nb, uint32_t N, uint32_t measure,
+                                     const int32_t* pa, const int32_t* pb, const double* L, float* out, cudaStream_t s,
+                                     bool bcs = false, double dcap = 0.0, double ham_scale = 1.0);
 cudaError_t launch_pairs(int mode, const uint32_t* A, uint64_t na, const uint32_t* B, uint64_t nb,
                          uint32_t N, uint32_t measure, const int32_t* pa, const int32_t* pb,
                          const double* L, void* out, cudaStream_t s);

@@ -412,6 +412,98 @@ static uint32_t next_pow2(uint32_t v) {
 
 static constexpr uint32_t kMaxMergeEntries = 8192;
 
+// ------------------------------------------------ estimate from a pab table ---
+// The all-pairs estimate split in two: the tensor-core AND-popcount writes pab[na][nb] (int32),
+// then this elementwise kernel evaluates the recipe (Alg. 1-4, canonical order) for every pair
+// and writes the float planes. The recipe is latency-bound fp64 work; here it runs at full
+// occupancy (one row segment of 4 columns per thread, 16-B loads and stores) instead of in the
+// 16 epilogue warps of the persistent tensor-core kernel. MM: the measure mask at compile time
+// (15 = every plane), 0 = runtime mask (BCS / scaled Hamming variants too).
+template <int MM>
+__global__ void __launch_bounds__(256)
+estimate_pab_kernel(const int32_t* __restrict__ pab, uint64_t na, uint64_t nb, uint32_t N, uint32_t measure,
+                    const int32_t* __restrict__ pa, const int32_t* __restrict__ pb, const double* __restrict__ Lg,
+                    uint32_t bcs, double dcap, double ham_scale, float* __restrict__ out) {
+  extern __shared__ __align__(16) double Ls[];
+  const bool l_in_smem = N + 1 <= kMaxSmemL;
+  if (l_in_smem)
+    for (uint32_t i = threadIdx.x; i <= N; i += blockDim.x) Ls[i] = Lg[i];
+  __syncthreads();
+  const double* L = l_in_smem ? Ls : Lg;
+  const uint32_t mm = MM ? (uint32_t)MM : measure;
+  const uint64_t plane = na * nb;
+  const bool vec = (nb & 3u) == 0 && (reinterpret_cast<uintptr_t>(pab) & 15u) == 0 &&
+                   (reinterpret_cast<uintptr_t>(pb) & 15u) == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  const uint64_t nb4 = (nb + 3) / 4;
+  for (uint64_t r = blockIdx.y; r < na; r += gridDim.y) {
+    const int a = __ldg(pa + r);
+    for (uint64_t c4 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c4 < nb4; c4 += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t c = 4 * c4;
+      int v[4], b[4];
+      if (vec) {
+        const int4 v4 = __ldcs(reinterpret_cast<const int4*>(pab + r * nb + c));
+        const int4 b4 = __ldg(reinterpret_cast<const int4*>(pb + c));
+        v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
+        b[0] = b4.x; b[1] = b4.y; b[2] = b4.z; b[3] = b4.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          v[u] = c + u < nb ? __ldcs(pab + r * nb + c + u) : 0;
+          b[u] = c + u < nb ? __ldg(pb + c + u) : 0;
+        }
+      }
+      float val[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        Est e;
+        if (MM == 0 && bcs) e = bcs_estimate_pair(a, b[u], v[u], dcap, L, mm);
+        else e = estimate_pair(a, b[u], v[u], (int)N, L, mm);
+        val[0][u] = __double2float_rn(e.ip);
+        val[1][u] = __double2float_rn(MM ? e.ham : __dmul_rn(e.ham, ham_scale));
+        val[2][u] = __double2float_rn(e.js);
+        val[3][u] = __double2float_rn(e.cs);
+      }
+      float* o = out + r * nb + c;
+#pragma unroll
+      for (uint32_t id = 0; id < 4; ++id) {
+        if (!(mm & (1u << id))) continue;
+        float* oq = o + (uint64_t)__popc(mm & ((1u << id) - 1u)) * plane;
+        if (vec) {
+          __stcs(reinterpret_cast<float4*>(oq), make_float4(val[id][0], val[id][1], val[id][2], val[id][3]));
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c + u < nb) __stcs(oq + u, val[id][u]);
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_estimate_from_pab(const int32_t* pab, uint64_t na, uint64_t nb, uint32_t N, uint32_t measure,
+                                     const int32_t* pa, const int32_t* pb, const double* L, float* out, cudaStream_t s,
+                                     bool bcs, double dcap, double ham_scale) {
+  if (na == 0 || nb == 0) return cudaSuccess;
+  const size_t smem = N + 1 <= kMaxSmemL ? (size_t)(N + 1) * 8 : 0;
+  const uint64_t nb4 = (nb + 3) / 4;
+  const unsigned gx = (unsigned)std::min<uint64_t>((nb4 + 255) / 256, 64);
+  const unsigned gy = (unsigned)std::min<uint64_t>(na, std::max<uint64_t>(1, (uint64_t)num_sms() * 16 / gx));
+  const bool all = measure == 15u && !bcs && ham_scale == 1.0;
+  cudaError_t e;
+  if (all) {
+    e = cudaFuncSetAttribute(estimate_pab_kernel<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    estimate_pab_kernel<15><<<dim3(gx, gy), 256, smem, s>>>(pab, na, nb, N, measure, pa, pb, L, 0u, dcap, ham_scale, out);
+  } else {
+    e = cudaFuncSetAttribute(estimate_pab_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    estimate_pab_kernel<0><<<dim3(gx, gy), 256, smem, s>>>(pab, na, nb, N, measure, pa, pb, L, bcs ? 1u : 0u, dcap,
+                                                          ham_scale, out);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
 uint32_t topk_splits(uint64_t nq, uint64_t ndb, uint32_t k) {
   if (nq == 0 || ndb == 0 || k == 0) return 1;
   const uint32_t TQ = k <= 128 - kTBN ? 32u : 16u;   // must match launch_topk

@@ -78,7 +78,10 @@ def test_bcs_build_duplicates_cancel_and_ragged_rows():
 
 @pytest.mark.parametrize("na,nb,N", [(300, 700, synth.TINY_N), (129, 257, 1024), (1, 1, 64), (70, 513, 4096),
                                      (200, 200, 33)])
-def test_bcs_estimate_planes(na, nb, N):
+@pytest.mark.parametrize("path", ["pab", "fused"])
+def test_bcs_estimate_planes(na, nb, N, path, monkeypatch):
+    """pab: tensor-core AND-popcount table + elementwise recipe kernel; fused: the estimate epilogue."""
+    monkeypatch.setenv("BINSKETCH_EST_PAB", "1" if path == "pab" else "0")
     spec = synth.scaled(synth.TINY, na + nb, seed=17)
     indptr, indices = synth.make_csr(spec)
     d = spec.d

@@ -57,7 +57,9 @@ def test_onehot_bad_code_latched():
 
 
 @pytest.mark.parametrize("na,nb,N", [(700, 700, 512), (129, 300, 1224), (1, 1, 64)])
-def test_categorical_estimate_bit_exact(na, nb, N):
+@pytest.mark.parametrize("path", ["pab", "fused"])
+def test_categorical_estimate_bit_exact(na, nb, N, path, monkeypatch):
+    monkeypatch.setenv("BINSKETCH_EST_PAB", "1" if path == "pab" else "0")
     cards = [5, 11, 3, 30, 8, 2]
     X = synth.make_categorical(na + nb, cards, seed=na + nb)
     ip, ix, d, _ = oracle.onehot(X, cards)

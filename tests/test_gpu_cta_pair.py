@@ -55,7 +55,8 @@ def test_andpopc_pair(cg, N, na, nb):
 
 
 @pytest.mark.parametrize("N", [2000, 5000])
-def test_estimate_pair(cg, N):
+def test_estimate_pair(cg, N, monkeypatch):
+    monkeypatch.setenv("BINSKETCH_EST_PAB", "0")   # the fused estimate epilogue on the pair engine
     A = _sketches(synth.scaled(synth.MEDIUM, 300, seed=93), N)
     B = _sketches(synth.scaled(synth.MEDIUM, 450, seed=94), N)
     B[:40] = A[:40]

@@ -35,7 +35,8 @@ def _rows(spans, N):
 
 
 def _check(N, d, pas, intervals, engine, monkeypatch):
-    monkeypatch.setenv("BINSKETCH_ENGINE", engine)
+    monkeypatch.setenv("BINSKETCH_ENGINE", "cuda" if engine == "cuda" else "tc")
+    monkeypatch.setenv("BINSKETCH_EST_PAB", "0" if engine == "tc-fused" else "1")
     A = _rows([(0, p) for p in pas], N)
     B = _rows(intervals, N)
     assert np.array_equal(oracle.popcount(A, N), np.asarray(pas))
@@ -44,7 +45,7 @@ def _check(N, d, pas, intervals, engine, monkeypatch):
     assert np.array_equal(got.cpu().numpy().view(np.uint32), ref.view(np.uint32))
 
 
-@pytest.mark.parametrize("engine", ["tc", "cuda"])
+@pytest.mark.parametrize("engine", ["tc", "tc-fused", "cuda"])
 def test_all_triples_small_N(engine, monkeypatch):
     N = 64
     pas = list(range(N + 1))
@@ -53,7 +54,7 @@ def test_all_triples_small_N(engine, monkeypatch):
         _check(N, d, pas, intervals, engine, monkeypatch)
 
 
-@pytest.mark.parametrize("engine", ["tc", "cuda"])
+@pytest.mark.parametrize("engine", ["tc", "tc-fused", "cuda"])
 @pytest.mark.parametrize("N", [1000, 2000])
 def test_triples_sampled_large_N(engine, N, monkeypatch):
     rng = np.random.default_rng(N)

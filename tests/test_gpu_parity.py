@@ -233,10 +233,13 @@ def test_andpopc_tc_saturated_and_empty_rows():
     assert got.max() == N
 
 
-@pytest.fixture(params=["tc", "cuda"])
+@pytest.fixture(params=["tc", "tc-fused", "cuda"])
 def engine(request, monkeypatch):
-    """Run a test on both pair engines: tensor-core (tcgen05 kind::i8) and CUDA-core (POPC)."""
-    monkeypatch.setenv("BINSKETCH_ENGINE", request.param)
+    """Run a test on both pair engines: tensor-core (tcgen05 kind::i8) and CUDA-core (POPC). All-pairs
+    estimates on the tensor cores go through the pab table + elementwise recipe ("tc") or the fused
+    estimate epilogue ("tc-fused")."""
+    monkeypatch.setenv("BINSKETCH_ENGINE", "cuda" if request.param == "cuda" else "tc")
+    monkeypatch.setenv("BINSKETCH_EST_PAB", "0" if request.param == "tc-fused" else "1")
     return request.param
 
 

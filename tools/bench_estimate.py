@@ -38,8 +38,10 @@ for N in [int(x) for x in a.Ns.split(",")]:
     pi_h = oracle.make_pi(synth.PI_SEED, d, N)
     pi = bs.make_pi(synth.PI_SEED, d, N)
     out = torch.empty((4, n, n), dtype=torch.float32, device="cuda")
-    for kind in ("binsketch-tc", "binsketch-cuda", "bcs-tc"):
+    for kind in ("binsketch-pab", "binsketch-tc", "binsketch-cuda", "bcs-pab", "bcs-tc"):
+        # pab: tensor-core AND-popcount table + elementwise recipe kernel; tc: the fused epilogue
         os.environ["BINSKETCH_ENGINE"] = "cuda" if kind == "binsketch-cuda" else "tc"
+        os.environ["BINSKETCH_EST_PAB"] = "1" if kind.endswith("pab") else "0"
         bcs = kind.startswith("bcs")
         sk = (bs.bcs_build if bcs else bs.build)(pi, d, N, ip, ix)
         op = bs.OP_BCS_ESTIMATE if bcs else bs.OP_ESTIMATE
