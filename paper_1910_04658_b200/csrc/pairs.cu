@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "bsk_device.cuh"
@@ -638,12 +639,21 @@ topk_pab_kernel(const int32_t* __restrict__ pab, uint64_t nq, uint64_t ndb, uint
 template <int CAPW>
 static cudaError_t launch_topk_pab_t(const int32_t* pab, uint64_t nq, uint64_t ndb, uint32_t N, uint32_t measure,
                                      uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* pd, const double* L,
-                                     uint32_t splits, double* part_key, int32_t* part_idx, int32_t* out_idx,
+                                     uint32_t& splits, double* part_key, int32_t* part_idx, int32_t* out_idx,
                                      float* out_score, cudaStream_t s) {
   const bool l_in_smem = N + 1 <= kMaxSmemL;
   const size_t smem = (l_in_smem ? (((size_t)(N + 1) * 8 + 15) & ~(size_t)15) : 0) + (size_t)8 * CAPW * 12;
   cudaError_t e = cudaFuncSetAttribute(topk_pab_kernel<CAPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  // db splits per query: as many as fit ONE wave of resident blocks (<= the workspace bound). A
+  // warp's candidate-buffer sorts grow only like k ln(n/k) with its stream length n, so longer
+  // streams cost fewer sorts in total, and a partial second wave costs a whole wave (Ranking,
+  // 1000 queries: 10 splits 3.48 ms, 6: 2.99, 4: 3.14, 3: 2.35 (one wave), 2: 2.58, 1: 3.60)
+  int bps = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, topk_pab_kernel<CAPW>, 256, smem) != cudaSuccess || bps < 1) bps = 1;
+  const uint64_t wave_warps = (uint64_t)num_sms() * (uint64_t)bps * 8;
+  splits = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(splits, wave_warps / nq));
+  if (const char* ev = std::getenv("BINSKETCH_PAB_SPLITS")) splits = std::max(1u, std::min<uint32_t>(splits, (uint32_t)std::atoi(ev)));   // dev A/B
   const uint64_t warps = nq * splits;
   topk_pab_kernel<CAPW><<<(unsigned)((warps + 7) / 8), 256, smem, s>>>(pab, nq, ndb, N, measure, k, flags, pq, pd, L,
                                                                        splits, part_key, part_idx, out_idx, out_score);
@@ -687,7 +697,7 @@ cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint6
                         const double* L, double* part_key, int32_t* part_idx, int32_t* out_idx,
                         float* out_score, cudaStream_t s, const int32_t* pab) {
   if (nq == 0 || k == 0) return cudaSuccess;
-  const uint32_t splits = topk_splits(nq, ndb, k);
+  uint32_t splits = topk_splits(nq, ndb, k);   // workspace bound; the pab path may use fewer
   cudaError_t e;
   if (pab) {
     e = k <= 128 ? launch_topk_pab_t<256>(pab, nq, ndb, N, measure, k, flags, pq, pd, L, splits, part_key, part_idx,
