@@ -82,6 +82,28 @@ def test_workspace_sizing(lib):
     assert lib.binsketch_workspace_bytes(3, 1000, 100_000, 4096, 100) == topk_small   # pure function
 
 
+def test_workspace_estimate_paths(lib, monkeypatch):
+    """All-pairs estimates: the default tensor-core path holds the int32 pab table (na*nb*4 bytes)
+    in the workspace while it fits the 4 GB budget; the fused epilogue (BINSKETCH_EST_PAB=0) and
+    tables beyond the budget do not (K10b). The env knob is read at each call."""
+    lib.binsketch_workspace_bytes.restype = ctypes.c_size_t
+    lib.binsketch_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
+                                              ctypes.c_uint32]
+    monkeypatch.delenv("BINSKETCH_ENGINE", raising=False)
+    monkeypatch.delenv("BINSKETCH_EST_PAB", raising=False)
+    na, nb = 10_000, 10_000
+    with_table = lib.binsketch_workspace_bytes(2, na, nb, 1000, 0)
+    assert with_table >= na * nb * 4
+    monkeypatch.setenv("BINSKETCH_EST_PAB", "0")
+    fused = lib.binsketch_workspace_bytes(2, na, nb, 1000, 0)
+    assert fused < na * nb * 4 and with_table - fused >= na * nb * 4
+    monkeypatch.delenv("BINSKETCH_EST_PAB")
+    big = lib.binsketch_workspace_bytes(2, 40_000, 40_000, 1000, 0)     # 6.4 GB table: over budget
+    assert big < 40_000 * 40_000 * 4
+    monkeypatch.setenv("BINSKETCH_ENGINE", "cuda")                       # CUDA-core engine: no table
+    assert lib.binsketch_workspace_bytes(2, na, nb, 1000, 0) < na * nb * 4
+
+
 def test_host_detected_errors(lib):
     vp = ctypes.c_void_p
     lib.binsketch_build.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint32, vp, vp, ctypes.c_uint64, vp, vp]
