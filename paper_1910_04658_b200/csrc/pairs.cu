@@ -420,8 +420,10 @@ static constexpr uint32_t kMaxMergeEntries = 8192;
 // occupancy (one row segment of 4 columns per thread, 16-B loads and stores) instead of in the
 // 16 epilogue warps of the persistent tensor-core kernel. MM: the measure mask at compile time
 // (15 = every plane), 0 = runtime mask (BCS / scaled Hamming variants too).
+// 4 blocks per SM (64 registers): latency-bound fp64 chains need the warps (vs 3 blocks at 80 registers:
+// Medium N = 1000 0.91 -> 0.89 ms, BCS 0.96 -> 0.85 ms)
 template <int MM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 estimate_pab_kernel(const int32_t* __restrict__ pab, uint64_t na, uint64_t nb, uint32_t N, uint32_t measure,
                     const int32_t* __restrict__ pa, const int32_t* __restrict__ pb, const double* __restrict__ Lg,
                     uint32_t bcs, double dcap, double ham_scale, float* __restrict__ out) {
