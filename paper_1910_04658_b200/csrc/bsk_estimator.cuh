@@ -160,4 +160,47 @@ __device__ __forceinline__ float key_to_score(double key, uint32_t m) {
 }
 
 
+// First plane of the threshold join (thresholds as keys, descending: planes t >= t0 have
+// key >= tkey[t]) for the estimated JS or COS key, deciding each threshold division-free where
+// that is certain: with the recipe's IP part (the same fp64 operations as estimate_pair),
+// JS >= t <=> ip (1 + t) >= t S and COS >= t <=> ip^2 >= t^2 La Lb (t in (0, 1]); a 1e-12
+// relative margin on both sides covers every rounding of the recipe's quotient, and a threshold
+// inside the margin is settled by the exact key (measure_key(estimate_pair)). Returns the same
+// t0 as scanning with the exact key.
+__device__ __forceinline__ uint32_t join_first_plane(int pa, int pb, int pab, int N, const double* __restrict__ L,
+                                                     uint32_t m, const double* tkey, uint32_t nthr) {
+  const int pu = pa + pb - pab;
+  const double La = L[pa], Lb = L[pb];
+  const double S = __dadd_rn(La, Lb);
+  double ip;
+  if (pu == N && pa < N && pb < N) {
+    ip = 0.0;
+  } else {
+    const double raw = __dsub_rn(S, L[pu]);
+    const double lo = raw > 0.0 ? raw : 0.0;
+    const double cap = La < Lb ? La : Lb;
+    ip = lo < cap ? lo : cap;
+  }
+  bool special = (m == 4u) ? (pa == 0 && pb == 0) || !(__dsub_rn(S, ip) > 0.0) : (pa == 0 || pb == 0);
+  const double lhs_c = m == 4u ? ip : __dmul_rn(ip, ip);
+  const double q = m == 4u ? S : __dmul_rn(La, Lb);
+  uint32_t t0 = nthr;
+  while (t0 > 0 && !special) {
+    const double t = tkey[t0 - 1];
+    if (t <= 0.0) { --t0; continue; }          // keys are clamped to [0, 1]
+    if (t > 1.0) break;
+    double lhs, rhs;
+    if (m == 4u) { lhs = __dmul_rn(lhs_c, __dadd_rn(1.0, t)); rhs = __dmul_rn(t, q); }
+    else { lhs = lhs_c; rhs = __dmul_rn(__dmul_rn(t, t), q); }
+    if (lhs >= __dmul_rn(rhs, 1.0 + 1e-12)) { --t0; continue; }   // certainly key >= t
+    if (lhs <= __dmul_rn(rhs, 1.0 - 1e-12)) break;                 // certainly key < t
+    special = true;                                                // within the margin: exact key
+  }
+  if (special) {
+    const double key = measure_key(estimate_pair(pa, pb, pab, N, L, m), m);
+    while (t0 > 0 && key >= tkey[t0 - 1]) --t0;
+  }
+  return t0;
+}
+
 }  // namespace bsk

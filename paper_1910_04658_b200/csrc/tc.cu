@@ -902,9 +902,13 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const uint32_t j = __ffs(keepm) - 1; keepm &= keepm - 1;
             const int pb = spb_s[j];
             const int pab = (int)sv[lane * (CW + 1) + j];
-            const double key = exact ? exact_key(pa, pb, pab, m) : measure_key(estimate_pair(pa, pb, pab, (int)p.N, L, m), m);
-            uint32_t t0 = nthr;
-            while (t0 > 0 && key >= p.tkey[t0 - 1]) --t0;   // planes t >= t0 pass
+            uint32_t t0 = nthr;   // planes t >= t0 pass
+            if (!exact && (m == 4u || m == 8u)) {
+              t0 = join_first_plane(pa, pb, pab, (int)p.N, L, m, p.tkey, nthr);   // division-free where certain
+            } else {
+              const double key = exact ? exact_key(pa, pb, pab, m) : measure_key(estimate_pair(pa, pb, pab, (int)p.N, L, m), m);
+              while (t0 > 0 && key >= p.tkey[t0 - 1]) --t0;
+            }
             const uint32_t h = (c + j) >> 5, bit = 1u << ((c + j) & 31u);
             for (uint32_t t = t0; t < nthr; ++t) wb[2 * t + h] |= bit;
           }
