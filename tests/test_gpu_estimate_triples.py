@@ -62,3 +62,26 @@ def test_triples_sampled_large_N(engine, N, monkeypatch):
     pbs = [0, 1, 2, N - 1, N] + rng.integers(0, N + 1, 300).tolist()
     intervals = [(s, s + p) for p in pbs for s in {0, N - p, int(rng.integers(0, N - p + 1))}]
     _check(N, 28_102, pas, intervals, engine, monkeypatch)
+
+
+@pytest.mark.parametrize("measure", [4, 8])
+def test_join_thresholds_on_exact_key_values(measure):
+    """Threshold join (sketch keys) with thresholds equal to keys that pairs actually take: the
+    division-free plane decision (join_first_plane) must defer to the exact key inside its margin
+    and reproduce the oracle's bitmaps bit for bit, ties at the threshold included."""
+    from oracle import definitional as D
+    N, d = 64, 1000
+    pas = list(range(N + 1))
+    intervals = [(s, s + p) for p in range(N + 1) for s in range(0, N - p + 1, 3)]
+    A = _rows([(0, p) for p in pas], N)
+    B = _rows(intervals, N)
+    L = D.card_table(N, d)
+    k = 2 if measure == 4 else 3
+    # exact fp64 keys of a few triples (the recipe R-C3) + round values that many pairs hit exactly
+    thr = sorted({D.estimate_canonical(pa, pb, pab, N, L)[k] for pa, pb, pab in
+                  [(10, 20, 5), (30, 30, 30), (40, 12, 7), (64, 64, 64), (17, 33, 9)]} | {0.5, 0.25, 1.0})
+    thr = [t for t in thr if t > 0.0][:16]
+    Ad, Bd = torch.from_numpy(A.view(np.int32)).cuda(), torch.from_numpy(B.view(np.int32)).cuda()
+    got = bs.join(Ad, Bd, N, d, measure, thr).cpu().numpy().view(np.uint32)
+    ref = oracle.join(A, B, N, d, measure, thr)
+    assert np.array_equal(got, ref)
