@@ -422,7 +422,10 @@ static constexpr uint32_t kMaxMergeEntries = 8192;
 // (15 = every plane), 0 = runtime mask (BCS / scaled Hamming variants too).
 // 4 blocks per SM (64 registers): latency-bound fp64 chains need the warps (vs 3 blocks at 80 registers:
 // Medium N = 1000 0.91 -> 0.89 ms, BCS 0.96 -> 0.85 ms)
-template <int MM>
+// SQ: the block owns whole rows (gridDim.x == 1) and memoises the COS denominator
+// sqrt(L[pa] * L[pb]) per |b_s| value in shared memory for each row — the same correctly rounded
+// operations as the recipe, computed N + 1 times per row instead of once per pair.
+template <int MM, bool SQ, bool BCS = false>
 __global__ void __launch_bounds__(256, 4)
 estimate_pab_kernel(const int32_t* __restrict__ pab, uint64_t na, uint64_t nb, uint32_t N, uint32_t measure,
                     const int32_t* __restrict__ pa, const int32_t* __restrict__ pb, const double* __restrict__ Lg,
@@ -433,6 +436,7 @@ estimate_pab_kernel(const int32_t* __restrict__ pab, uint64_t na, uint64_t nb, u
     for (uint32_t i = threadIdx.x; i <= N; i += blockDim.x) Ls[i] = Lg[i];
   __syncthreads();
   const double* L = l_in_smem ? Ls : Lg;
+  double* sq = Ls + (N + 1);
   const uint32_t mm = MM ? (uint32_t)MM : measure;
   const uint64_t plane = na * nb;
   const bool vec = (nb & 3u) == 0 && (reinterpret_cast<uintptr_t>(pab) & 15u) == 0 &&
@@ -440,6 +444,12 @@ estimate_pab_kernel(const int32_t* __restrict__ pab, uint64_t na, uint64_t nb, u
   const uint64_t nb4 = (nb + 3) / 4;
   for (uint64_t r = blockIdx.y; r < na; r += gridDim.y) {
     const int a = __ldg(pa + r);
+    if constexpr (SQ) {
+      __syncthreads();   // the previous row's denominators are no longer read
+      const double La = L[a];
+      for (uint32_t i = threadIdx.x; i <= N; i += blockDim.x) sq[i] = __dsqrt_rn(__dmul_rn(La, L[i]));
+      __syncthreads();
+    }
     for (uint64_t c4 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c4 < nb4; c4 += (uint64_t)gridDim.x * blockDim.x) {
       const uint64_t c = 4 * c4;
       int v[4], b[4];
@@ -459,8 +469,17 @@ estimate_pab_kernel(const int32_t* __restrict__ pab, uint64_t na, uint64_t nb, u
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         Est e;
-        if (MM == 0 && bcs) e = bcs_estimate_pair(a, b[u], v[u], dcap, L, mm);
-        else e = estimate_pair(a, b[u], v[u], (int)N, L, mm);
+        if (BCS || (MM == 0 && bcs)) e = bcs_estimate_pair(a, b[u], v[u], dcap, L, SQ ? (mm & 7u) : mm);
+        else e = estimate_pair(a, b[u], v[u], (int)N, L, SQ ? (mm & 7u) : mm);
+        if constexpr (SQ) {   // COS with the memoised denominator (the recipe's operations)
+          if (a == 0 || b[u] == 0) {
+            e.cs = 0.0;
+          } else {
+            double cv = __ddiv_rn(e.ip, sq[b[u]]);
+            cv = cv > 0.0 ? cv : 0.0;
+            e.cs = cv < 1.0 ? cv : 1.0;
+          }
+        }
         val[0][u] = __double2float_rn(e.ip);
         val[1][u] = __double2float_rn(MM ? e.ham : __dmul_rn(e.ham, ham_scale));
         val[2][u] = __double2float_rn(e.js);
@@ -492,16 +511,28 @@ cudaError_t launch_estimate_from_pab(const int32_t* pab, uint64_t na, uint64_t n
   const unsigned gx = (unsigned)std::min<uint64_t>((nb4 + 255) / 256, 64);
   const unsigned gy = (unsigned)std::min<uint64_t>(na, std::max<uint64_t>(1, (uint64_t)num_sms() * 16 / gx));
   const bool all = measure == 15u && !bcs && ham_scale == 1.0;
+  // COS denominators memoised per row while both tables fit 48 KB and a row is long enough to
+  // amortise them (N + 1 square roots per row against nb pairs)
+  // (BCS too: its COS is ip / sqrt(B[pa] B[pb]) over its own table, the same memo)
+  const bool sqm = measure == 15u && ham_scale == 1.0 && (size_t)(N + 1) * 16 <= 48 * 1024 && nb >= 4 * (uint64_t)(N + 1);
   cudaError_t e;
-  if (all) {
-    e = cudaFuncSetAttribute(estimate_pab_kernel<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (sqm) {
+    const size_t smem2 = (size_t)(N + 1) * 16;
+    const unsigned gy2 = (unsigned)std::min<uint64_t>(na, (uint64_t)num_sms() * 16);
+    auto kern = bcs ? estimate_pab_kernel<15, true, true> : estimate_pab_kernel<15, true, false>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (e != cudaSuccess) return e;
-    estimate_pab_kernel<15><<<dim3(gx, gy), 256, smem, s>>>(pab, na, nb, N, measure, pa, pb, L, 0u, dcap, ham_scale, out);
+    kern<<<dim3(1, gy2), 256, smem2, s>>>(pab, na, nb, N, measure, pa, pb, L, bcs ? 1u : 0u, dcap, ham_scale, out);
+  } else if (all) {
+    e = cudaFuncSetAttribute(estimate_pab_kernel<15, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    estimate_pab_kernel<15, false><<<dim3(gx, gy), 256, smem, s>>>(pab, na, nb, N, measure, pa, pb, L, 0u, dcap,
+                                                                  ham_scale, out);
   } else {
-    e = cudaFuncSetAttribute(estimate_pab_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(estimate_pab_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    estimate_pab_kernel<0><<<dim3(gx, gy), 256, smem, s>>>(pab, na, nb, N, measure, pa, pb, L, bcs ? 1u : 0u, dcap,
-                                                          ham_scale, out);
+    estimate_pab_kernel<0, false><<<dim3(gx, gy), 256, smem, s>>>(pab, na, nb, N, measure, pa, pb, L, bcs ? 1u : 0u, dcap,
+                                                                 ham_scale, out);
   }
   count_launch();
   return cudaGetLastError();

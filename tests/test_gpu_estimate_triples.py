@@ -85,3 +85,24 @@ def test_join_thresholds_on_exact_key_values(measure):
     got = bs.join(Ad, Bd, N, d, measure, thr).cpu().numpy().view(np.uint32)
     ref = oracle.join(A, B, N, d, measure, thr)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("bcs", [False, True])
+@pytest.mark.parametrize("N", [500, 1224])
+def test_estimate_rows_memoised_cos_denominator(bcs, N, monkeypatch):
+    """Rows of >= 4 (N + 1) db columns take the recipe kernel's per-row memo of sqrt(L[pa] L[pb])
+    (pairs.cu, SQ); the planes stay bit-identical to the oracle (BinSketch and BCS)."""
+    import synth
+    monkeypatch.setenv("BINSKETCH_ENGINE", "tc")
+    monkeypatch.setenv("BINSKETCH_EST_PAB", "1")
+    spec = synth.scaled(synth.MEDIUM, 90 + 4 * (N + 1) + 7, seed=31 + N)
+    ip, ix = synth.make_csr(spec)
+    pi = oracle.make_pi(synth.PI_SEED, spec.d, N)
+    S, _ = (oracle.bcs_sketch if bcs else oracle.sketch)(pi, spec.d, N, ip, ix)
+    A, B = S[:90], S[90:]
+    B[0] = 0
+    B[5] = A[3]
+    Ad, Bd = torch.from_numpy(A.view(np.int32)).cuda(), torch.from_numpy(B.view(np.int32)).cuda()
+    got = (bs.bcs_estimate if bcs else bs.estimate)(Ad, Bd, N, spec.d, 15).cpu().numpy()
+    ref = (oracle.bcs_estimate if bcs else oracle.estimate)(A, B, N, spec.d, 15)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
