@@ -432,3 +432,16 @@ def test_topk_several_measures_in_one_call(k, engine):
             ri, rs = oracle.topk(Q, D, N, d, m, k, exclude_self=len(ms) == 2)
             assert np.array_equal(gi[t].cpu().numpy(), ri)
             assert_est_close(gs[t].cpu().numpy(), rs)
+
+
+@pytest.mark.parametrize("measure", [bs.JS, bs.COS])
+def test_topk_pab_single_split_direct_outputs(measure, monkeypatch):
+    """k > 64 takes the tensor-core pab table + threshold top-k; with more queries than one wave of
+    warps the launcher picks ONE db split per query and the kernel writes the lists directly (no
+    merge). Ties and duplicated db rows included."""
+    monkeypatch.setenv("BINSKETCH_ENGINE", "tc")
+    N, d = synth.RANKING_N, synth.RANKING_DB.d
+    D = _sketches(synth.scaled(synth.RANKING_DB, 700, seed=57), N)
+    D[40:60] = D[3]
+    Q = _sketches(synth.scaled(synth.RANKING_Q, 4000, seed=58), N)
+    _check_topk(Q, D, N, d, measure, 100)
