@@ -76,37 +76,72 @@ cudaError_t launch_make_pi(uint64_t seed, uint64_t d, uint32_t N, uint32_t* pi, 
 }
 
 // ------------------------------------------------------------------ K1 ----
-// Sketch construction, v4. A warp owns a tile of RW <= 32 consecutive rows (lane l holds
-// row l's [start, end)); the tile's nonzeros are one contiguous span of `indices`, which
-// the warp streams as coalesced 16-byte quads (lane l: elements 4l..4l+3 and
-// 128+4l..128+4l+3 of each 256-element iteration, next iteration prefetched).
+// Sketch construction, v5: one continuous element stream per warp.
 //
-// Row of an element without a search: rows are compacted to the NONEMPTY ones (their
-// end offsets are distinct), and for each 2048-element chunk of the span the warp builds
-// in shared memory a bitmap P with bit q set iff a nonempty row ends at chunk offset q,
-// plus, per 32-bit word w of P, B[w] = the tile address of the row live at the word's
-// start. The row of element q is then B[q/32] + popc(P[q/32] & mask_le(q)) rows on — an
-// AND, a POPC and an IMAD per element, no loop and no divergence.
+// A warp owns a contiguous range of row tiles (RW rows each) and streams the range's
+// nonzeros, indices[indptr[Ra] .. indptr[Rb]), as ONE sequence of stages (S elements,
+// 1-D bulk copies issued by lane 0 into a per-warp shared ring, completion on an
+// mbarrier) — no per-tile restart and no half-empty tail stage per tile. Stage data are
+// read as 16-byte quads: lane l holds elements 4l..4l+3 (+128 h) of each 256-element half.
 //
-// pi(i) comes from (MODE):
-//   kPiSeeded  : the splitmix64 recipe evaluated in registers (no table);
-//   kPiSmem16  : the whole table as uint16 in shared memory (d small);
-//   kPiCache16 : a direct-mapped shared-memory cache of the table, 64K uint16 slots
-//                entry = (i >> 16) << vb | pi(i), prefilled with slot s <- pi(s);
-//   kPiCache32 : the same with 32K uint32 slots when tag + value need more than 16 bits;
-//   kPiGlobal  : read-only L1/L2 gather.
-// Since pi is read-only every entry ever written is correct, so racing fills are benign.
-// Bits are OR-ed into the warp's shared tile (RED.OR), and the tile is written once with
-// coalesced streaming stores — every output word exactly once, no memset.
+// Rows live in a per-warp shared ring of RR = 2 RW sketch rows (compact: empty rows take
+// no slot). The two oldest unflushed tiles t, t+1 form the WINDOW: a stage is processed
+// up to the window end (the end of tile t+1); when tile t is complete it is flushed
+// (every output word written once, coalesced 16-byte streaming stores, then its ring rows
+// re-zeroed) and tile t+2 enters the window. Rows of a stage that lie beyond the window
+// are processed in a further pass over the same stage data (only when 2 tiles hold fewer
+// than S nonzeros).
+//
+// Row of an element without a search: a 2048-element bitmap P (bit q: a nonempty window
+// row ends at offset q) plus, per 32-bit word w, B[w] = the ring row live at the word's
+// start; the row of element q is B[q/32] + popc(P[q/32] & mask_le(q)) — wrapped into the
+// ring with one LOP3 (ring bytes a power of two, ring base aligned to it).
+//
+// pi(i) comes from (MODE): kPiSeeded (splitmix64 recipe in registers), kPiSmem16 (the whole
+// table in shared memory as uint16), kPiCache16 / kPiCache32 (direct-mapped shared cache of
+// the table, entry = tag:value), kPiGlobal (read-only L1/L2 gather). pi is read-only, so
+// every cache entry ever written is correct and racing fills are benign.
+// Bits are OR-ed (XOR for the BCS parity sketch) into the ring with shared reductions.
 enum PiMode { kPiSeeded = 0, kPiSmem16 = 1, kPiCache16 = 2, kPiCache32 = 3, kPiGlobal = 4 };
 
-constexpr int kIter = 256;                      // elements per warp iteration (2 quads per lane)
-constexpr int kChunk = 2048;                    // elements per row-boundary bitmap chunk
-constexpr int kChunkWords = kChunk / 32;        // 64 {P, B} pairs
-constexpr uint32_t kMetaBytes = kChunkWords * 8 + 32 * 4;   // {P,B} pairs + compact row index
-constexpr uint32_t kCache16Slots = 65536;       // 128 KB
-constexpr uint32_t kCache32Slots = 32768;       // 128 KB
+constexpr int kChunk = 2048;                  // elements per row-boundary bitmap
+constexpr int kChunkWords = kChunk / 32;      // 64 {P, B} pairs
+constexpr uint32_t kMetaBytes = kChunkWords * 8;
+constexpr uint32_t kCache16Slots = 65536;     // 128 KB
+constexpr uint32_t kCache32Slots = 32768;     // 128 KB
 constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kNS = 2;                        // stage ring depth per warp
+constexpr uint32_t kAuxFixed = kMetaBytes + 16 * kNS;  // bitmap + mbarriers (per warp; + a zero row of 4W bytes)
+
+// Per-mode launch shape. Cache / shared-table modes: one 512-thread block per SM (the table
+// shared by all warps), 1 KB stages; the others: BSK_BUILD_BLOCKS blocks of BSK_BUILD_THREADS
+// per SM, 4 KB stages (measured: DESIGN.md K1).
+#ifndef BSK_BUILD_STAGE
+#define BSK_BUILD_STAGE 1024      // elements per stage (register-pi modes)
+#endif
+#ifndef BSK_BUILD_THREADS
+#define BSK_BUILD_THREADS 384
+#endif
+#ifndef BSK_BUILD_BLOCKS
+#define BSK_BUILD_BLOCKS 1
+#endif
+#ifndef BSK_BUILD_RRMAX
+#define BSK_BUILD_RRMAX 64        // ring rows cap (tiles of RR / 2 rows)
+#endif
+#ifndef BSK_BUILD_PI_STAGE
+#define BSK_BUILD_PI_STAGE 256    // elements per stage (shared-memory pi modes)
+#endif
+#ifndef BSK_BUILD_PI_THREADS
+#define BSK_BUILD_PI_THREADS 384
+#endif
+template <int MODE>
+struct BuildCfg {
+  static constexpr bool kSmemPi = !(MODE == kPiSeeded || MODE == kPiGlobal);
+  static constexpr int kThreads = kSmemPi ? BSK_BUILD_PI_THREADS : BSK_BUILD_THREADS;
+  static constexpr int kBlocks = kSmemPi ? 1 : BSK_BUILD_BLOCKS;
+  static constexpr int kStage = kSmemPi ? BSK_BUILD_PI_STAGE : BSK_BUILD_STAGE;   // elements per stage
+  static constexpr int kStageBytes = kStage * 4;
+};
 
 struct BuildParams {
   const uint32_t* pi;
@@ -116,16 +151,19 @@ struct BuildParams {
   const int32_t* indices;
   uint64_t n;
   uint32_t* out;
-  uint32_t d, W, RW;
-  uint32_t pi_bytes;     // shared bytes before the per-warp regions
-  uint32_t warp_bytes;   // per-warp region: meta (kMetaBytes), cp.async ring, RW x W tile
-  uint32_t vb;           // cache: value bits
+  uint64_t ntiles;        // ceil(n / RW)
+  uint32_t d, W, RR;      // RR: ring rows (power of two >= 4); tiles of RW = RR / 2 rows
+  uint32_t pi_bytes;      // shared bytes of the pi table / cache (block-wide, first)
+  uint32_t ring_align;    // alignment of the rings (RR * 4W when N is a power of two, else 16)
+  uint32_t aux_bytes;     // per-warp stages + bitmap + mbarriers
+  uint32_t vb;            // cache: value bits
+  uint32_t out16;         // out 16-B aligned and W % 4 == 0: vector flush
   unsigned int* status;
 };
 
 // 32-bit shared-memory accessors: shared addresses stay in one register, no generic
-// conversion per access. Volatile keeps them ordered among themselves; none clobbers
-// "memory", so global loads (indices, pi) schedule freely around them.
+// conversion per access. Volatile keeps them ordered among themselves (and after the
+// mbarrier waits); none clobbers "memory", so global loads schedule freely around them.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -158,16 +196,27 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void sts_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w));
 }
-__device__ __forceinline__ void red_or_shared(uint32_t a, uint32_t v) {
-  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
-}
-__device__ __forceinline__ void red_xor_shared(uint32_t a, uint32_t v) {
-  asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(a), "r"(v));
-}
-// A sketch bit: OR (BinSketch) or XOR (BCS parity buckets).
+// A sketch bit: OR (BinSketch) or XOR (BCS parity buckets),
+// optionally predicated (no branch: the partial-stage path stays convergent).
 template <bool XOR>
 __device__ __forceinline__ void put_bit(uint32_t a, uint32_t v) {
-  if (XOR) red_xor_shared(a, v); else red_or_shared(a, v);
+  if (XOR) asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(a), "r"(v));
+  else asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+template <bool XOR>
+__device__ __forceinline__ void put_bit_if(bool pred, uint32_t a, uint32_t v) {
+  if (XOR)
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.xor.b32 [%0], %1;\n\t}"
+                 ::"r"(a), "r"(v), "r"((uint32_t)pred));
+  else
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}"
+                 ::"r"(a), "r"(v), "r"((uint32_t)pred));
+}
+// a * b + c on the FMA pipe (IMAD): the ALU pipe is the busier one in K1's inner loop
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
 }
 // 1 << (x mod 32) in one funnel shift (shf.l.wrap takes the shift amount mod 32).
 __device__ __forceinline__ uint32_t bit_of(uint32_t x) {
@@ -181,6 +230,36 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// mbarrier + 1-D bulk copy (TMA engine) for the per-warp index stream.
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+// generic-proxy accesses to a ring slot before the async proxy (bulk copy) overwrites it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // 64-bit x * c (mod 2^64) as exactly three 32-bit multiplies (mul.wide + 2 mad.lo).
 __device__ __forceinline__ uint64_t mul64c(uint64_t x, uint32_t clo, uint32_t chi) {
   uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32), rlo, rhi;
@@ -193,11 +272,9 @@ __device__ __forceinline__ uint64_t mul64c(uint64_t x, uint32_t clo, uint32_t ch
   return ((uint64_t)rhi << 32) | rlo;
 }
 
-// pi(i) for a power-of-two N; seed1 = seed + gamma, so seed + (i+1)*gamma = seed1 + i*gamma.
-// Only the low log2(N) bits of the finalizer are needed. Pipe balance (ncu): every IMAD
-// form runs on the FMA-heavy pipe at half the ALU-pipe rate, so the xor-shifts stay on the
-// ALU (SHF + LOP3) and the three 64-bit multiplies are the only IMADs. Returns x, the low
-// finalizer word before masking (j = x & (N-1); x & 31 = j & 31 when N >= 32).
+// pi(i) for a power-of-two N; seed1 = seed + gamma, so seed + (i+1)*gamma = seed1 + i*gamma
+// (one wide multiply-add). Only the low log2(N) bits of the finalizer are needed. Returns
+// x, the low finalizer word before masking (j = x & (N-1); x & 31 = j & 31 when N >= 32).
 __device__ __forceinline__ uint32_t pi_pow2_raw(uint64_t seed1, uint32_t i) {
   uint32_t zl, zh;   // z = seed1 + i * gamma (64-bit), as a carry chain of 32-bit multiply-adds
   asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\t"
@@ -220,60 +297,45 @@ __device__ __forceinline__ uint32_t ldg_if(const uint32_t* ptr, bool pred, uint3
   return v;
 }
 
-// Per-mode launch shape. 24 warps per SM (<= 85 registers): cache / shared-table modes as
-// one 768-thread block (the cache shared by all warps), the others as two 384-thread
-// blocks. kStages: depth of each warp's cp.async ring of index quads (kStages-1 iterations
-// of 1 KB in flight per warp: 72 KB per SM for the seeded / global modes).
-template <int MODE>
-struct BuildCfg {
-  static constexpr bool kSmemPi = !(MODE == kPiSeeded || MODE == kPiGlobal);
-  static constexpr int kThreads = kSmemPi ? 512 : 256;     // per block
-  static constexpr int kBlocks = kSmemPi ? 1 : 3;          // per SM (launch bound)
-  static constexpr int kStages = 2;                        // ring depth
-  static constexpr int kStage = kSmemPi ? 256 : 512;       // elements per ring stage
-  static constexpr int kStageBytes = kStage * 4;
+// One row tile in registers (warp-collective state): lane l < rows holds the end offset
+// (relative to the warp's stream base) of the tile's row l; lanes >= rows hold the tile end.
+struct Tile {
+  int e;          // end of this lane's row (monotone across lanes)
+  uint32_t ne;    // nonempty-row mask
+  uint32_t c;     // compact index of the tile's first nonempty row (ring row = c mod RR)
+  int tend;       // end of the tile's last row
+  uint32_t rows;  // rows in the tile
 };
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int K>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K)); }
-
-// LOGN > 0: N = 2^LOGN >= 32 compiled in (sketch-word and row shifts become immediates);
-// LOGN = 0: any N. XOR: BCS parity sketch (bits toggled instead of set).
-template <int MODE, int LOGN, bool VEC, bool XOR>
+template <int MODE, int LOGN, bool XOR>
 __global__ void __launch_bounds__(BuildCfg<MODE>::kThreads, BuildCfg<MODE>::kBlocks)
 build_kernel(const BuildParams p) {
-  constexpr int NS = BuildCfg<MODE>::kStages;
-  constexpr int kStage = BuildCfg<MODE>::kStage, kStageBytes = BuildCfg<MODE>::kStageBytes;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
-  const uint32_t N = p.mn.N, W = p.W, RW = p.RW, Wb = 4 * W, d = p.d;
-  const uint32_t pi_a = smem_u32(smem);
-  // per-warp region: {P,B} pairs | compact row index [32] | ring [NS][kStageBytes] | tile [RW+2][W]
-  const uint32_t meta_a = pi_a + p.pi_bytes + (uint32_t)warp * p.warp_bytes;
-  const uint32_t crow_a = meta_a + kChunkWords * 8;
-  const uint32_t ring_a = meta_a + kMetaBytes;
-  const uint32_t tile_a = ring_a + NS * kStageBytes;
-  const uint64_t seed1 = p.seed + 0x9E3779B97F4A7C15ULL;
-  constexpr uint32_t kSlots = MODE == kPiCache16 ? kCache16Slots : kCache32Slots;
-  constexpr uint32_t kSlotBits = MODE == kPiCache16 ? 16 : 15;
-  const uint32_t vb = p.vb, vmask = (1u << vb) - 1u;
+  constexpr int S = BuildCfg<MODE>::kStage, SB = BuildCfg<MODE>::kStageBytes;
   constexpr bool POW2 = LOGN > 0;
   constexpr uint32_t wmask = POW2 ? ((1u << LOGN) - 1u) & ~31u : 0u;   // j & wmask = 32 * (j / 32)
   constexpr uint32_t wsh = POW2 ? LOGN - 3 : 0;                         // log2(4W)
+  constexpr uint32_t kSlots = MODE == kPiCache16 ? kCache16Slots : kCache32Slots;
+  constexpr uint32_t kSlotBits = MODE == kPiCache16 ? 16 : 15;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const uint32_t N = p.mn.N, W = p.W, Wb = 4 * W, d = p.d, RR = p.RR, RW = RR >> 1;
+  const uint32_t ringB = RR * Wb;
+  const uint32_t pi_a = smem_u32(smem);
+  const uint32_t rows0 = (pi_a + p.pi_bytes + p.ring_align - 1) & ~(p.ring_align - 1);
+  const uint32_t ring_a = rows0 + (uint32_t)warp * ringB;
+  const uint32_t stage_a = rows0 + (uint32_t)nwarps * ringB + (uint32_t)warp * p.aux_bytes;
+  const uint32_t meta_a = stage_a + kNS * SB;
+  const uint32_t mbar_a = meta_a + kMetaBytes;
+  const uint32_t zero_a = mbar_a + 8 * kNS;           // one all-zero sketch row (flush of empty rows)
+  const uint64_t seed1 = p.seed + 0x9E3779B97F4A7C15ULL;
+  const uint32_t vb = p.vb, vmask = (1u << vb) - 1u;
 
   unsigned bad = 0;
-  uint32_t maxj = 0;
+  uint32_t maxj = 0, maxidx = 0;
   if (MODE == kPiSmem16) {
     for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
-      uint32_t v = __ldg(p.pi + i);
+      const uint32_t v = __ldg(p.pi + i);
       maxj = max(maxj, v);
       sts_u16(pi_a + 2 * i, min(v, N - 1));
     }
@@ -285,199 +347,262 @@ build_kernel(const BuildParams p) {
       if (MODE == kPiCache16) sts_u16(pi_a + 2 * s, v); else sts_u32(pi_a + 4 * s, v);
     }
   }
-  if (BuildCfg<MODE>::kSmemPi) __syncthreads();
+  for (uint32_t w = 4 * lane; w < RR * W; w += 128) sts_v4(ring_a + 4 * w, 0u, 0u, 0u, 0u);
+  for (uint32_t w = lane; w < W; w += 32) sts_u32(zero_a + 4 * w, 0u);
+  if (lane == 0) {
+    for (int s = 0; s < kNS; ++s) mbar_init(mbar_a + 8 * s, 1);
+    fence_proxy_async();
+  }
+  __syncthreads();
 
-  // lane constants: masks selecting chunk-word bits <= element (4*lane + k) mod 32
+  // lane constants: masks selecting bitmap-word bits <= element (4*lane + k) mod 32
   uint32_t mle[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) mle[k] = (2u << ((4 * lane + k) & 31)) - 1u;
   const uint32_t lmlt = lanemask_lt();
-  uint32_t maxidx = 0;
 
-  const uint64_t ntiles = (p.n + RW - 1) / RW;
-  const uint64_t tstride = (uint64_t)gridDim.x * nwarps;
-  uint64_t t = (uint64_t)blockIdx.x * nwarps + warp;
+  // ---- this warp's tiles [t_begin, t_end) and its element stream ----
+  const uint64_t G = (uint64_t)gridDim.x * nwarps, g = (uint64_t)blockIdx.x * nwarps + warp;
+  const uint64_t t_begin = p.ntiles * g / G, t_end = p.ntiles * (g + 1) / G;
+  if (t_begin < t_end) {
+    const uint64_t Ra = t_begin * RW, Rb = min(t_end * RW, p.n);
+    const int64_t S0 = __ldg(p.indptr + Ra), Send = __ldg(p.indptr + Rb), Etot = __ldg(p.indptr + p.n);
+    const bool valid = S0 >= 0 && S0 <= Send && Send <= Etot;
+    auto tile_rows = [&](uint64_t tt) -> uint32_t { return (uint32_t)min((uint64_t)RW, p.n - tt * RW); };
+    auto out_row = [&](uint64_t r) { return p.out + r * W; };
 
-  // Row tile tt: lane l < rows holds row r0+l's [s, e).
-  auto tile_rows = [&](uint64_t tt) -> uint32_t {
-    return tt < ntiles ? (uint32_t)min((uint64_t)RW, p.n - tt * RW) : 0u;
-  };
-  auto load_info = [&](uint64_t tt, int64_t& s_, int64_t& e_) {
-    s_ = 0; e_ = 0;
-    if ((uint32_t)lane < tile_rows(tt)) {
-      s_ = __ldg(p.indptr + tt * RW + lane);
-      e_ = __ldg(p.indptr + tt * RW + lane + 1);
-    }
-  };
-  // Streamed span of tile tt (warp-collective): [base, base + span) of `indices`, base
-  // 16-B aligned when VEC (lo = E0 - base head elements belong to earlier rows). span = 0
-  // for invalid tiles (bad indptr: rows stay zero) and for tiles of > 2^31 nonzeros
-  // (handled by a per-row loop).
-  auto span_of = [&](uint64_t tt, int64_t s_, int64_t e_, int64_t& base_, int& lo_) -> int {
-    const uint32_t rows_ = tile_rows(tt);
-    base_ = 0; lo_ = 0;
-    if (rows_ == 0) return 0;
-    const int64_t E0 = __shfl_sync(kFull, s_, 0), E1 = __shfl_sync(kFull, e_, rows_ - 1);
-    const bool ok = __all_sync(kFull, (uint32_t)lane >= rows_ || s_ <= e_) && E0 >= 0;
-    base_ = VEC ? (E0 & ~(int64_t)3) : E0;
-    lo_ = (int)(E0 - base_);
-    return (ok && E1 - base_ <= 0x7fff0000ll) ? (int)(E1 - base_) : 0;
-  };
-
-  int64_t cs, ce, ns, nE;            // current / next tile's per-lane row bounds
-  load_info(t, cs, ce);
-  load_info(t + tstride, ns, nE);
-
-  // ---- producer: cp.async of 256-element iterations into the ring, NS-1 ahead, running
-  // through the current tile and into the next one; group g holds stream position g.
-  // Bytes past span are zero-filled (src-size); the < 4 head elements before E0 are zeroed
-  // by the consumer. Out-of-range elements then land in the tile's virtual rows.
-  int ptile = 0, pwb = 0, pspan, plo;   // ptile: 0 = current tile, 1 = next tile
-  int64_t pbase;
-  const int32_t* psrc;                  // indices + pbase + pwb + 4*lane
-  uint32_t kp = 0, kc = 0;              // positions issued / consumed
-  uint32_t pslot = ring_a + 16 * lane;  // ring slot of position kp (this lane's bytes)
-  pspan = span_of(t, cs, ce, pbase, plo);
-  psrc = p.indices + pbase + 4 * lane;
-  auto issue = [&]() {
-    while (pwb >= pspan) {
-      if (ptile == 1 || t + tstride >= ntiles) return;   // wait for the consumer
-      ptile = 1; pwb = 0;
-      pspan = span_of(t + tstride, ns, nE, pbase, plo);
-      psrc = p.indices + pbase + 4 * lane;
-    }
-    if (VEC && pwb + kStage <= pspan) {   // whole stage in range
-#pragma unroll
-      for (int h = 0; h < kStage / 128; ++h) cp_async16(pslot + 512 * h, psrc + 128 * h, 16u);
-    } else
-#pragma unroll
-    for (int h = 0; h < kStage / 128; ++h) {
-      const int rem = pspan - (pwb + 128 * h + 4 * lane);   // elements left from this quad on
-      if (VEC) {
-        cp_async16(pslot + 512 * h, psrc + 128 * h, (uint32_t)min(max(rem, 0), 4) * 4u);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) cp_async4(pslot + 512 * h + 4 * k, psrc + 128 * h + k, k < rem ? 4u : 0u);
-      }
-    }
-    cp_async_commit();
-    ++kp;
-    pwb += kStage;
-    psrc += kStage;
-    pslot = (kp % NS == 0) ? pslot - (NS - 1) * kStageBytes : pslot + kStageBytes;
-  };
-  auto wait_pos = [&]() {   // wait until position kc has landed (kp - kc - 1 newer groups may stay pending)
-    if (kp - kc - 1 >= NS - 1) cp_async_wait<NS - 1>();
-    else cp_async_wait<0>();   // fewer newer groups (producer blocked at a tile end): drain
-  };
-  for (int i = 0; i < NS - 1; ++i) issue();
-  uint32_t cslot = ring_a + 16 * lane;  // ring slot of position kc
-
-  // Tile rows in shared memory: row 0 = virtual head row (elements before E0 in the first
-  // aligned quad), rows 1..nne = the tile's nonempty rows in order, row nne+1 = virtual
-  // tail row (zero-filled elements past E1). The virtual rows are never stored.
-  for (; t < ntiles; t += tstride) {
-    const uint64_t r0 = t * RW;
-    const uint32_t rows = tile_rows(t);
-    const bool has = (uint32_t)lane < rows;
-    const int64_t s = cs, e = ce;
-    const int64_t E0 = __shfl_sync(kFull, s, 0);
-    const int64_t E1 = __shfl_sync(kFull, e, rows - 1);
-    const bool ok = __all_sync(kFull, !has || s <= e) && E0 >= 0;
-    const uint32_t nw = rows * W;
-    uint32_t* dst = p.out + r0 * W;
-    const bool ne = ok && has && e > s;
-    const uint32_t NE = __ballot_sync(kFull, ne);
-    const uint32_t crow_l = __popc(NE & lmlt) + 1u;      // tile row of this lane's row
-    if (!ok) bad = 1;                // decreasing / negative indptr: rows stay zero, latched
-    for (uint32_t w = 4 * lane; w < (rows + 2) * W; w += 128) sts_v4(tile_a + 4 * w, 0, 0, 0, 0);   // padded to 16 B
-    if (has) sts_u32(crow_a + 4 * lane, ne ? crow_l : kFull);
-    const int64_t base = VEC ? (E0 & ~(int64_t)3) : E0;
-    __syncwarp();
-    if (ok && E1 - base > 0x7fff0000ll) {
-      // > 2^31 nonzeros in one tile: per-row loop with 64-bit offsets (correct, not fast)
-      for (uint32_t r = 0; r < rows; ++r) {
-        const int64_t rs = __shfl_sync(kFull, s, r), re = __shfl_sync(kFull, e, r);
-        const uint32_t ra = tile_a + __shfl_sync(kFull, crow_l, r) * Wb;
-        for (int64_t q = rs + lane; q < re; q += 32) {
-          const uint32_t x = (uint32_t)p.indices[q];
-          maxidx = max(maxidx, x);
-          uint32_t jj;
-          if (MODE == kPiSeeded) {
-            jj = pi_seeded(p.seed, (uint64_t)x, p.mn);
-          } else {
-            jj = __ldg(p.pi + min(x, d - 1));
-            maxj = max(maxj, jj);
-            jj = min(jj, N - 1);
+    if (!valid || Send - S0 > 0x7ff00000ll) {
+      // Invalid indptr (latched, rows zeroed) or more than 2^31 nonzeros in one warp's range:
+      // a row-at-a-time loop through ring row 0 (64-bit offsets; correct, not fast).
+      for (uint64_t r = Ra; r < Rb; ++r) {
+        const int64_t rs = __ldg(p.indptr + r), re = __ldg(p.indptr + r + 1);
+        if (!valid || rs > re || rs < 0 || re > Etot) {
+          bad = 1;
+        } else {
+          for (int64_t q = rs + lane; q < re; q += 32) {
+            const uint32_t x = (uint32_t)__ldg(p.indices + q);
+            maxidx = max(maxidx, x);
+            uint32_t jj;
+            if (MODE == kPiSeeded) {
+              jj = pi_seeded(p.seed, (uint64_t)x, p.mn);
+            } else {
+              jj = __ldg(p.pi + min(x, d - 1));
+              maxj = max(maxj, jj);
+              jj = min(jj, N - 1);
+            }
+            put_bit<XOR>(ring_a + ((jj >> 5) << 2), 1u << (jj & 31u));
           }
-          put_bit<XOR>(ra + ((jj >> 5) << 2), 1u << (jj & 31u));
         }
+        __syncwarp();
+        for (uint32_t w = lane; w < W; w += 32) {
+          __stcs(out_row(r) + w, lds_u32(ring_a + 4 * w));
+          sts_u32(ring_a + 4 * w, 0u);
+        }
+        __syncwarp();
       }
-    } else if (ok) {
-      const int span = (int)(E1 - base);
-      const int lo = (int)(E0 - base);
-      const int pe = ne ? (int)(e - base) : -1;   // end offset of this lane's (nonempty) row
-      for (int ws = 0; ws < span; ws += kStage) {
-        issue();
-        wait_pos();
-        const uint32_t stage = cslot;
-        ++kc;
-        cslot = (kc % NS == 0) ? cslot - (NS - 1) * kStageBytes : cslot + kStageBytes;
-        if ((ws & (kChunk - 1)) == 0) {
-          // row-boundary bitmap for [ws, ws + kChunk): bit q set iff a row (virtual head
-          // row included) ends at offset ws + q; B = tile row address at each word start
-          sts_v4(meta_a + 16 * lane, 0, 0, 0, 0);
-          __syncwarp();
-          const int q = pe - ws;
-          if (ne && q > 0 && q < kChunk) red_or_shared(meta_a + 8 * (uint32_t)(q >> 5), 1u << (q & 31));
-          if (ws == 0 && lo > 0 && lane == 0) {
-            red_or_shared(meta_a, 1u << lo);
-            // head elements (earlier rows' data, before E0) -> index 0 (virtual head row)
-            const uint4 h4 = lds_v4(stage);
-            sts_v4(stage, 0u, lo > 1 ? 0u : h4.y, lo > 2 ? 0u : h4.z, h4.w);
-          }
-          const uint32_t before = __popc(__ballot_sync(kFull, ne && pe <= ws)) + (lo <= ws ? 1u : 0u);
-          __syncwarp();
-          const uint4 pr = lds_v4(meta_a + 16 * lane);
-          const uint32_t c0 = __popc(pr.x), c = c0 + __popc(pr.z);
-          uint32_t incl = c;
+    } else {
+      const int64_t base = S0 & ~(int64_t)3;            // 16-B aligned stream start
+      const int head = (int)(S0 - base), end = (int)(Send - base), end4 = end & ~3;
+      const int nst = (end + S - 1) / S;
+      const int32_t* src0 = p.indices + base;
+
+      // raw indptr ends of tile tt (prefetched one tile ahead)
+      auto load_raw = [&](uint64_t tt) -> int64_t {
+        return (uint32_t)lane < tile_rows(tt) ? __ldg(p.indptr + tt * RW + lane + 1) : INT64_MIN;
+      };
+      // clamp into [prev_end, end], make monotone (inclusive max scan), flag any change
+      auto finish = [&](int64_t raw, uint32_t rows, int prev_end, uint32_t c) -> Tile {
+        Tile T;
+        const bool has = (uint32_t)lane < rows;
+        const int64_t v = raw - base;
+        int e = has ? (int)min(max(v, (int64_t)prev_end), (int64_t)end) : end;
+        int st = __shfl_up_sync(kFull, e, 1);
+        if (lane == 0) st = prev_end;
+        if (!__all_sync(kFull, !has || (e >= st && (int64_t)e == v))) {
+          // a decreasing or out-of-range indptr (latched): make the ends monotone
+          bad = 1;
+          if (!has) e = prev_end;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += y;
+            const int y = __shfl_up_sync(kFull, e, o);
+            if (lane >= o) e = max(e, y);
           }
-          const uint32_t b0 = tile_a + (before + incl - c) * Wb;
-          sts_v4(meta_a + 16 * lane, pr.x, b0, pr.z, b0 + c0 * Wb);
-          __syncwarp();
+          st = __shfl_up_sync(kFull, e, 1);
+          if (lane == 0) st = prev_end;
         }
-        // one 256-element half of the stage; FULL: the whole stage lies inside the span
-        auto half_step = [&](const int half, auto full_tag) {
-          constexpr bool FULL = decltype(full_tag)::value;
-          const int wb = ws + kIter * half;
-          const uint4 qa = lds_v4(stage + 1024 * half), qb = lds_v4(stage + 1024 * half + 512);
-          const uint32_t cur[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-          const uint32_t wq = (uint32_t)((wb & (kChunk - 1)) >> 5) + (uint32_t)(lane >> 3);
-          uint32_t addr[8], j[8];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint2 pb = lds_v2(meta_a + 8 * (wq + 4 * h));
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              addr[4 * h + k] = pb.y + (POW2 ? ((uint32_t)__popc(pb.x & mle[k]) << wsh)
-                                            : (uint32_t)__popc(pb.x & mle[k]) * Wb);
+        T.rows = rows;
+        const int last = __shfl_sync(kFull, e, rows - 1);   // (all lanes: a shuffle must not diverge)
+        T.e = has ? e : last;
+        T.ne = __ballot_sync(kFull, has && e > st);
+        T.tend = __shfl_sync(kFull, T.e, 31);
+        T.c = c;
+        return T;
+      };
+      auto empty_tile = [&](int at, uint32_t c) -> Tile {
+        Tile T;
+        T.e = at; T.ne = 0u; T.tend = at; T.rows = 0u; T.c = c;
+        return T;
+      };
+      // tile tt complete: write its rows (every output word exactly once), re-zero its ring rows
+      auto flush = [&](const Tile& T, uint64_t tt) {
+        const uint32_t nw = T.rows * W;
+        uint32_t* dst = out_row(tt * RW);
+        if (POW2 && p.out16 && LOGN <= 12) {
+          // lane r: ring address of the tile's row r (an empty row reads the warp's zero row);
+          // 128 words per iteration, no per-word predicate for a whole tile
+          const uint32_t myra = ((T.ne >> lane) & 1u) ? ring_a + ((T.c + __popc(T.ne & lmlt)) & (RR - 1u)) * Wb : zero_a;
+          constexpr uint32_t lw = LOGN > 5 ? LOGN - 5 : 0;               // log2(W)
+          constexpr uint32_t rpi = lw <= 7 ? (128u >> lw) : 1u;           // rows per iteration
+          const uint32_t sub = (4u * lane) >> lw, wo = 4u * ((4u * lane) & ((1u << lw) - 1u));
+          uint4* d4 = reinterpret_cast<uint4*>(dst) + lane;
+          if (nw == RW * W && (RW * W) % 128 == 0) {
+#pragma unroll 4
+            for (uint32_t i = 0; i < RW * W / 128; ++i) {
+              const uint32_t a = __shfl_sync(kFull, myra, (i * rpi + sub) & 31u) + wo;
+              const uint4 v = lds_v4(a);
+              sts_v4(a, 0u, 0u, 0u, 0u);
+              __stcs(d4 + 32 * i, v);
+            }
+          } else {
+            for (uint32_t i = 0; 128 * i < nw; ++i) {          // warp-uniform trip count
+              const uint32_t a = __shfl_sync(kFull, myra, (i * rpi + sub) & 31u) + wo;
+              if (4 * lane + 128 * i < nw) {
+                const uint4 v = lds_v4(a);
+                sts_v4(a, 0u, 0u, 0u, 0u);
+                __stcs(d4 + 32 * i, v);
+              }
+            }
           }
+        } else if (p.out16) {
+          for (uint32_t w = 4 * lane; w < nw; w += 128) {
+            const uint32_t r = w / W;
+            const uint32_t wi = w - r * W;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if ((T.ne >> r) & 1u) {
+              const uint32_t idx = (T.c + __popc(T.ne & ((1u << r) - 1u))) & (RR - 1u);
+              const uint32_t a = ring_a + idx * Wb + 4 * wi;
+              v = lds_v4(a);
+              sts_v4(a, 0u, 0u, 0u, 0u);
+            }
+            __stcs(reinterpret_cast<uint4*>(dst + w), v);
+          }
+        } else {
+          for (uint32_t w = lane; w < nw; w += 32) {
+            const uint32_t r = w / W;
+            const uint32_t wi = w - r * W;
+            uint32_t v = 0u;
+            if ((T.ne >> r) & 1u) {
+              const uint32_t idx = (T.c + __popc(T.ne & ((1u << r) - 1u))) & (RR - 1u);
+              const uint32_t a = ring_a + idx * Wb + 4 * wi;
+              v = lds_u32(a);
+              sts_u32(a, 0u);
+            }
+            __stcs(dst + w, v);
+          }
+        }
+        __syncwarp();
+      };
+
+      uint64_t t = t_begin;
+      Tile T0 = finish(load_raw(t), tile_rows(t), head, 0u);
+      Tile T1 = t + 1 < t_end ? finish(load_raw(t + 1), tile_rows(t + 1), T0.tend, T0.c + __popc(T0.ne))
+                              : empty_tile(T0.tend, T0.c + __popc(T0.ne));
+      int64_t raw2 = t + 2 < t_end ? load_raw(t + 2) : 0;
+      int wend = T1.tend;
+      auto advance = [&]() {
+        T0 = T1;
+        ++t;
+        const uint32_t c = T0.c + __popc(T0.ne);
+        if (t + 1 < t_end) {
+          T1 = finish(raw2, tile_rows(t + 1), T0.tend, c);
+          raw2 = t + 2 < t_end ? load_raw(t + 2) : 0;
+        } else {
+          T1 = empty_tile(T0.tend, c);
+        }
+        wend = T1.tend;
+      };
+
+      // stage k -> ring slot k % kNS; bulk copy of its 16-B aligned part (lane 0)
+      auto issue = [&](int k) {
+        if (k >= nst || lane != 0) return;
+        const int s = k * S;
+        const int nb = max(0, min(s + S, end4) - s) * 4;
+        const uint32_t slot = stage_a + (uint32_t)(k % kNS) * SB, mb = mbar_a + 8u * (uint32_t)(k % kNS);
+        fence_proxy_async();
+        if (nb > 0) {
+          mbar_expect_tx(mb, (uint32_t)nb);
+          bulk_load(slot, src0 + s, (uint32_t)nb, mb);
+        } else {
+          mbar_arrive(mb);
+        }
+      };
+
+      // row-boundary bitmap of [b0, b0 + kChunk) for the window's rows
+      auto build_bitmap = [&](int b0) {
+        sts_v4(meta_a + 16 * lane, 0u, 0u, 0u, 0u);
+        __syncwarp();
+        int q = T0.e - b0;
+        if (((T0.ne >> lane) & 1u) && q > 0 && q < kChunk) put_bit<false>(meta_a + 8 * (uint32_t)(q >> 5), 1u << (q & 31));
+        q = T1.e - b0;
+        if (((T1.ne >> lane) & 1u) && q > 0 && q < kChunk) put_bit<false>(meta_a + 8 * (uint32_t)(q >> 5), 1u << (q & 31));
+        const uint32_t before = T0.c + __popc(T0.ne & __ballot_sync(kFull, T0.e <= b0)) +
+                                __popc(T1.ne & __ballot_sync(kFull, T1.e <= b0));
+        __syncwarp();
+        const uint4 pr = lds_v4(meta_a + 16 * lane);
+        const uint32_t c0 = __popc(pr.x), c = c0 + __popc(pr.z);
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const uint32_t b = before + incl - c;
+        const uint32_t B0 = POW2 ? ((b & (RR - 1u)) << wsh) : (b & (RR - 1u));
+        const uint32_t B1 = POW2 ? (((b + c0) & (RR - 1u)) << wsh) : ((b + c0) & (RR - 1u));
+        sts_v4(meta_a + 16 * lane, pr.x, B0, pr.z, B1);
+        __syncwarp();
+      };
+
+      // one 256-element half of a stage: off = stage-relative offset of the half, wb = its
+      // bitmap-relative offset; PRED: only elements at stage offsets [lo, hi) take effect
+      auto half_step = [&](const uint32_t slot, const int off, const int wb, const int lo, const int hi,
+                           auto pred_tag) {
+        constexpr bool PRED = decltype(pred_tag)::value;
+        const uint4 qa = lds_v4(slot + 4 * off + 16 * lane), qb = lds_v4(slot + 4 * off + 512 + 16 * lane);
+        const uint32_t cur[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+        bool ok[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int pos = off + 128 * (u >> 2) + 4 * lane + (u & 3);
+          ok[u] = !PRED || (pos >= lo && pos < hi);
+        }
+        const uint32_t wq = (uint32_t)(wb >> 5) + (uint32_t)(lane >> 3);
+        uint32_t rowp[8];   // ring row part: byte offset (POW2) or ring index
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint2 pb = lds_v2(meta_a + 8 * (wq + 4 * h));
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            rowp[4 * h + k] = POW2 ? mad_u32((uint32_t)__popc(pb.x & mle[k]), 1u << wsh, pb.y)   // FMA pipe, off the ALU
+                                   : pb.y + (uint32_t)__popc(pb.x & mle[k]);
+        }
+        if (PRED) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) maxidx = max(maxidx, ok[u] ? cur[u] : 0u);
+        } else {
           maxidx = __vimax3_u32(maxidx, __vimax3_u32(cur[0], cur[1], cur[2]),
                                 __vimax3_u32(__vimax3_u32(cur[3], cur[4], cur[5]), cur[6], cur[7]));
-          uint32_t bit[8];   // 1 << (j & 31)
-          if (MODE == kPiSeeded && POW2) {
-            // word offset from j & ~31 (LEA.HI); x & 31 = j & 31 since N >= 32
+        }
+        uint32_t j[8], bit[8];
+        if (MODE == kPiSeeded && POW2) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const uint32_t x = pi_pow2_raw(seed1, cur[u]);
-              j[u] = x & wmask;                         // = (j >> 5) << 5
-              bit[u] = bit_of(x);
-            }
-          } else if (MODE == kPiSeeded) {
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t x = pi_pow2_raw(seed1, cur[u]);
+            j[u] = x & wmask;                         // = (j >> 5) << 5
+            bit[u] = bit_of(x);                       // x & 31 = j & 31 since N >= 32
+          }
+        } else {
+          if (MODE == kPiSeeded) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) j[u] = pi_seeded(p.seed, (uint64_t)cur[u], p.mn);
           } else if (MODE == kPiSmem16) {
@@ -486,9 +611,9 @@ build_kernel(const BuildParams p) {
           } else if (MODE == kPiGlobal) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-              const uint32_t g = __ldg(p.pi + min(cur[u], d - 1));
-              maxj = max(maxj, g);
-              j[u] = min(g, N - 1);
+              const uint32_t gv = __ldg(p.pi + min(cur[u], d - 1));
+              maxj = max(maxj, ok[u] ? gv : 0u);
+              j[u] = POW2 ? gv : min(gv, N - 1);    // POW2: the ring mask keeps any j in bounds
             }
           } else {
             // probe all 8, then issue all misses' loads (independent, predicated), then fill
@@ -506,72 +631,95 @@ build_kernel(const BuildParams p) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               if (miss[u]) {
-                maxj = max(maxj, j[u]);
+                maxj = max(maxj, ok[u] ? j[u] : 0u);
                 j[u] = min(j[u], N - 1);
                 const uint32_t ent = ((x[u] >> kSlotBits) << vb) | j[u];
                 if (MODE == kPiCache16) sts_u16(pi_a + 2 * slot_[u], ent); else sts_u32(pi_a + 4 * slot_[u], ent);
               }
             }
           }
-          if (!(MODE == kPiSeeded && POW2)) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) { bit[u] = bit_of(j[u]); j[u] &= ~31u; }
-          }
-          if (FULL) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) put_bit<XOR>(addr[u] + (j[u] >> 3), bit[u]);
-          } else {   // tile tail: skip the zero-filled elements (they would all hit one word)
-            const int rem = span - wb;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (128 * (u >> 2) + 4 * lane + (u & 3) < rem) put_bit<XOR>(addr[u] + (j[u] >> 3), bit[u]);
-          }
-        };
-        if (ws + kStage <= span) {
-#pragma unroll
-          for (int h = 0; h < kStage / kIter; ++h) half_step(h, std::true_type{});
-        } else {
-#pragma unroll 1
-          for (int h = 0; h < kStage / kIter; ++h)
-            if (ws + kIter * h < span) half_step(h, std::false_type{});
+          for (int u = 0; u < 8; ++u) { bit[u] = bit_of(j[u]); j[u] &= ~31u; }
         }
+        uint32_t addr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          addr[u] = POW2 ? (((rowp[u] + (j[u] >> 3)) & (ringB - 1u)) | ring_a)
+                         : ring_a + (rowp[u] & (RR - 1u)) * Wb + (j[u] >> 3);
+        if (PRED) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) put_bit_if<XOR>(ok[u], addr[u], bit[u]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) put_bit<XOR>(addr[u], bit[u]);
+        }
+      };
+
+      for (int i = 0; i < kNS - 1; ++i) issue(i);
+      int done = head;            // stream offsets < done are processed
+      int b0 = 0;
+      bool bm_ok = false;
+      int fast_lim = 0;           // a stage [s, s + S) with done == s and s + S <= fast_lim runs unpredicated
+      const int tail_k = end4 < end ? end4 / S : -1;
+      // flush every complete tile; after an advance, rebuild the bitmap for the next stage
+      auto retire = [&](int next_s) {
+        if (t < t_end && T0.tend <= done) {
+          do {
+            flush(T0, t);
+            advance();
+          } while (t < t_end && T0.tend <= done);
+          bm_ok = false;
+          if (t < t_end && done == next_s && next_s < end) { build_bitmap(next_s); b0 = next_s; bm_ok = true; }
+        }
+        fast_lim = bm_ok ? min(min(wend, end), b0 + kChunk) : 0;
+      };
+      for (int k = 0; k < nst; ++k) {
+        issue(k + kNS - 1);
+        const uint32_t slot = stage_a + (uint32_t)(k % kNS) * SB;
+        mbar_wait(mbar_a + 8u * (uint32_t)(k % kNS), (uint32_t)(k / kNS) & 1u);
+        const int s = k * S;
+        if (k == tail_k) {   // < 4 trailing elements past the bulk copy: plain loads
+          if (lane < end - end4) sts_u32(slot + 4u * (uint32_t)(end4 - s + lane), (uint32_t)__ldg(src0 + end4 + lane));
+          __syncwarp();
+        }
+        bool full = done == s && s + S <= fast_lim;
+        if (!full) {
+          const int se = min(s + S, end);
+          while (done < se) {
+            if (t >= t_end) { done = se; break; }          // only after a latched bad indptr
+            const int lim = min(se, wend);
+            if (!bm_ok || s + S > b0 + kChunk) { build_bitmap(s); b0 = s; bm_ok = true; }
+            if (done == s && lim == s + S) { full = true; break; }
+#pragma unroll 1
+            for (int h = 0; h < S / 256; ++h)
+              if (256 * h + 256 > done - s && 256 * h < lim - s)
+                half_step(slot, 256 * h, s - b0 + 256 * h, done - s, lim - s, std::true_type{});
+            done = lim;
+            __syncwarp();
+            if (done < se) retire(s);
+          }
+        }
+        if (full) {
+#pragma unroll
+          for (int h = 0; h < S / 256; ++h) half_step(slot, 256 * h, s - b0 + 256 * h, 0, S, std::false_type{});
+          done = s + S;
+        }
+        __syncwarp();
+        retire(s + S);
       }
-    }
-    __syncwarp();
-    // write the tile: rows in order, empty rows as zeros; every output word exactly once
-    const uint32_t all = rows == 32 ? kFull : ((1u << rows) - 1u);
-    if (NE == all && (W & 3u) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15u) == 0) {
-      for (uint32_t w = 4 * lane; w < nw; w += 128) {
-        const uint4 v = lds_v4(tile_a + Wb + 4 * w);   // tile rows 1..rows
-        __stcs(reinterpret_cast<uint4*>(dst + w), v);
+      while (t < t_end) {   // tiles whose rows are all empty after the last element
+        flush(T0, t);
+        advance();
       }
-    } else {
-      for (uint32_t w = lane; w < nw; w += 32) {
-        const uint32_t r = w / W;
-        const uint32_t cr = lds_u32(crow_a + 4 * r);
-        __stcs(dst + w, cr == kFull ? 0u : lds_u32(tile_a + 4 * (cr * W + (w - r * W))));
-      }
-    }
-    __syncwarp();
-    // advance: next becomes current; the producer follows (it is on the next tile, or done
-    // with this one and must restart on the new current tile)
-    cs = ns; ce = nE;
-    load_info(t + 2 * tstride, ns, nE);
-    if (ptile == 1) {
-      ptile = 0;
-    } else {
-      pwb = 0;
-      pspan = span_of(t + tstride, cs, ce, pbase, plo);
-      psrc = p.indices + pbase + 4 * lane;
     }
   }
-  cp_async_wait<0>();
   if (maxidx >= d || maxj >= N) bad = 1;
   if (__any_sync(kFull, bad != 0) && lane == 0) latch(p.status, kStatusIndex);
 }
 
-// Fallback for very wide sketches (one row's W words do not fit a warp's share of
-// shared memory): rows zeroed by cudaMemsetAsync, then global atomicOr (atomicXor: BCS).
+// Fallback for very wide sketches (one row's W words do not fit the per-warp ring) and for
+// index arrays that are not 16-B aligned (the bulk copies need it): rows zeroed by
+// cudaMemsetAsync, then global atomicOr (atomicXor: BCS).
 __global__ void build_wide_kernel(const uint32_t* __restrict__ pi, uint64_t seed, uint64_t d, ModN mn,
                                   bool seeded, bool parity, const int64_t* __restrict__ indptr,
                                   const int32_t* __restrict__ indices, uint64_t n,
@@ -605,97 +753,96 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
                          const int64_t* indptr, const int32_t* indices, uint64_t n,
                          uint32_t* out, cudaStream_t s, bool parity) {
   if (n == 0) return cudaSuccess;
-  const uint32_t W = (N + 31) / 32;
+  const uint64_t W64 = ((uint64_t)N + 31) / 32;
+  const uint32_t W = (uint32_t)W64;
   const ModN mn = make_modn(N);
   unsigned int* st = status_ptr();
   const int sms = num_sms();
-  int dev = 0, smem_optin = 0;
+  int dev = 0, smem_optin = 0, smem_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t optin = (size_t)smem_optin;
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+
+  auto wide = [&]() -> cudaError_t {
+    cudaError_t e = cudaMemsetAsync(out, 0, n * W64 * 4, s);
+    if (e != cudaSuccess) return e;
+    build_wide_kernel<<<sms * 8, 256, 0, s>>>(pi, seed, d, mn, pi == nullptr, parity, indptr, indices, n, out, W, st);
+    count_launch();
+    return cudaGetLastError();
+  };
+  if ((reinterpret_cast<uintptr_t>(indices) & 15u) != 0 || W64 > 4096) return wide();
 
   const uint32_t vb = bits_for(N - 1);
   const uint32_t dbits = bits_for(d - 1);
   const bool c16 = N <= 65536 && (dbits > 16 ? dbits - 16 : 0) + vb <= 16;
   const bool c32 = (dbits > 15 ? dbits - 15 : 0) + vb <= 32;
-  const size_t smem16_bytes = ((d * 2 + 15) / 16) * 16;
+  const uint64_t smem16_bytes = ((d * 2 + 15) / 16) * 16;
   int mode = kPiGlobal;
   if (pi == nullptr) mode = kPiSeeded;
   else if (N <= 65536 && smem16_bytes <= 100 * 1024) mode = kPiSmem16;
   else if (c16) mode = kPiCache16;
   else if (c32) mode = kPiCache32;
-  // Experiment knob (ncu A/B of the pi source): BINSKETCH_BUILD_MODE=global|cache|smem16.
+  // Experiment knob (A/B of the pi source): BINSKETCH_BUILD_MODE=global|cache|cache32|smem16.
   if (const char* f = pi != nullptr ? std::getenv("BINSKETCH_BUILD_MODE") : nullptr) {
     if (!std::strcmp(f, "global")) mode = kPiGlobal;
     if (!std::strcmp(f, "cache")) mode = c16 ? kPiCache16 : (c32 ? kPiCache32 : mode);
     if (!std::strcmp(f, "cache32") && c32) mode = kPiCache32;
-    if (!std::strcmp(f, "smem16") && N <= 65536 && smem16_bytes + 64 * 1024 <= optin) mode = kPiSmem16;
+    if (!std::strcmp(f, "smem16") && N <= 65536 && smem16_bytes + 64 * 1024 <= (uint64_t)smem_optin) mode = kPiSmem16;
   }
-  // Shared memory per warp: meta + ring (kStages KB) + an RW x W tile, RW <= 32 rows.
-  auto rows_fit = [&](size_t per_warp, int stages, int stage_bytes) -> uint32_t {
-    const size_t fixed = kMetaBytes + (size_t)stages * stage_bytes + 16 + 8 * (size_t)W;   // + 2 virtual rows
-    return per_warp > fixed ? (uint32_t)std::min<size_t>(32, (per_warp - fixed) / (4 * (size_t)W)) : 0u;
-  };
-  bool smem_pi = mode == kPiSmem16 || mode == kPiCache16 || mode == kPiCache32;
-  uint32_t pi_bytes = mode == kPiSmem16 ? (uint32_t)smem16_bytes : (smem_pi ? 128u * 1024u : 0u);
-  int threads = smem_pi ? BuildCfg<kPiCache16>::kThreads : BuildCfg<kPiSeeded>::kThreads;
-  int stages = smem_pi ? BuildCfg<kPiCache16>::kStages : BuildCfg<kPiSeeded>::kStages;
-  int stage_bytes = smem_pi ? BuildCfg<kPiCache16>::kStageBytes : BuildCfg<kPiSeeded>::kStageBytes;
-  int bps = smem_pi ? BuildCfg<kPiCache16>::kBlocks : BuildCfg<kPiSeeded>::kBlocks;
-  size_t budget = optin / bps;
-  uint32_t RW = rows_fit(budget > pi_bytes ? (budget - pi_bytes) / (threads / 32) : 0, stages, stage_bytes);
-  if (RW == 0 && smem_pi) {       // wide sketches: fall back to the global-gather variant
-    mode = kPiGlobal; smem_pi = false; pi_bytes = 0;
-    threads = BuildCfg<kPiGlobal>::kThreads; stages = BuildCfg<kPiGlobal>::kStages;
-    stage_bytes = BuildCfg<kPiGlobal>::kStageBytes;
-    bps = BuildCfg<kPiGlobal>::kBlocks;
-    budget = optin / bps;
-    RW = rows_fit(budget / (threads / 32), stages, stage_bytes);
-  }
-  if (RW == 0) {
-    cudaError_t e = cudaMemsetAsync(out, 0, n * (size_t)W * 4, s);
-    if (e != cudaSuccess) return e;
-    build_wide_kernel<<<sms * 8, 256, 0, s>>>(pi, seed, d, mn, pi == nullptr, parity, indptr, indices, n, out, W, st);
-    count_launch();
-    return cudaGetLastError();
-  }
-  BuildParams bp;
-  bp.pi = pi; bp.seed = seed; bp.mn = mn; bp.indptr = indptr; bp.indices = indices; bp.n = n; bp.out = out;
-  bp.d = (uint32_t)d; bp.W = W; bp.RW = RW; bp.vb = vb; bp.status = st;
-  bp.pi_bytes = smem_pi ? pi_bytes : 0u;
-  bp.warp_bytes = kMetaBytes + (uint32_t)(stages * stage_bytes) + (uint32_t)((((size_t)(RW + 2) * W * 4) + 15) / 16 * 16);
-  const size_t smem = bp.pi_bytes + (size_t)bp.warp_bytes * (threads / 32);
-  const uint64_t ntiles = (n + RW - 1) / RW;
-  const uint64_t want = (ntiles + (threads / 32) - 1) / (threads / 32);
-  const int fit = (int)std::max<size_t>(1, std::min<size_t>((size_t)bps, optin / std::max<size_t>(smem, 1)));
-  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms * fit));
   // compiled-in sketch widths: the configs' N = 1024 (W = 32) and 4096 (W = 128); the BCS
   // parity variant is instantiated for the generic width only
   const int logn = parity ? 0 : (N == 1024 ? 10 : (N == 4096 ? 12 : 0));
-  const bool vec = (reinterpret_cast<uintptr_t>(indices) & 15u) == 0;
+  const uint64_t Wb = 4 * W64;
+
+  // Shared memory per block: [pi] [align slack] [rings: nwarps x RR x Wb] [aux: nwarps x (stages + bitmap + mbar)]
+  auto plan = [&](int m, uint32_t& RR, uint32_t& pi_bytes, uint32_t& align, uint32_t& aux, int& threads, int& bps,
+                  size_t& smem) -> bool {
+    const bool smem_pi = m == kPiSmem16 || m == kPiCache16 || m == kPiCache32;
+    threads = smem_pi ? BuildCfg<kPiCache16>::kThreads : BuildCfg<kPiSeeded>::kThreads;
+    bps = smem_pi ? BuildCfg<kPiCache16>::kBlocks : BuildCfg<kPiSeeded>::kBlocks;
+    const uint32_t stage_bytes = smem_pi ? BuildCfg<kPiCache16>::kStageBytes : BuildCfg<kPiSeeded>::kStageBytes;
+    pi_bytes = m == kPiSmem16 ? (uint32_t)smem16_bytes : (smem_pi ? 128u * 1024u : 0u);
+    aux = kNS * stage_bytes + kAuxFixed + (uint32_t)((Wb + 15) / 16 * 16);   // 16-B aligned per-warp regions
+    const size_t budget = std::min<size_t>((size_t)smem_optin, (size_t)smem_sm / bps - 1024);
+    const int nw = threads / 32;
+    for (uint32_t rr = BSK_BUILD_RRMAX; rr >= 4; rr >>= 1) {
+      const uint64_t ringB = rr * Wb;
+      align = logn ? (uint32_t)ringB : 16u;
+      smem = pi_bytes + (size_t)(align - 16) + (size_t)nw * (ringB + aux);
+      if (ringB <= (1u << 20) && smem <= budget) { RR = rr; return true; }
+    }
+    return false;
+  };
+  uint32_t RR = 0, pi_bytes = 0, align = 16, aux = 0;
+  int threads = 0, bps = 0;
+  size_t smem = 0;
+  if (!plan(mode, RR, pi_bytes, align, aux, threads, bps, smem)) {
+    if (mode == kPiSeeded || !plan(kPiGlobal, RR, pi_bytes, align, aux, threads, bps, smem)) return wide();
+    mode = kPiGlobal;
+  }
+  BuildParams bp;
+  bp.pi = pi; bp.seed = seed; bp.mn = mn; bp.indptr = indptr; bp.indices = indices; bp.n = n; bp.out = out;
+  bp.d = (uint32_t)d; bp.W = W; bp.RR = RR; bp.vb = vb; bp.status = st;
+  bp.pi_bytes = pi_bytes; bp.ring_align = align; bp.aux_bytes = aux;
+  bp.ntiles = (n + RR / 2 - 1) / (RR / 2);
+  bp.out16 = ((W & 3u) == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) ? 1u : 0u;
+  const int nw = threads / 32;
+  const uint64_t want = (bp.ntiles + nw - 1) / nw;
+  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms * bps));
   cudaError_t e = cudaSuccess;
-#define BSK_LAUNCH_BUILD4(M, LN, V, X)                                                                           \
+#define BSK_LAUNCH_BUILD3(M, LN, X)                                                                              \
   do {                                                                                                           \
-    e = cudaFuncSetAttribute(build_kernel<M, LN, V, X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    e = cudaFuncSetAttribute(build_kernel<M, LN, X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
     if (e != cudaSuccess) return e;                                                                              \
-    build_kernel<M, LN, V, X><<<(unsigned)blocks, threads, smem, s>>>(bp);                                       \
+    build_kernel<M, LN, X><<<(unsigned)blocks, threads, smem, s>>>(bp);                                          \
     count_launch();                                                                                              \
   } while (0)
-#define BSK_LAUNCH_BUILD3(M, LN, V)                       \
-  do {                                                    \
-    if (LN == 0 && parity) BSK_LAUNCH_BUILD4(M, 0, V, true); \
-    else BSK_LAUNCH_BUILD4(M, LN, V, false);              \
-  } while (0)
-#define BSK_LAUNCH_BUILD2(M, LN)                 \
-  do {                                           \
-    if (vec) BSK_LAUNCH_BUILD3(M, LN, true);     \
-    else BSK_LAUNCH_BUILD3(M, LN, false);        \
-  } while (0)
-#define BSK_LAUNCH_BUILD(M)                                  \
-  do {                                                       \
-    if (logn == 10) BSK_LAUNCH_BUILD2(M, 10);                \
-    else if (logn == 12) BSK_LAUNCH_BUILD2(M, 12);           \
-    else BSK_LAUNCH_BUILD2(M, 0);                            \
+#define BSK_LAUNCH_BUILD(M)                                   \
+  do {                                                        \
+    if (logn == 10) BSK_LAUNCH_BUILD3(M, 10, false);          \
+    else if (logn == 12) BSK_LAUNCH_BUILD3(M, 12, false);     \
+    else if (parity) BSK_LAUNCH_BUILD3(M, 0, true);           \
+    else BSK_LAUNCH_BUILD3(M, 0, false);                      \
   } while (0)
   switch (mode) {
     case kPiSeeded: BSK_LAUNCH_BUILD(kPiSeeded); break;
@@ -705,9 +852,7 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
     default: BSK_LAUNCH_BUILD(kPiGlobal); break;
   }
 #undef BSK_LAUNCH_BUILD
-#undef BSK_LAUNCH_BUILD2
 #undef BSK_LAUNCH_BUILD3
-#undef BSK_LAUNCH_BUILD4
   return cudaGetLastError();
 }
 
