@@ -196,6 +196,14 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void sts_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w));
 }
+__device__ __forceinline__ void sts_u16_if(bool pred, uint32_t a, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u16 [%0], %1;\n\t}"
+               ::"r"(a), "h"((unsigned short)v), "r"((uint32_t)pred));
+}
+__device__ __forceinline__ void sts_u32_if(bool pred, uint32_t a, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"
+               ::"r"(a), "r"(v), "r"((uint32_t)pred));
+}
 // A sketch bit: OR (BinSketch) or XOR (BCS parity buckets),
 // optionally predicated (no branch: the partial-stage path stays convergent).
 template <bool XOR>
@@ -527,8 +535,9 @@ build_kernel(const BuildParams p) {
         if (k >= nst || lane != 0) return;
         const int s = k * S;
         const int nb = max(0, min(s + S, end4) - s) * 4;
+        // (no proxy fence: the slot's previous contents were read by LDS whose results the
+        // warp consumed before this point, and the mbarrier wait orders the copy's writes)
         const uint32_t slot = stage_a + (uint32_t)(k % kNS) * SB, mb = mbar_a + 8u * (uint32_t)(k % kNS);
-        fence_proxy_async();
         if (nb > 0) {
           mbar_expect_tx(mb, (uint32_t)nb);
           bulk_load(slot, src0 + s, (uint32_t)nb, mb);
@@ -628,14 +637,15 @@ build_kernel(const BuildParams p) {
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) j[u] = ldg_if(p.pi + x[u], miss[u], c[u] & vmask);
+            // fill every missed slot (branch-free: predicated stores). Measured: a probabilistic
+            // fill (1/4 of misses, hashed) keeps the simulated hit rate but was slower (1.75 vs 1.68 ms).
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-              if (miss[u]) {
-                maxj = max(maxj, ok[u] ? j[u] : 0u);
-                j[u] = min(j[u], N - 1);
-                const uint32_t ent = ((x[u] >> kSlotBits) << vb) | j[u];
-                if (MODE == kPiCache16) sts_u16(pi_a + 2 * slot_[u], ent); else sts_u32(pi_a + 4 * slot_[u], ent);
-              }
+              maxj = max(maxj, (ok[u] && miss[u]) ? j[u] : 0u);
+              if (!POW2) j[u] = min(j[u], N - 1);      // POW2: the ring mask keeps any j in bounds
+              const uint32_t ent = ((x[u] >> kSlotBits) << vb) | (j[u] & vmask);
+              if (MODE == kPiCache16) sts_u16_if(miss[u], pi_a + 2 * slot_[u], ent);
+              else sts_u32_if(miss[u], pi_a + 4 * slot_[u], ent);
             }
           }
 #pragma unroll
