@@ -77,6 +77,12 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                : "memory");
 }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+// one lane of a converged warp (the same lane in every call)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t r;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(r));
+  return r != 0u;
+}
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // K-major operand tile of 128-byte rows, 128B-swizzled (as TMA writes it): 8-row
@@ -98,6 +104,27 @@ __device__ __forceinline__ void mma_u8(uint32_t d_tmem, uint64_t a, uint64_t b, 
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T (A from tensor memory: lane = row, 4 K-bytes per column).
+__device__ __forceinline__ void mma_u8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum));
+}
+// 32 lanes x 32 consecutive columns <- 32 registers per thread, then wait for the stores.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};"
+      ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+        "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+        "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -210,6 +237,31 @@ __device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[32]) {
 
 }  // namespace tc
 
+#ifdef BSK_TOPK_PROF
+#define BSK_T0(v) const long long v = clock64()
+#define BSK_TADD(slot, t0) atomicAdd(&g_tkstats[slot], (unsigned long long)(clock64() - (t0)))
+#else
+#define BSK_T0(v)
+#define BSK_TADD(slot, t0)
+#endif
+#ifdef BSK_TOPK_STATS
+// dev instrumentation (never in the product build): warp-tiles, all-rows-skippable warp-tiles,
+// passing chunks, survivors, direct-path warp-tiles, candidates; BSK_TOPK_PROF adds clock64
+// cycle sums: [6] epilogue waits tfull, [7] filter, [8] scoring, [9] tile setup (metadata wait +
+// bound), [10] MMA waits tempty, [11] MMA waits full, [12] producer waits empty, [13] epilogue
+// item loop, [14] MMA role total
+__device__ unsigned long long g_tkstats[16];
+}  // namespace bsk
+extern "C" int bsk_topk_stats(unsigned long long* host8) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host8, bsk::g_tkstats, 128);
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(bsk::g_tkstats, z, 128);
+  return 0;
+}
+namespace bsk {
+#endif
+
 // ------------------------------------------------------------- expansion ---
 // out[r][b] = bit b of row r (LSB-first words), b < 32W; zero for 32W <= b < Kp.
 __global__ void expand_kernel(const uint32_t* __restrict__ sk, uint64_t n, uint32_t W, uint32_t Kp,
@@ -289,7 +341,10 @@ __global__ void pb_scatter_kernel(const int32_t* __restrict__ pb, uint64_t n, ui
 constexpr int kTcM = 128, kTcN = 256;
 constexpr int kTcAcc = 512 / kTcN;   // TMEM accumulators (512 columns)
 constexpr uint32_t kTcSmemMax = 227 * 1024;
-enum TcMode { kTcAndPopc = 0, kTcEstimate = 1, kTcTopk = 2, kTcJoin = 3 };
+enum TcMode { kTcAndPopc = 0, kTcEstimate = 1, kTcTopk = 2, kTcJoin = 3, kTcTopkT = 4 };
+// kTcTopkT: the fused top-k with the query tile A resident in TMEM (columns [0, Kp/4), Kp <= 1024)
+// for the whole work item and 128-wide db tiles (two 128-column accumulators after it): only B
+// streams through shared memory, so each MMA's operand traffic drops from A + B to B.
 constexpr uint32_t kTcMaxThr = 16;   // thresholds per join launch
 
 // Roles per mode: warp 0 TMA producer, warp 1 MMA issuer, then kEpi epilogue warps (kEpi/4 per
@@ -297,7 +352,7 @@ constexpr uint32_t kTcMaxThr = 16;   // thresholds per join launch
 // recipe per pair, latency-bound) runs 16 warps reading 8-column chunks; the others 4 warps.
 template <int MODE>
 struct TcRoles {
-  static constexpr int kEpi = (MODE == kTcEstimate || MODE == kTcJoin) ? 16 : 4;   // TMEM-reading warps
+  static constexpr int kEpi = (MODE == kTcEstimate || MODE == kTcJoin) ? 16 : (MODE == kTcTopkT ? 8 : 4);   // TMEM-reading warps
   static constexpr uint32_t kThreads = 64 + 32 * kEpi;
   static constexpr int kCW = (MODE == kTcEstimate || MODE == kTcJoin) ? 8 : 32;   // columns per TMEM load
 };
@@ -347,6 +402,8 @@ struct TcParams {
   uint32_t l_topk_smem;   // kTcTopk: table staged after the heaps (bytes, 0 = global)
   double lc;              // log1p(-1/N): closed-form inverse of the table for the tile bound
   const int32_t* qperm;   // kTcTopk: A row (queries sorted by |a_s| descending) -> original query index
+  const uint8_t* a8;      // kTcTopkT: the widened query rows [na][kp] (loaded into TMEM per item)
+  uint32_t kp;            // kTcTopkT: bytes per widened row (Kp <= 1024)
   unsigned long long* item_ctr;   // dynamic work queue: next item (zeroed before the launch)
   uint32_t* bits;         // kTcJoin: match bitmaps [nthr][na][wpr] (zeroed before the launch)
   uint64_t wpr;           // kTcJoin: words per bitmap row = ceil(nb / 32)
@@ -382,6 +439,12 @@ __global__ void __launch_bounds__(TcRoles<MODE>::kThreads, 1)
 tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcParams p) {
   using G = TcGeom<KC, CG>;
   constexpr int kEpi = TcRoles<MODE>::kEpi;
+  constexpr bool TOPK = MODE == kTcTopk || MODE == kTcTopkT;
+  constexpr bool ATM = MODE == kTcTopkT;                    // A resident in TMEM
+  constexpr int TN = ATM ? 128 : kTcN;                      // db rows per tile
+  constexpr uint32_t kAB = ATM ? 0u : G::kABytes;           // A bytes per stage
+  constexpr uint32_t kSB = ATM ? (uint32_t)TN * KC : G::kStageBytes;   // stage bytes
+  constexpr uint32_t kAcc0 = ATM ? 256u : 0u;               // first accumulator column
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB alignment by pointer arithmetic on the shared array (keeps the shared address space,
   // so heap / table accesses compile to LDS/STS, not generic LD/ST). Both CTAs of a pair get
@@ -389,7 +452,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   uint8_t* smem = smem_raw + ((1024u - (tc::saddr(smem_raw) & 1023u)) & 1023u);
   const uint32_t S = p.stages;
   const uint32_t base = tc::saddr(smem);
-  const uint32_t bars = base + S * G::kStageBytes;
+  const uint32_t bars = base + S * kSB;
   auto full = [&](uint32_t s) { return bars + 8u * s; };
   auto empty = [&](uint32_t s) { return bars + 8u * (S + s); };
   auto tfull = [&](int a) { return bars + 8u * (2 * S + a); };
@@ -404,9 +467,10 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   // kTcTopk: 4-slot ring of per-tile db metadata, bulk-loaded by the producer
   auto mfull = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 13 + k); };
   auto mempty = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 17 + k); };
-  uint8_t* extra = smem + S * G::kStageBytes + 1024;        // estimator table or top-k heaps
+  const uint32_t aready = bars + 8u * (2 * S + 2 * kTcAcc + 21);   // kTcTopkT: item's A in TMEM
+  uint8_t* extra = smem + S * kSB + 1024;        // estimator table or top-k heaps
   // kTcTopk: the metadata ring [4][256] int2 after the heaps and the survivor scratch
-  int2* meta_s = reinterpret_cast<int2*>(extra + (size_t)p.k * kTcM * 12 + 32 * kTcM * 4);
+  int2* meta_s = reinterpret_cast<int2*>(extra + (size_t)p.k * kTcM * 12 + (kEpi / 4) * 32 * kTcM * 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? tc::cluster_rank() : 0u;
   const bool leader = rank == 0u;
@@ -415,10 +479,13 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // CG = 2 counts: tempty one arrival per epilogue warp of both CTAs; iempty the leader's MMA
     // lane + epilogue warps and the peer's producer lane + epilogue warps (the leader's barriers)
     for (uint32_t s = 0; s < S; ++s) { tc::mbar_init(full(s), 1); tc::mbar_init(empty(s), 1); }
-    for (int a = 0; a < kTcAcc; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), CG == 1 ? 32 * kEpi : 2 * kEpi); }
+    // warps that read each accumulator: every epilogue warp, except top-k (one group of 4)
+    constexpr int kTileWarps = TOPK ? 4 : kEpi;
+    for (int a = 0; a < kTcAcc; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), CG == 1 ? 32 * kTileWarps : 2 * kTileWarps); }
     constexpr int kTake = kEpi;   // item consumers besides the MMA / producer lanes
     for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(ifull(k), 1); tc::mbar_init(iempty(k), CG == 1 ? 1 + kTake : 2 + 2 * kTake); }
-    for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(mfull(k), 1); tc::mbar_init(mempty(k), kEpi); }
+    for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(mfull(k), 1); tc::mbar_init(mempty(k), kTileWarps); }
+    tc::mbar_init(aready, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -431,8 +498,8 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
   }
   const double* L = p.L;
-  double* Ls = reinterpret_cast<double*>(extra + ((MODE == kTcTopk || MODE == kTcJoin) ? p.heap_smem : 0u));
-  if ((MODE == kTcEstimate && p.l_smem) || MODE == kTcTopk || (MODE == kTcJoin && p.l_topk_smem)) {   // top-k always stages the table
+  double* Ls = reinterpret_cast<double*>(extra + ((TOPK || MODE == kTcJoin) ? p.heap_smem : 0u));
+  if ((MODE == kTcEstimate && p.l_smem) || TOPK || (MODE == kTcJoin && p.l_topk_smem)) {   // top-k always stages the table
     for (uint32_t i = threadIdx.x; i <= p.N; i += blockDim.x) Ls[i] = p.L[i];
     L = Ls;
   }
@@ -490,104 +557,150 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
   };
 
+  // Producer and MMA roles run as whole converged warps (barrier waits by every lane, the TMA /
+  // MMA / commit instructions under elect.sync), so the descriptor and coordinate arithmetic
+  // stays on the uniform datapath instead of a single-thread branch (ELECT + R2UR broadcasts +
+  // BRA.U.ANY around every tcgen05 / TMA instruction).
   if (warp == 0) {
-    if (lane == 0) {   // ---- TMA producer (both CTAs: own A rows, own half of the B rows)
+    {   // ---- TMA producer (both CTAs: own A rows, own half of the B rows)
       uint32_t stage = 0, phase = 0, mcount = 0;
       for (uint32_t ii = 0;; ++ii) {
-        const uint64_t it = (CG == 1 || leader) ? publish_item(ii) : take_item(ii);
+        uint64_t it = 0;
+        if (lane == 0) it = (CG == 1 || leader) ? publish_item(ii) : take_item(ii);
+        it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= p.nitems) break;
         uint64_t mt; uint32_t sp, nt0, nt1;
         item_range(it, mt, sp, nt0, nt1);
         for (uint32_t nt = nt0; nt < nt1; ++nt) {
-          if constexpr (MODE == kTcTopk) {   // the tile's db metadata for the epilogue
+          if constexpr (TOPK) {   // the tile's db metadata for the epilogue
             const uint32_t ms = mcount & 3u;
             tc::mbar_wait(mempty(ms), ((mcount >> 2) & 1u) ^ 1u);
-            tc::mbar_expect_tx(mfull(ms), kTcN * 8u);
-            tc::bulk_load(tc::saddr(meta_s) + ms * kTcN * 8u, p.meta + (size_t)nt * kTcN, kTcN * 8u, mfull(ms));
+            if (tc::elect_one()) {
+              tc::mbar_expect_tx(mfull(ms), TN * 8u);
+              tc::bulk_load(tc::saddr(meta_s) + ms * kTcN * 8u, p.meta + (size_t)nt * TN, TN * 8u, mfull(ms));
+            }
+            __syncwarp();
             ++mcount;
           }
           for (uint32_t kc = 0; kc < p.nk; ++kc) {
+            BSK_T0(tw2);
             tc::mbar_wait(empty(stage), phase ^ 1u);
-            const uint32_t sa = base + stage * G::kStageBytes;
-            if constexpr (CG == 1) {
-              tc::mbar_expect_tx(full(stage), G::kStageBytes);
-              tc::tma_load_2d(sa, &tmA, (int32_t)(kc * KC), (int32_t)(mt * kTcM), full(stage));
-              tc::tma_load_2d(sa + G::kABytes, &tmB, (int32_t)(kc * KC), (int32_t)(nt * kTcN), full(stage));
-            } else {
-              if (leader) tc::mbar_expect_tx(full(stage), 2u * G::kStageBytes);   // both CTAs' bytes
-              const uint32_t fb = tc::mapa(full(stage), 0u);
-              tc::tma_load_2d_pair(sa, &tmA, (int32_t)(kc * KC), (int32_t)(mt * kTcM), fb);
-              tc::tma_load_2d_pair(sa + G::kABytes, &tmB, (int32_t)(kc * KC),
-                                   (int32_t)(nt * kTcN + rank * (kTcN / 2)), fb);
+            if (TOPK && lane == 0) BSK_TADD(12, tw2);
+            const uint32_t sa = base + stage * kSB;
+            if (tc::elect_one()) {
+              if constexpr (ATM) {
+                tc::mbar_expect_tx(full(stage), kSB);
+                tc::tma_load_2d(sa, &tmB, (int32_t)(kc * KC), (int32_t)(nt * TN), full(stage));
+              } else if constexpr (CG == 1) {
+                tc::mbar_expect_tx(full(stage), G::kStageBytes);
+                tc::tma_load_2d(sa, &tmA, (int32_t)(kc * KC), (int32_t)(mt * kTcM), full(stage));
+                tc::tma_load_2d(sa + G::kABytes, &tmB, (int32_t)(kc * KC), (int32_t)(nt * kTcN), full(stage));
+              } else {
+                if (leader) tc::mbar_expect_tx(full(stage), 2u * G::kStageBytes);   // both CTAs' bytes
+                const uint32_t fb = tc::mapa(full(stage), 0u);
+                tc::tma_load_2d_pair(sa, &tmA, (int32_t)(kc * KC), (int32_t)(mt * kTcM), fb);
+                tc::tma_load_2d_pair(sa + G::kABytes, &tmB, (int32_t)(kc * KC),
+                                     (int32_t)(nt * kTcN + rank * (kTcN / 2)), fb);
+              }
             }
+            __syncwarp();
             if (++stage == S) { stage = 0; phase ^= 1u; }
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {   // ---- MMA issuer (the leader's, for the pair when CG = 2)
-      constexpr uint32_t idesc = (2u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)((kTcM * CG) >> 4) << 24);
+    if (leader) {   // ---- MMA issuer (the leader's, for the pair when CG = 2)
+      BSK_T0(tmma);
+      constexpr uint32_t idesc = (2u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)((kTcM * CG) >> 4) << 24);
       uint32_t stage = 0, phase = 0, aphase = 0;
       int acc = 0;
       for (uint32_t ii = 0;; ++ii) {
-        const uint64_t it = take_item(ii);
+        uint64_t it = 0;
+        if (lane == 0) it = take_item(ii);
+        it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= p.nitems) break;
         uint64_t mt; uint32_t sp, nt0, nt1;
         item_range(it, mt, sp, nt0, nt1);
-        for (uint32_t nt = nt0; nt < nt1; ++nt) {
-          tc::mbar_wait(tempty(acc), aphase ^ 1u);
+        if constexpr (ATM) {   // this item's A rows in TMEM (written by the epilogue warps)
+          tc::mbar_wait(aready, ii & 1u);
           tc::fence_after();
-          const uint32_t d = tmem + (uint32_t)acc * kTcN;
+        }
+        for (uint32_t nt = nt0; nt < nt1; ++nt) {
+          BSK_T0(tw0);
+          tc::mbar_wait(tempty(acc), aphase ^ 1u);
+          if (TOPK && lane == 0) BSK_TADD(10, tw0);
+          tc::fence_after();
+          const uint32_t d = tmem + kAcc0 + (uint32_t)acc * TN;
           for (uint32_t kc = 0; kc < p.nk; ++kc) {
+            BSK_T0(tw1);
             tc::mbar_wait(full(stage), phase);
+            if (TOPK && lane == 0) BSK_TADD(11, tw1);
             tc::fence_after();
-            const uint32_t sa = base + stage * G::kStageBytes;
-            const uint64_t da = desc_sw<KC>(sa), db = desc_sw<KC>(sa + G::kABytes);
+            const uint32_t sa = base + stage * kSB;
+            const uint64_t da = desc_sw<KC>(sa), db = desc_sw<KC>(sa + kAB);
+            if (tc::elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < KC / 32; ++kk) {   // K = 32 bytes per MMA: +2 in 16-B units
-              if constexpr (CG == 1) tc::mma_u8(d, da + 2u * kk, db + 2u * kk, idesc, (kc | (uint32_t)kk) != 0u);
-              else tc::mma_u8_pair(d, da + 2u * kk, db + 2u * kk, idesc, (kc | (uint32_t)kk) != 0u);
+              for (int kk = 0; kk < KC / 32; ++kk) {   // K = 32 bytes per MMA: +2 in 16-B units
+                if constexpr (ATM) tc::mma_u8_ts(d, tmem + (kc * KC + 32u * kk) / 4u, db + 2u * kk, idesc, (kc | (uint32_t)kk) != 0u);
+                else if constexpr (CG == 1) tc::mma_u8(d, da + 2u * kk, db + 2u * kk, idesc, (kc | (uint32_t)kk) != 0u);
+                else tc::mma_u8_pair(d, da + 2u * kk, db + 2u * kk, idesc, (kc | (uint32_t)kk) != 0u);
+              }
+              // frees the smem stage (both CTAs' when CG = 2) when these MMAs finish
+              if constexpr (CG == 1) tc::commit(empty(stage));
+              else tc::commit_pair(empty(stage), (uint16_t)3u);
             }
-            // frees the smem stage (both CTAs' when CG = 2) when these MMAs finish
-            if constexpr (CG == 1) tc::commit(empty(stage));
-            else tc::commit_pair(empty(stage), (uint16_t)3u);
+            __syncwarp();
             if (++stage == S) { stage = 0; phase ^= 1u; }
           }
           // accumulator ready for the epilogue (of both CTAs)
-          if constexpr (CG == 1) tc::commit(tfull(acc));
-          else tc::commit_pair(tfull(acc), (uint16_t)3u);
+          if (tc::elect_one()) {
+            if constexpr (CG == 1) tc::commit(tfull(acc));
+            else tc::commit_pair(tfull(acc), (uint16_t)3u);
+          }
+          __syncwarp();
           if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
         }
       }
+      if (TOPK && lane == 0) BSK_TADD(14, tmma);
     }
-  } else if (MODE == kTcTopk) {
+  } else if (TOPK) {
     // ---- top-k epilogue: thread = one query row (TMEM lane), its k best (key, db index)
-    // as a heap (worst at the root) in shared memory. Per 256-column tile: a prefilter
+    // as a heap (worst at the root) in shared memory. kEpi / 4 groups of four warps (one per
+    // TMEM lane quadrant) take the tiles in turn (group g: the tiles of accumulator g when
+    // there are two groups), so two tiles are filtered at once; a row's heap is shared by the
+    // groups under a per-row lock, and its threshold is published for the other group's
+    // prefilter (index written before key, read key first: any read is a valid lower bound).
+    // Per tile: a prefilter
     // bound pmin on the AND-popcount (db sorted by popcount, so the tile's pb range is
     // narrow); chunks of 32 columns whose max pab < pmin are skipped with one compare.
     // Survivors: while a row's heap fills, each lane evaluates its own columns; in steady
     // state they go through a per-warp queue and are scored lane-parallel (exact fp64
     // recipe), only the rare insertions being serialised to the owning lane.
+    constexpr uint32_t NGRP = kEpi / 4;               // epilogue groups
     const uint32_t lb = 32u * (uint32_t)(warp & 3);
     const uint32_t rt = lb + (uint32_t)lane;          // row within the tile
+    const uint32_t grp = (uint32_t)(warp - 2) >> 2;   // this warp's group
     const uint32_t m = p.measure, K = p.k;
     constexpr uint32_t kQCap = 256;                   // per-warp survivor queue entries
-    double* hk = reinterpret_cast<double*>(extra);
-    int32_t* hi = reinterpret_cast<int32_t*>(extra + (size_t)K * kTcM * 8);
-    uint32_t* scr = reinterpret_cast<uint32_t*>(extra + (size_t)K * kTcM * 12);            // [32][128]
-    // this warp's copy of the tile's db popcounts [256] and original indices [256]
-    uint32_t mcount = 0;   // tiles seen: metadata ring slot / phase
-    uint2* q = reinterpret_cast<uint2*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4) +
-               (size_t)(warp - 2) * kQCap;
-    uint4* cq = reinterpret_cast<uint4*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 +
-                                         4 * kQCap * 8) + (size_t)(warp - 2) * 32;   // per-warp candidate list
-    uint32_t* own = reinterpret_cast<uint32_t*>(extra + (size_t)K * kTcM * 12 + 32 * kTcM * 4 + 4 * 2 * kTcN * 4 +
-                                                4 * kQCap * 8 + 4 * 32 * 16) + (size_t)(warp - 2) * 32;   // per-owner candidate masks
+    // shared-memory layout (host: topk_heap_smem): heaps | per-group scratch | metadata ring |
+    // per-warp queues, candidates, owner masks | per-row count, threshold, lock
+    uint8_t* xp = extra;
+    double* hk = reinterpret_cast<double*>(xp);                    xp += (size_t)K * kTcM * 8;
+    int32_t* hi = reinterpret_cast<int32_t*>(xp);                  xp += (size_t)K * kTcM * 4;
+    uint32_t* scr = reinterpret_cast<uint32_t*>(xp) + grp * 32 * kTcM;   xp += NGRP * 32 * kTcM * 4;   // [32][128] per group
+    xp += 4 * kTcN * 8;                                                  // metadata ring (meta_s)
+    uint2* q = reinterpret_cast<uint2*>(xp) + (size_t)(warp - 2) * kQCap;  xp += kEpi * kQCap * 8;
+    uint4* cq = reinterpret_cast<uint4*>(xp) + (size_t)(warp - 2) * 32;    xp += kEpi * 32 * 16;   // per-warp candidate list
+    uint32_t* own = reinterpret_cast<uint32_t*>(xp) + (size_t)(warp - 2) * 32;  xp += kEpi * 32 * 4;   // per-owner masks
+    volatile uint32_t* cnt_s = reinterpret_cast<volatile uint32_t*>(xp);  xp += kTcM * 4;
+    volatile double* Tp = reinterpret_cast<volatile double*>(xp);        xp += kTcM * 8;
+    volatile int32_t* Tip = reinterpret_cast<volatile int32_t*>(xp);     xp += kTcM * 4;
+    uint32_t* lk = reinterpret_cast<uint32_t*>(xp);
     auto hkey = [&](uint32_t i) -> double& { return hk[i * kTcM + rt]; };
     auto hidx = [&](uint32_t i) -> int32_t& { return hi[i * kTcM + rt]; };
-    uint32_t aphase = 0;
-    int acc = 0;
+    auto epi_bar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpi) : "memory"); };
+    uint32_t tcount = 0;   // tiles seen (every group): accumulator, metadata slot and phases
     for (uint32_t ii = 0;; ++ii) {
       uint64_t it = 0;
       if (lane == 0) it = take_item(ii);
@@ -597,6 +710,24 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       item_range(it, mt, sp, nt0, nt1);
       const uint64_t r = mt * kTcM + rt;               // row of the (sorted) query matrix
       const bool valid = r < p.na;
+      if (ATM && grp == 0) {
+        // this item's 128 query rows -> TMEM columns [0, kp/4) (lane = row, 4 K-bytes per column).
+        // The previous item's MMAs are complete (this warp waited on its last accumulator).
+        const uint4* src = reinterpret_cast<const uint4*>(p.a8 + (valid ? r : 0) * p.kp);
+        for (uint32_t c0 = 0; c0 < p.kp / 4u; c0 += 32) {
+          uint32_t v[32];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 x = valid ? __ldg(src + c0 / 4u + j) : make_uint4(0u, 0u, 0u, 0u);
+            v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
+          }
+          tc::tmem_st32(tmem + (lb << 16) + c0, v);
+        }
+        tc::tmem_st_wait();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(aready);
+      }
       const int pa = valid ? __ldg(p.pa + r) : 0;
       const uint64_t rq = (valid && p.qperm) ? (uint64_t)__ldg(p.qperm + r) : r;   // original query index
       const double La = Ls[pa];
@@ -604,7 +735,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       uint32_t cnt = valid ? 0u : K, pmin = 0;   // invalid rows count as full (never insert)
       double T = -__longlong_as_double(0x7ff0000000000000LL);
       int32_t Ti = kSentinelIdx;
-      if (p.chain && sp > 0) {
+      if (grp == 0 && p.chain && sp > 0) {
         // resume this row's heap from the previous chunk (chunk order per query tile is
         // enforced by the done counters: 4 epilogue warps finish each chunk)
         if (lane == 0) {
@@ -625,6 +756,16 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           if (cnt == K) { T = hkey(0); Ti = hidx(0); }
         }
       }
+      if (grp == 0) {   // publish the row state for both groups
+        cnt_s[rt] = cnt; Tip[rt] = Ti; Tp[rt] = T; lk[rt] = 0u;
+      }
+      epi_bar();
+      // threshold of this row as published by any group (a valid lower bound of the current one)
+      auto refresh = [&]() {
+        cnt = cnt_s[rt];
+        if (cnt >= K) { T = Tp[rt]; __threadfence_block(); Ti = Tip[rt]; }
+      };
+      refresh();
       auto sift_down = [&](uint32_t i) {
         for (;;) {
           const uint32_t l = 2 * i + 1, rr = l + 1;
@@ -638,20 +779,31 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           i = w;
         }
       };
-      // offer (key, original db index) to this lane's row
+      // offer (key, original db index) to this lane's row: under the row lock, against the
+      // heap itself; republishes the threshold (index first, then key)
       auto offer = [&](double key, int32_t orig) {
         if ((p.flags & 1u) && (uint64_t)orig == rq) return;
-        if (cnt < K) {
-          hkey(cnt) = key; hidx(cnt) = orig;
-          if (++cnt == K) {
+        while (atomicCAS(lk + rt, 0u, 1u) != 0u) {}
+        __threadfence_block();
+        uint32_t c = cnt_s[rt];
+        bool pub = false;
+        if (c < K) {
+          hkey(c) = key; hidx(c) = orig;
+          cnt_s[rt] = ++c;
+          if (c == K) {
             for (int i = (int)K / 2 - 1; i >= 0; --i) sift_down((uint32_t)i);
-            T = hkey(0); Ti = hidx(0);
+            pub = true;
           }
-        } else if (before(key, orig, T, Ti)) {
+        } else if (before(key, orig, hkey(0), hidx(0))) {
           hkey(0) = key; hidx(0) = orig;
           sift_down(0);
-          T = hkey(0); Ti = hidx(0);
+          pub = true;
         }
+        cnt = c;
+        if (c >= K) { T = hkey(0); Ti = hidx(0); }
+        if (pub) { Tip[rt] = Ti; __threadfence_block(); Tp[rt] = T; }
+        __threadfence_block();
+        atomicExch(lk + rt, 0u);
       };
       // Upper bound of the key over every pair of this row with a db row of popcount
       // pb in [lo, hi] and AND-popcount pab (K10): the IP raw value decreases
@@ -700,17 +852,79 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         return qq;
       };
       for (uint32_t nt = nt0; nt < nt1; ++nt) {
-        const uint64_t n0 = (uint64_t)nt * kTcN;
+        const uint32_t my = tcount++;
+        if (my % NGRP != grp) continue;                // the other group's tile
+        const int acc = (int)(my % kTcAcc);
+        const uint32_t aphase = (my / kTcAcc) & 1u;
+        BSK_T0(te0);
+        refresh();
+        const uint64_t n0 = (uint64_t)nt * TN;
         // this tile's db popcounts / original indices, bulk-loaded by the producer
-        const uint32_t ms = mcount & 3u;
-        tc::mbar_wait(mfull(ms), (mcount >> 2) & 1u);
+        const uint32_t ms = my & 3u;
+        tc::mbar_wait(mfull(ms), (my >> 2) & 1u);
         const int2* tm = meta_s + ms * kTcN;
-        const uint32_t nval = (uint32_t)min((uint64_t)kTcN, p.nb - n0);
+        const uint32_t nval = (uint32_t)min((uint64_t)TN, p.nb - n0);
         // the tile's popcount range (the db is popcount-sorted, descending or ascending)
         if (valid) pmin = tile_pmin(min((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x), max((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x));
         const bool direct = __any_sync(0xffffffffu, cnt < K);
+#ifdef BSK_TOPK_STATS
+        {
+          const uint32_t hi_ = max((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x);
+          const bool skip = __all_sync(0xffffffffu, !valid || (cnt >= K && pmin > min((uint32_t)pa, hi_)));
+          if (lane == 0) { atomicAdd(&g_tkstats[0], 1ull); if (skip) atomicAdd(&g_tkstats[1], 1ull); if (direct) atomicAdd(&g_tkstats[4], 1ull); }
+        }
+#endif
+        if (lane == 0) BSK_TADD(9, te0);
+        BSK_T0(te1);
         tc::mbar_wait(tfull(acc), aphase);
+        if (lane == 0) BSK_TADD(6, te1);
+        BSK_T0(te2);
         tc::fence_after();
+        // survivors queued by this warp since the last call, scored lane-parallel (exact fp64 recipe)
+        uint32_t qn = 0;
+        auto score_queue = [&]() {
+          __syncwarp();
+          for (uint32_t b = 0; b < qn; b += 32) {
+            const bool has = b + lane < qn;
+            const uint2 e = has ? q[b + lane] : make_uint2(0u, 0u);
+            const int owner = (int)(e.y >> 24);
+            const int pa_o = __shfl_sync(0xffffffffu, pa, owner);
+            const double T_o = __shfl_sync(0xffffffffu, T, owner);
+            const int32_t Ti_o = __shfl_sync(0xffffffffu, Ti, owner);
+            double key = -__longlong_as_double(0x7ff0000000000000LL);
+            const int2 me = tm[e.x];
+            if (has) key = measure_key(estimate_pair(pa_o, me.x, (int)(e.y & 0xFFFFFFu), (int)p.N, Ls, m), m);
+            // candidates — those that would enter the owner's heap at its current threshold
+            // (key, then the tie order of R-G17 on the db index, checked here lane-parallel:
+            // rows with tiny sketches tie with thousands of db rows) — go back to their owners
+            const bool cand = has && before(key, me.y, T_o, Ti_o);
+            const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+#ifdef BSK_TOPK_STATS
+            if (lane == 0) atomicAdd(&g_tkstats[5], (unsigned long long)__popc(bal));
+#endif
+            if (bal) {
+              // owner-parallel insertion: candidate of evaluating lane e sits in cq[e]; the
+              // lowest lane of each same-owner group publishes the group's mask to its owner,
+              // and every owner walks its own candidates (rounds = max candidates per owner)
+              const uint32_t grp = __match_any_sync(0xffffffffu, cand ? (uint32_t)owner : 32u + (uint32_t)lane);
+              __syncwarp();
+              own[lane] = 0u;
+              if (cand) cq[lane] = make_uint4(e.x, (uint32_t)owner, __double2loint(key), __double2hiint(key));
+              __syncwarp();
+              if (cand && (grp & ((1u << lane) - 1u)) == 0u) own[owner] = grp;
+              __syncwarp();
+              uint32_t mine = own[lane];
+              while (mine) {
+                const uint32_t ee = __ffs(mine) - 1; mine &= mine - 1;
+                const uint4 c4 = cq[ee];
+                offer(__hiloint2double((int)c4.w, (int)c4.z), tm[c4.x].y);
+              }
+              __syncwarp();
+            }
+          }
+          __syncwarp();
+          qn = 0;
+        };
         // one 32-column chunk (values v): prefilter, then survivors
         auto chunk = [&](const uint32_t c, uint32_t (&v)[32]) {
           if (c >= nval) return;
@@ -721,6 +935,12 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           // survivor mask of this lane
           const uint32_t sm = pass ? ge_mask32(v, pmin) & (left >= 32 ? 0xffffffffu : ((1u << left) - 1u)) : 0u;
           const uint32_t ns = __popc(sm);
+#ifdef BSK_TOPK_STATS
+          {
+            const uint32_t tot = __reduce_add_sync(0xffffffffu, ns);
+            if (lane == 0) { atomicAdd(&g_tkstats[2], 1ull); atomicAdd(&g_tkstats[3], (unsigned long long)tot); }
+          }
+#endif
           uint32_t off = ns;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, off, o); if (lane >= o) off += y; }
@@ -754,69 +974,51 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             __syncwarp();
             return;
           }
-          // queue: (column in tile, owner lane << 24 | pab)
+          // queue: (column in tile, owner lane << 24 | pab); scored after the accumulator is
+          // released (score_queue), so the MMA never waits on survivor scoring
+          if (qn + total > kQCap) score_queue();
+          off += qn;
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if ((sm >> j) & 1u) q[off++] = make_uint2(c + (uint32_t)j, ((uint32_t)lane << 24) | v[j]);
-          __syncwarp();
-          for (uint32_t b = 0; b < total; b += 32) {
-            const bool has = b + lane < total;
-            const uint2 e = has ? q[b + lane] : make_uint2(0u, 0u);
-            const int owner = (int)(e.y >> 24);
-            const int pa_o = __shfl_sync(0xffffffffu, pa, owner);
-            const double T_o = __shfl_sync(0xffffffffu, T, owner);
-            const int32_t Ti_o = __shfl_sync(0xffffffffu, Ti, owner);
-            double key = -__longlong_as_double(0x7ff0000000000000LL);
-            const int2 me = tm[e.x];
-            if (has) key = measure_key(estimate_pair(pa_o, me.x, (int)(e.y & 0xFFFFFFu), (int)p.N, Ls, m), m);
-            // candidates — those that would enter the owner's heap at its current threshold
-            // (key, then the tie order of R-G17 on the db index, checked here lane-parallel:
-            // rows with tiny sketches tie with thousands of db rows) — go back to their owners
-            const bool cand = has && before(key, me.y, T_o, Ti_o);
-            const uint32_t bal = __ballot_sync(0xffffffffu, cand);
-            if (bal) {
-              // owner-parallel insertion: candidate of evaluating lane e sits in cq[e]; the
-              // lowest lane of each same-owner group publishes the group's mask to its owner,
-              // and every owner walks its own candidates (rounds = max candidates per owner)
-              const uint32_t grp = __match_any_sync(0xffffffffu, cand ? (uint32_t)owner : 32u + (uint32_t)lane);
-              __syncwarp();
-              own[lane] = 0u;
-              if (cand) cq[lane] = make_uint4(e.x, (uint32_t)owner, __double2loint(key), __double2hiint(key));
-              __syncwarp();
-              if (cand && (grp & ((1u << lane) - 1u)) == 0u) own[owner] = grp;
-              __syncwarp();
-              uint32_t mine = own[lane];
-              while (mine) {
-                const uint32_t ee = __ffs(mine) - 1; mine &= mine - 1;
-                const uint4 c4 = cq[ee];
-                offer(__hiloint2double((int)c4.w, (int)c4.z), tm[c4.x].y);
-              }
-              __syncwarp();
-            }
-          }
+          qn += total;
           __syncwarp();
                 };
-        // TMEM loads software-pipelined: chunk c+1 is in flight while chunk c is tested
-        const uint32_t tb = tmem + (lb << 16) + (uint32_t)acc * kTcN;
-        uint32_t va[32], vb[32];
-        tc::tmem_ld32_issue(tb, va);
-        tc::tmem_ld_wait(va);
+        // 64 columns per step: both TMEM loads in flight, one vote for the pair of chunks (the
+        // prefilter rejects ~90 % of them); the whole tile is skipped without reading TMEM when
+        // no row of the warp can reach its threshold in it (pmin above the row's largest pab)
+        const uint32_t tb = tmem + (lb << 16) + kAcc0 + (uint32_t)acc * TN;
+        const uint32_t tile_hi = max((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x);
+#ifdef BSK_TOPK_NULLEPI
+        if (false) {   // dev: MMA/TMA-side bound of the tiling (results are garbage)
+#else
+        if (__any_sync(0xffffffffu, valid && (cnt < K || pmin <= min((uint32_t)pa, tile_hi)))) {
+#endif
+          uint32_t va[32], vb[32];
 #pragma unroll 1
-        for (uint32_t c = 0; c < (uint32_t)kTcN; c += 64) {
-          tc::tmem_ld32_issue(tb + c + 32, vb);
-          chunk(c, va);
-          tc::tmem_ld_wait(vb);
-          if (c + 64 < (uint32_t)kTcN) tc::tmem_ld32_issue(tb + c + 64, va);
-          chunk(c + 32, vb);
-          if (c + 64 < (uint32_t)kTcN) tc::tmem_ld_wait(va);
+          for (uint32_t c = 0; c < nval; c += 64) {
+            tc::tmem_ld32_issue(tb + c, va);
+            tc::tmem_ld32_issue(tb + c + 32, vb);
+            tc::tmem_ld_wait(va);
+            tc::tmem_ld_wait(vb);
+            const uint32_t mx = max(max32(va), max32(vb));
+            if (__any_sync(0xffffffffu, valid && mx >= pmin)) {
+              chunk(c, va);
+              chunk(c + 32, vb);
+            }
+          }
         }
         release_acc(acc);
+        if (lane == 0) BSK_TADD(7, te2);
+        BSK_T0(te3);
+        if (qn) score_queue();
+        if (lane == 0) BSK_TADD(8, te3);
         __syncwarp();   // every lane done with this tile's metadata
         if (lane == 0) tc::mbar_arrive(mempty(ms));
-        ++mcount;
-        if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
       }
-      if (valid) {   // partial list of this (row, chunk) — or the row's running heap when chained
+      epi_bar();   // every group done with this item's tiles
+      cnt = cnt_s[rt];
+      if (grp == 0 && valid) {   // partial list of this (row, chunk) — or the row's running heap when chained
         const uint64_t slot = p.chain ? rq : rq * p.splits + sp;
         double* ok = p.part_key + slot * K;
         int32_t* oi = p.part_idx + slot * K;
@@ -825,7 +1027,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           __stcg(oi + i, i < cnt ? hidx(i) : kSentinelIdx);
         }
       }
-      if (p.chain) {
+      if (grp == 0 && p.chain) {
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(p.done + mt / CG, 1u);
@@ -1107,8 +1309,8 @@ cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* o
 // when there are enough query tiles to keep every SM busy; otherwise it uses independent
 // per-chunk partial lists merged afterwards.
 struct TcSplit { uint32_t splits, chain; };
-static TcSplit tc_split_rule(uint64_t na, uint64_t nb, uint32_t N, bool topk, uint32_t k = 0) {
-  const uint64_t tiles_n = (nb + kTcN - 1) / kTcN, mtiles = (na + kTcM - 1) / kTcM, sms = 148;
+static TcSplit tc_split_rule(uint64_t na, uint64_t nb, uint32_t N, bool topk, uint32_t k = 0, uint32_t tn = kTcN) {
+  const uint64_t tiles_n = (nb + tn - 1) / tn, mtiles = (na + kTcM - 1) / kTcM, sms = 148;
   const uint64_t chunk_bytes = 40ull << 20;
   uint64_t s_l2 = (nb * tc_kpad(N) + chunk_bytes - 1) / chunk_bytes;
   uint64_t s_par = (2 * sms + mtiles - 1) / mtiles;
@@ -1131,6 +1333,7 @@ static TcSplit tc_split_rule(uint64_t na, uint64_t nb, uint32_t N, bool topk, ui
 // BINSKETCH_TC_CG=1|2 overrides (dev A/B; K10).
 template <int MODE>
 static int tc_cg(uint32_t Kp) {
+  if (MODE == kTcTopkT) return 1;
   if (const char* e = std::getenv("BINSKETCH_TC_CG")) return std::atoi(e) == 2 ? 2 : 1;
   return (Kp >= 16384u || (MODE == kTcAndPopc && Kp >= 4096u)) ? 2 : 1;
 }
@@ -1141,21 +1344,28 @@ template <int MODE, int KC, int CG>
 static cudaError_t tc_launch_cg(const uint8_t* A8, const uint8_t* B8, TcParams& p, uint32_t N, uint32_t extra_bytes,
                                 uint32_t force_splits, cudaStream_t s) {
   using G = TcGeom<KC, CG>;
+  constexpr bool ATM = MODE == kTcTopkT;
+  constexpr uint32_t TN = ATM ? 128u : (uint32_t)kTcN;
+  constexpr uint32_t kSB = ATM ? TN * KC : G::kStageBytes;
   const uint32_t Kp = tc_kpad(N);
   if (p.na > 0x7fffffffull || p.nb > 0x7fffffffull) return cudaErrorInvalidValue;
+  if (ATM && (CG != 1 || Kp > 1024u)) return cudaErrorInvalidValue;   // A must fit TMEM columns [0, 256)
   const uint32_t fixed = 1024 /* align */ + 1024 /* barriers */ + extra_bytes;
-  if (fixed + 2 * G::kStageBytes > kTcSmemMax) return cudaErrorInvalidConfiguration;
-  p.stages = std::min<uint32_t>(8, (kTcSmemMax - fixed) / G::kStageBytes);
+  if (fixed + 2 * kSB > kTcSmemMax) return cudaErrorInvalidConfiguration;
+  p.stages = std::min<uint32_t>(ATM ? 16u : 8u, (kTcSmemMax - fixed) / kSB);
+  if (const char* st = std::getenv("BINSKETCH_TC_STAGES"))   // dev A/B: cap the ring depth
+    p.stages = std::max<uint32_t>(2u, std::min<uint32_t>(p.stages, (uint32_t)std::atoi(st)));
   alignas(64) CUtensorMap ma, mb;
-  if (!make_map(&ma, A8, p.na, Kp, kTcM, KC) || !make_map(&mb, B8, p.nb, Kp, kTcN / CG, KC)) return cudaErrorNotSupported;
+  if (!make_map(&ma, A8, p.na, Kp, kTcM, KC) || !make_map(&mb, B8, p.nb, Kp, ATM ? TN : kTcN / CG, KC))
+    return cudaErrorNotSupported;
   cudaError_t e = cudaSuccess;
   p.nk = Kp / KC;
-  p.tiles_n = (uint32_t)((p.nb + kTcN - 1) / kTcN);
+  p.tiles_n = (uint32_t)((p.nb + TN - 1) / TN);
   const uint64_t mtiles = (p.na + kTcM * CG - 1) / (kTcM * CG);   // items' m-index: 128 x CG rows
   if (force_splits) {
     p.splits = force_splits;
   } else {
-    const TcSplit sc = tc_split_rule(p.na, p.nb, N, MODE == kTcTopk);
+    const TcSplit sc = tc_split_rule(p.na, p.nb, N, MODE == kTcTopk || ATM, 0, TN);
     p.splits = sc.splits;
     p.chain = sc.chain;
   }
@@ -1168,7 +1378,7 @@ static cudaError_t tc_launch_cg(const uint8_t* A8, const uint8_t* B8, TcParams& 
     e = cudaMemsetAsync(p.done, 0, mtiles * sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
   }
-  const uint32_t smem = p.stages * G::kStageBytes + fixed;
+  const uint32_t smem = p.stages * kSB + fixed;
   auto kern = tc_pairs_kernel<MODE, KC, CG>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -1250,10 +1460,18 @@ cudaError_t launch_sort_by_popcount(const int32_t* pb, uint64_t n, uint32_t N, u
   return cudaGetLastError();
 }
 
+// The fused top-k keeps the query tile in TMEM (kTcTopkT) when its widened rows fit 256 columns;
+// BINSKETCH_TC_ATM=0 forces the shared-memory A operand (dev A/B).
+static bool tc_topk_atm(uint32_t N) {
+  if (const char* e = std::getenv("BINSKETCH_TC_ATM")) if (!std::strcmp(e, "0")) return false;
+  return tc_kpad(N) <= 1024u;
+}
+static uint32_t tc_topk_tn(uint32_t N) { return tc_topk_atm(N) ? 128u : (uint32_t)kTcN; }
+
 uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t N, uint32_t k) {
   // partial lists per query in the workspace: 1 when the heaps are chained, else one per chunk
   if (nq == 0 || ndb == 0 || k == 0) return 1;
-  const TcSplit r = tc_split_rule(nq, ndb, N, true, k);
+  const TcSplit r = tc_split_rule(nq, ndb, N, true, k, tc_topk_tn(N));
   return r.chain ? 1u : r.splits;
 }
 
@@ -1270,12 +1488,17 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
   p.lc = std::log1p(-1.0 / (double)N);
   p.prefilter = (prefilter && perm) ? 1u : 0u;   // the per-tile bound needs the popcount-sorted db
   p.part_key = part_key; p.part_idx = part_idx;
-  p.heap_smem = k * kTcM * 12 + 32 * kTcM * 4 + 4 * kTcN * 8 + 4 * 256 * 8 + 4 * 32 * 16 + 4 * 32 * 4;   // heaps, scratch, metadata ring, queues, candidates, owner masks
+  // heaps, per-group scratch, metadata ring, per-warp queues / candidates / owner masks, row state
+  const bool atm = tc_topk_atm(N);
+  const uint32_t ne = atm ? TcRoles<kTcTopkT>::kEpi : TcRoles<kTcTopk>::kEpi;
+  p.heap_smem = k * kTcM * 12 + (ne / 4) * 32 * kTcM * 4 + 4 * kTcN * 8 + ne * 256 * 8 + ne * 32 * 16 + ne * 32 * 4 + kTcM * 20;
   const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
   if (lb > 48 * 1024) return cudaErrorInvalidValue;   // caller keeps N <= tc_topk_max_n()
   p.l_topk_smem = lb;
   // splits computed with the device-independent rule (148) so the workspace matches
-  const TcSplit sc = tc_split_rule(nq, ndb, N, true, k);
+  const TcSplit sc = tc_split_rule(nq, ndb, N, true, k, tc_topk_tn(N));
+  p.a8 = Q8;
+  p.kp = tc_kpad(N);
   p.chain = sc.chain;
   p.done = done;
   {
@@ -1285,7 +1508,8 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
     count_launch();
     p.meta = meta;
   }
-  cudaError_t e = tc_launch<kTcTopk, 64>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, sc.splits, s);
+  cudaError_t e = atm ? tc_launch<kTcTopkT, 128>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, sc.splits, s)
+                      : tc_launch<kTcTopk, 64>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, sc.splits, s);
   if (e != cudaSuccess) return e;
   const uint32_t lists = p.chain ? 1u : p.splits;
   if (lists != tc_topk_splits(nq, ndb, N, k)) return cudaErrorInvalidConfiguration;
