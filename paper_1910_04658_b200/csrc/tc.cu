@@ -239,12 +239,12 @@ __device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[32]) {
 
 #ifdef BSK_TOPK_PROF
 #define BSK_T0(v) const long long v = clock64()
-#define BSK_TADD(slot, t0) atomicAdd(&g_tkstats[slot], (unsigned long long)(clock64() - (t0)))
+#define BSK_TADD(slot, t0) (pacc[(slot) - 6] += (unsigned long long)(clock64() - (t0)))
 #else
 #define BSK_T0(v)
 #define BSK_TADD(slot, t0)
 #endif
-#ifdef BSK_TOPK_STATS
+#if defined(BSK_TOPK_STATS) || defined(BSK_TOPK_PROF)
 // dev instrumentation (never in the product build): warp-tiles, all-rows-skippable warp-tiles,
 // passing chunks, survivors, direct-path warp-tiles, candidates; BSK_TOPK_PROF adds clock64
 // cycle sums: [6] epilogue waits tfull, [7] filter, [8] scoring, [9] tile setup (metadata wait +
@@ -465,13 +465,18 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   auto iempty = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 5 + k); };
   const uint32_t iring = bars + 8u * (2 * S + 2 * kTcAcc + 9);   // 4 x u64 item ids
   // kTcTopk: 4-slot ring of per-tile db metadata, bulk-loaded by the producer
+  // top-k: ring of per-tile db metadata (kMS slots of TN entries, 8 KB), bulk-loaded by the producer
+  constexpr uint32_t kMS = ATM ? 8u : 4u;
   auto mfull = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 13 + k); };
-  auto mempty = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 17 + k); };
-  const uint32_t aready = bars + 8u * (2 * S + 2 * kTcAcc + 21);   // kTcTopkT: item's A in TMEM
+  auto mempty = [&](uint32_t k) { return bars + 8u * (2 * S + 2 * kTcAcc + 21 + k); };
+  const uint32_t aready = bars + 8u * (2 * S + 2 * kTcAcc + 29);   // kTcTopkT: item's A in TMEM
   uint8_t* extra = smem + S * kSB + 1024;        // estimator table or top-k heaps
   // kTcTopk: the metadata ring [4][256] int2 after the heaps and the survivor scratch
   int2* meta_s = reinterpret_cast<int2*>(extra + (size_t)p.k * kTcM * 12 + (kEpi / 4) * 32 * kTcM * 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef BSK_TOPK_PROF
+  unsigned long long pacc[9] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};   // per-lane cycle sums, slots 6..14
+#endif
   const uint32_t rank = CG == 2 ? tc::cluster_rank() : 0u;
   const bool leader = rank == 0u;
 
@@ -484,7 +489,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     for (int a = 0; a < kTcAcc; ++a) { tc::mbar_init(tfull(a), 1); tc::mbar_init(tempty(a), CG == 1 ? 32 * kTileWarps : 2 * kTileWarps); }
     constexpr int kTake = kEpi;   // item consumers besides the MMA / producer lanes
     for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(ifull(k), 1); tc::mbar_init(iempty(k), CG == 1 ? 1 + kTake : 2 + 2 * kTake); }
-    for (uint32_t k = 0; k < 4; ++k) { tc::mbar_init(mfull(k), 1); tc::mbar_init(mempty(k), kTileWarps); }
+    for (uint32_t k = 0; k < kMS; ++k) { tc::mbar_init(mfull(k), 1); tc::mbar_init(mempty(k), kTileWarps); }
     tc::mbar_init(aready, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -571,17 +576,24 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (it >= p.nitems) break;
         uint64_t mt; uint32_t sp, nt0, nt1;
         item_range(it, mt, sp, nt0, nt1);
-        for (uint32_t nt = nt0; nt < nt1; ++nt) {
-          if constexpr (TOPK) {   // the tile's db metadata for the epilogue
-            const uint32_t ms = mcount & 3u;
-            tc::mbar_wait(mempty(ms), ((mcount >> 2) & 1u) ^ 1u);
-            if (tc::elect_one()) {
-              tc::mbar_expect_tx(mfull(ms), TN * 8u);
-              tc::bulk_load(tc::saddr(meta_s) + ms * kTcN * 8u, p.meta + (size_t)nt * TN, TN * 8u, mfull(ms));
-            }
-            __syncwarp();
-            ++mcount;
+        // top-k: the tiles' db metadata for the epilogue, kMetaAhead tiles ahead of the B stages
+        // (the epilogue derives its per-tile bound before the accumulator is ready)
+        constexpr uint32_t kMetaAhead = ATM ? 3u : 0u;
+        auto issue_meta = [&](uint32_t tnt) {
+          const uint32_t ms = mcount % kMS;
+          tc::mbar_wait(mempty(ms), ((mcount / kMS) & 1u) ^ 1u);
+          if (tc::elect_one()) {
+            tc::mbar_expect_tx(mfull(ms), TN * 8u);
+            tc::bulk_load(tc::saddr(meta_s) + ms * TN * 8u, p.meta + (size_t)tnt * TN, TN * 8u, mfull(ms));
           }
+          __syncwarp();
+          ++mcount;
+        };
+        if constexpr (TOPK)
+          for (uint32_t j = nt0; j < min(nt1, nt0 + kMetaAhead); ++j) issue_meta(j);
+        for (uint32_t nt = nt0; nt < nt1; ++nt) {
+          if constexpr (TOPK)
+            if (nt + kMetaAhead < nt1) issue_meta(nt + kMetaAhead);
           for (uint32_t kc = 0; kc < p.nk; ++kc) {
             BSK_T0(tw2);
             tc::mbar_wait(empty(stage), phase ^ 1u);
@@ -761,9 +773,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       epi_bar();
       // threshold of this row as published by any group (a valid lower bound of the current one)
-      auto refresh = [&]() {
+      auto refresh = [&]() {   // (volatile shared loads issue in program order: key, then index)
         cnt = cnt_s[rt];
-        if (cnt >= K) { T = Tp[rt]; __threadfence_block(); Ti = Tip[rt]; }
+        if (cnt >= K) { T = Tp[rt]; Ti = Tip[rt]; }
       };
       refresh();
       auto sift_down = [&](uint32_t i) {
@@ -829,7 +841,11 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       double c_T = 0.0;
       auto tile_pmin = [&](uint32_t lo, uint32_t hi_) -> uint32_t {
         if (!filt || cnt < K || lo == 0) return 0u;
+#ifdef BSK_PMIN_STALE
+        if (lo == c_lo && hi_ == c_hi) return c_pmin;   // dev A/B: a stale (lower) threshold is conservative
+#else
         if (lo == c_lo && hi_ == c_hi && T == c_T) return c_pmin;   // sorted db: runs of equal ranges
+#endif
         const double g = T - 1e-9 * fmax(1.0, fabs(T));
         const uint32_t pmax = min((uint32_t)pa, hi_);
         const double Llo = Ls[lo];
@@ -847,7 +863,19 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // q0 is a lower bound of the exact answer (the fp32 error of pr is < 0.01, far below the
         // 2-step margin), so only the upward refinement is needed
         uint32_t qq = q0 <= 0.0f ? 0u : min((uint32_t)q0, pmax);
-        while (qq <= pmax && key_bound(qq, lo, hi_) < g) ++qq;
+        // refinement, four candidates per step evaluated independently (the answer is
+        // typically within q0 + 3): the first qq with key_bound(qq) >= g
+        for (;;) {
+          bool ok[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) ok[u] = qq + u > pmax || key_bound(qq + u, lo, hi_) >= g;
+          if (ok[0] || ok[1] || ok[2] || ok[3]) {
+            qq += ok[0] ? 0u : (ok[1] ? 1u : (ok[2] ? 2u : 3u));
+            break;
+          }
+          qq += 4;
+        }
+        qq = min(qq, pmax + 1);
         c_lo = lo; c_hi = hi_; c_T = T; c_pmin = qq;
         return qq;
       };
@@ -860,9 +888,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         refresh();
         const uint64_t n0 = (uint64_t)nt * TN;
         // this tile's db popcounts / original indices, bulk-loaded by the producer
-        const uint32_t ms = my & 3u;
-        tc::mbar_wait(mfull(ms), (my >> 2) & 1u);
-        const int2* tm = meta_s + ms * kTcN;
+        const uint32_t ms = my % kMS;
+        tc::mbar_wait(mfull(ms), (my / kMS) & 1u);
+        const int2* tm = meta_s + ms * TN;
         const uint32_t nval = (uint32_t)min((uint64_t)TN, p.nb - n0);
         // the tile's popcount range (the db is popcount-sorted, descending or ascending)
         if (valid) pmin = tile_pmin(min((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x), max((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x));
@@ -994,18 +1022,16 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #else
         if (__any_sync(0xffffffffu, valid && (cnt < K || pmin <= min((uint32_t)pa, tile_hi)))) {
 #endif
-          uint32_t va[32], vb[32];
+          uint32_t va[32];
 #pragma unroll 1
-          for (uint32_t c = 0; c < nval; c += 64) {
+          for (uint32_t c = 0; c < nval; c += 32) {   // one 32-column chunk at a time (register budget)
             tc::tmem_ld32_issue(tb + c, va);
-            tc::tmem_ld32_issue(tb + c + 32, vb);
             tc::tmem_ld_wait(va);
-            tc::tmem_ld_wait(vb);
-            const uint32_t mx = max(max32(va), max32(vb));
-            if (__any_sync(0xffffffffu, valid && mx >= pmin)) {
-              chunk(c, va);
-              chunk(c + 32, vb);
-            }
+#ifdef BSK_EPI_LDONLY
+            if (va[0] == 0xdeadbeefu && va[31] == 0x12345678u) pmin = 0;   // dev: keep the loads, skip the filter
+            continue;
+#endif
+            chunk(c, va);
           }
         }
         release_acc(acc);
@@ -1246,6 +1272,11 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
     }
   }
+#ifdef BSK_TOPK_PROF
+  if (lane == 0)
+    for (int i = 0; i < 9; ++i)
+      if (pacc[i]) atomicAdd(&g_tkstats[6 + i], pacc[i]);
+#endif
   tc::fence_before();
   if constexpr (CG == 1) __syncthreads();
   else tc::cluster_sync();   // no CTA leaves while its peer may still signal its barriers / TMEM
