@@ -37,7 +37,15 @@ import numpy as np  # noqa: E402
 METRIC = "sketch rows/s (HBM GB/s) and estimated pairs/s vs popc roofline, 1xB200"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 SM_COUNT_B200 = 148
-POPC_PER_CLK_SM = 16          # CUDA C++ Programming Guide throughput table (cc 10.x); K9 calibrates
+# K9 (tools/microbench.cu, profiles/r02_microbench_k9.jsonl): POPC per SM clock, median over SMs of
+# ops / busy span by clock64 (clock-independent), median of 3 runs, SM clock verified near max
+# (implied 1942 MHz). The CUDA guide's table value is 16.
+POPC_PER_CLK_SM = 15.11
+POPC_BASIS = "K9 measured 15.11 POPC/clk/SM (profiles/r02_microbench_k9.jsonl) x 148 SMs x SM clock"
+# ncu --set full of the fused top-k kernel at this workload (one launch).
+TOPK_NCU = {"source": "profiles/r02_topk_final_summary.txt", "tensor_pipe_active_pct": 43.4,
+            "issue_active_pct": 20.9, "dram_bytes_per_launch": 2.369e9 + 0.586e9, "kernel_share_of_stage": "98.3 %",
+            "launch_list": "profiles/r02_launches_large_summary.txt"}
 HBM_FALLBACK_GBS = 6650.0     # B200_PROFILING.md fallback
 
 
@@ -317,47 +325,43 @@ def run_ours(args):
     del bufs
 
     # --- roofline of the dominant kernel ---
-    # Default engine: tensor cores (tc_pairs_kernel<kTcTopk>: tcgen05 kind::i8 on {0,1}-byte
-    # operands + fused fp64 top-k epilogue). Algorithmic work = 2 * pairs * N int8 ops (the
-    # K padding to a multiple of 128 is overhead, not credit). Peak = int8 dense = 2 x the
-    # measured bf16 cuBLAS peak (nominal int8/bf16 ratio 4.5/2.25), the sustained figure
-    # because the kernel runs inside a long step. Denominator time = the whole top-k stage
-    # (popcounts + byte expansion + MMA/top-k kernel + merge), so frac is conservative.
+    # Default engine: tensor cores (tc_pairs_kernel, fused top-k: tcgen05 kind::i8 on {0,1}-byte
+    # operands + fp64 top-k epilogue). Algorithmic work = 2 * pairs * N int8 ops (the K padding to
+    # a multiple of 128 is overhead, not credit). Peak = int8 dense = 2 x the measured bf16 cuBLAS
+    # peak (nominal int8 : bf16 = 4.5 : 2.25): the BURST figure, because these steps run ~40 ms at
+    # the maximum SM clock with no power cap (clocks below); the sustained figure (measured
+    # power-capped at 1342 MHz) is printed beside it. Time basis = the whole top-k call (popcounts,
+    # sort, expansion, the kernel, merge), so frac is a lower bound for the kernel itself.
     engine = os.environ.get("BINSKETCH_ENGINE", "tc")
     f_sm = (clocks["sm_mhz"] or pk.get("sm_max_mhz", 1965.0)) * 1e6
-    sm_max = (clocks.get("sm_max_mhz") or pk.get("sm_max_mhz", 1965.0)) * 1e6
-    peak_words = SM_COUNT_B200 * POPC_PER_CLK_SM * sm_max            # word-ops/s at max clock
+    peak_words = SM_COUNT_B200 * POPC_PER_CLK_SM * f_sm              # word-ops/s at the measured clock
     achieved_words = pairs_per_step * W * args.steps / t_topk
     popc = {"achieved": achieved_words / 1e12, "peak": peak_words / 1e12, "unit": "Tword-popc/s",
-            "frac": achieved_words / peak_words,
-            "peak_basis": f"148 SMs x {POPC_PER_CLK_SM} POPC/clk/SM x sm_max_mhz (guide table; DESIGN.md)"}
+            "frac": achieved_words / peak_words, "peak_basis": POPC_BASIS + " (measured during this run)"}
+    burst = 2.0 * pk.get("bf16_tflops", 1590.0)
+    sust = 2.0 * pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1590.0))
+    ach = 2.0 * pairs_per_step * N * args.steps / t_topk / 1e12
+    tc_common = {"achieved": ach, "peak": burst, "unit": "TOPS (int8)", "frac": ach / burst,
+                 "peak_basis": "2 x MEASURED_PEAKS bf16_tflops (burst; nominal int8:bf16 = 2:1)",
+                 "peak_sustained": sust, "frac_of_sustained": ach / sust,
+                 "peak_sustained_basis": "2 x MEASURED_PEAKS bf16_tflops_sustained (power-capped, 1342 MHz)",
+                 "traffic": None, "popc_equivalent": popc}
     if engine != "cuda" and k <= 64 and N <= 6143:
-        int8_peak = 2.0 * pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1590.0))
-        ach = 2.0 * pairs_per_step * N * args.steps / t_topk / 1e12
-        roofline = {"bound": "tensor", "kernel": "tc_pairs_kernel<kTcTopk> (tcgen05.mma kind::i8 + fused top-k)",
-                    "achieved": ach, "peak": int8_peak, "unit": "TOPS (int8)", "frac": ach / int8_peak,
-                    "peak_basis": "2 x MEASURED_PEAKS bf16_tflops_sustained (nominal int8:bf16 = 2:1)",
-                    "time_basis": "whole top-k stage (expand + popcount + MMA/top-k + merge; the kernel is 98.6 % "
-                                  "of it in profiles/r01_k10b/launches_large_v8_summary.txt)",
-                    "traffic": None, "popc_equivalent": popc}
+        roofline = {"bound": "tensor", "kernel": "tc_pairs_kernel (tcgen05.mma kind::i8, query tile in TMEM + fused top-k)",
+                    **tc_common,
+                    "time_basis": "whole top-k call (popcount + sort + expand + fused kernel + merge); the kernel's "
+                                  "share of it: " + str(TOPK_NCU["kernel_share_of_stage"]) + " (" + TOPK_NCU["launch_list"] + ")"}
         if args.workload == "large":
-            # DRAM bytes of one launch of this kernel at this workload, from `ncu --set full`
-            # (profiles/r01_tc_topk_large_v8_summary.txt: 4.076 GB read + 0.589 GB written); the
-            # contraction reads its operands from L2 (hit rate ~98 %), so this is not its bound
-            roofline["traffic"] = 4.0755e9 + 0.5891e9
-            roofline["traffic_unit"] = "DRAM bytes per launch (ncu)"
+            roofline["ncu"] = {k_: v for k_, v in TOPK_NCU.items() if k_ != "dram_bytes_per_launch"}
+            roofline["traffic"] = TOPK_NCU["dram_bytes_per_launch"]
+            roofline["traffic_unit"] = "DRAM bytes per launch (ncu; operands are L2-resident)"
     elif engine != "cuda":
-        int8_peak = 2.0 * pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1590.0))
-        ach = 2.0 * pairs_per_step * N * args.steps / t_topk / 1e12
-        roofline = {"bound": "tensor", "kernel": "tc_pairs_kernel<kTcAndPopc> -> pab table -> topk_kernel<FROMPAB>",
-                    "achieved": ach, "peak": int8_peak, "unit": "TOPS (int8)", "frac": ach / int8_peak,
-                    "peak_basis": "2 x MEASURED_PEAKS bf16_tflops_sustained (nominal int8:bf16 = 2:1)",
-                    "time_basis": "whole top-k stage (expand + tensor-core AND-popcount + threshold top-k + merge)",
-                    "traffic": None, "popc_equivalent": popc}
+        roofline = {"bound": "tensor", "kernel": "tc_pairs_kernel<kTcAndPopc> -> pab table -> topk_pab_kernel",
+                    **tc_common,
+                    "time_basis": "whole top-k call (expand + tensor-core AND-popcount + threshold top-k + merge)"}
     else:
         roofline = {"bound": "alu", "kernel": "topk_kernel (LOP3+POPC mainloop + fp64 epilogue)",
                     "achieved": popc["achieved"], "peak": popc["peak"], "unit": "Tword-popc/s", "frac": popc["frac"],
-                    "frac_at_measured_clock": achieved_words / (SM_COUNT_B200 * POPC_PER_CLK_SM * f_sm),
                     "peak_basis": popc["peak_basis"], "traffic": None}
 
     result = {
@@ -378,7 +382,8 @@ def run_ours(args):
     if rank == 0 and not args.no_extras and args.workload == "large":
         result["build"] = bench_buildonly(args, bs, torch, pk, pk_src)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(args, w, ip_h, ix_h, qp_h, qx_h)
+        gpu_idx = out_idx.cpu().numpy()
+        result["cpu_baseline"], result["parity"] = cpu_baseline(args, w, ip_h, ix_h, qp_h, qx_h, gpu_idx)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -446,15 +451,73 @@ def _oracle_sample_step(w, ip_h, ix_h, qp_h, qx_h, nsample, nthreads):
     return nsample * D.shape[0]
 
 
-def cpu_baseline(args, w, ip_h, ix_h, qp_h, qx_h):
-    nthreads = os.cpu_count() or 1
-    nsample = {"large": 2000, "ranking": 200, "tiny": 1000}[args.workload]
-    t0 = time.perf_counter()
-    pairs = _oracle_sample_step(w, ip_h, ix_h, qp_h, qx_h, nsample, nthreads)
-    t = time.perf_counter() - t0
-    return {"value": pairs / t, "unit": "pairs/s", "cores": nthreads, "kind": "oracle",
-            "sample": f"oracle (oracle/oracle.cpp, OpenMP) on the same workload: pi + all {len(ip_h) - 1} sketches "
-                      f"+ top-{w['k']} for {nsample} query rows vs all db rows; {t:.1f} s"}
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _omp_threads(n):
+    """Thread count of the oracle's OpenMP runtime (libgomp is shared with liboracle.so)."""
+    import ctypes
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+        return True
+    except OSError:
+        return False
+
+
+def cpu_baseline(args, w, ip_h, ix_h, qp_h, qx_h, gpu_idx):
+    """The CPU oracle (as it stands, never tuned) on the GPU box's host cores, bounded samples of
+    the same workload: top-k pairs/s all cores and one thread, sketch rows/s all cores and one
+    thread, median of 3 each. The all-core top-k lists double as the in-run parity check of the
+    GPU's lists for the same query rows (this leg is the one place the bench may run the oracle)."""
+    import oracle
+    import synth
+    N, d, k, m = w["N"], w["db"].d, w["k"], w["measure"]
+    cores = os.cpu_count() or 1
+    nq_all = {"large": 1000, "ranking": 100, "tiny": 1000}[args.workload]
+    nq_one = {"large": 50, "ranking": 5, "tiny": 100}[args.workload]
+    pi = oracle.make_pi(synth.PI_SEED, d, N)
+
+    def timed(fn, reps=3):
+        ts, out = [], None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            out = fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts), out
+
+    _omp_threads(cores)
+    t_sk, (D, _) = timed(lambda: oracle.sketch(pi, d, N, ip_h, ix_h))   # orc_sketch is sequential
+    if qp_h is not None:
+        Q, _ = oracle.sketch(pi, d, N, qp_h, qx_h)
+        excl = False
+    else:
+        Q, excl = D, w["exclude_self"]
+    ndb = D.shape[0]
+    t_all, (ri, _) = timed(lambda: oracle.topk(Q[:nq_all], D, N, d, m, k, exclude_self=excl, nthreads=cores))
+    t_one, _ = timed(lambda: oracle.topk(Q[:nq_one], D, N, d, m, k, exclude_self=excl, nthreads=1))
+    rows = len(ip_h) - 1
+    g = gpu_idx if gpu_idx.ndim == 2 else gpu_idx[0]          # first measure's plane
+    same = int(np.sum(np.all(g[:nq_all] == ri, axis=1)))
+    parity = {"kind": f"top-{k} index lists of query rows 0..{nq_all - 1} (of {g.shape[0]}) from the last timed "
+                      "step vs the CPU oracle, bit-exact, ties to the lower index",
+              "rows": nq_all, "identical_rows": same, "ok": same == nq_all,
+              "full_check": "profiles/r02_parity_large_full.log" if args.workload == "large" else None}
+    base = {"value": nq_all * ndb / t_all, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+            "cpu_model": _cpu_model(), "repeats": 3, "statistic": "median",
+            "single_thread": {"value": nq_one * ndb / t_one, "unit": "pairs/s", "cores": 1},
+            "build_rows_per_s": {"value": rows / t_sk, "cores": 1,
+                                 "sample": f"oracle sketch of all {rows} rows of this workload's CSR (N={N}); "
+                                           "the oracle's sketch loop is sequential (oracle.cpp orc_sketch)"},
+            "sample": f"oracle (oracle/oracle.cpp, OpenMP): top-{k} of {nq_all} query rows vs all {ndb} db rows "
+                      f"({cores} threads) and of {nq_one} rows (1 thread); median of 3 each"}
+    return base, parity
 
 
 # -------------------------------------------------------- reference arm ---

@@ -70,6 +70,14 @@ enum { BINSKETCH_MAX_THRESHOLDS = 16 };    /* thresholds per binsketch_join call
 
 enum { BINSKETCH_MAX_K = 256 };            /* largest k binsketch_topk accepts */
 
+/* Largest sketch length N accepted (larger values return BINSKETCH_EUNSUPPORTED):
+ * construction and popcounts (make_pi, build*, bcs_build*, popcount) take every N >= 2 (their
+ * sizes are computed in 64 bits; rows wider than 4096 words use a global-atomic fallback);
+ * everything that stages the (N+1)-entry cardinality table (andpopc, estimate, topk, join*,
+ * bcs_*, mse, categorical_estimate, card_table, workspace_bytes) up to 2^24 bits. */
+#define BINSKETCH_MAX_N_BUILD 0xFFFFFFFFu
+#define BINSKETCH_MAX_N_PAIRS 0x01000000u
+
 /* ops for binsketch_workspace_bytes */
 enum { BINSKETCH_OP_ANDPOPC = 1, BINSKETCH_OP_ESTIMATE = 2, BINSKETCH_OP_TOPK = 3, BINSKETCH_OP_JOIN = 4,
        BINSKETCH_OP_JOIN_LIST = 5, BINSKETCH_OP_BCS_ESTIMATE = 6,
@@ -291,7 +299,8 @@ binsketch_status binsketch_card_table(uint32_t N, uint64_t d, double* host_out);
 
 /* Synchronises `stream`, returns BINSKETCH_EINDEX if a device-side input
  * error was latched since the last call (and clears it), ECUDA on a CUDA
- * error, else OK. */
+ * error, else OK. The status word is per device: this reports (and clears)
+ * the errors of calls made while the current CUDA device was the same. */
 binsketch_status binsketch_device_status(binsketch_stream_t stream);
 
 /* Number of kernels this library has enqueued since it was loaded (all

@@ -3,7 +3,7 @@
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
 ``cpu_baseline`` / ``--impl reference`` legs may import this package. The
 product path (``paper_1910_04658_b200``) must never import it, and shares no
-code with it (tests/test_independence.py checks this).
+code with it (tests/test_abi_host.py::test_product_shares_no_code_with_oracle checks this).
 
 ``liboracle.so`` is built from ``oracle.cpp`` (plain C++17, fp64, no FMA
 contraction, OpenMP over rows). ``definitional.py`` is the per-bit

@@ -412,12 +412,19 @@ def topk_from_host_csr(db_indptr_h: torch.Tensor, db_indices_h: torch.Tensor, pi
     """Host (pinned) CSR in, host top-k lists out, through the C ABI: H2D of the db CSR (and of a
     separate query CSR, if given) and pi -> binsketch_build -> binsketch_topk per measure -> D2H of
     every (idx, score) list. Without a query CSR the db rows are the queries (self-join).
+    `measures` (an int bit mask or an iterable of measure bits) is deduplicated; with several
+    measures the output planes are stacked in bit order IP, HAM, JS, COS (as binsketch_topk
+    writes them), whatever order the caller listed them in.
     Returns ((idx_host, score_host) — [measure][nq][k] for several measures —, h2d_bytes, d2h_bytes)."""
     b = bufs if bufs is not None else {}
     n = db_indptr_h.numel() - 1
     sep = q_indptr_h is not None
     nq = (q_indptr_h.numel() - 1) if sep else n
-    ms = list(measures)
+    bits = measures if isinstance(measures, int) else 0
+    if not isinstance(measures, int):
+        for m in measures:
+            bits |= int(m)
+    ms = [m for m in (IP, HAM, JS, COS) if bits & m]
     if "db_ip" not in b:
         b["db_ip"] = torch.empty_like(db_indptr_h, device="cuda")
         b["db_ix"] = torch.empty_like(db_indices_h, device="cuda")

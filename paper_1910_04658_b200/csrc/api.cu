@@ -105,7 +105,7 @@ bool engine_tc() {
 }
 bool use_tc(int op, uint32_t N, uint32_t k = 0) {
   if (engine_cuda()) return false;
-  if (op == BINSKETCH_OP_TOPK) return k <= bsk::tc_topk_max_k() && N <= bsk::tc_topk_max_n();
+  if (op == BINSKETCH_OP_TOPK) return k <= bsk::tc_topk_max_k() && N <= bsk::tc_topk_max_n() && bsk::tc_topk_fits(N, k);
   // all-pairs estimate: the epilogue (fp64 recipe, 16 B of planes per pair) dominates; at W <= 32
   // the CUDA-core kernel's 32 POPCs per pair are cheaper than the tensor-core pipeline around it
   // (Medium, 1e8 pairs x 4 planes: N = 1000 1.28 vs 1.49 ms; N = 2000 1.87 vs 1.56 ms)
@@ -241,6 +241,7 @@ uint32_t binsketch_recommended_N(uint32_t psi, double rho) {
 
 binsketch_status binsketch_make_pi(uint64_t seed, uint64_t d, uint32_t N, uint32_t* pi, binsketch_stream_t stream) {
   if (N < 2 || (d > 0 && pi == nullptr)) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_BUILD) return BINSKETCH_EUNSUPPORTED;
   return cuda_status(bsk::launch_make_pi(seed, d, N, pi, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -248,6 +249,7 @@ static binsketch_status build_common(const uint32_t* pi, uint64_t seed, uint64_t
                                      const int64_t* indptr, const int32_t* indices, uint64_t n,
                                      uint32_t* out, binsketch_stream_t stream, bool parity = false) {
   if (N < 2) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_BUILD) return BINSKETCH_EUNSUPPORTED;
   if (n == 0) return BINSKETCH_OK;
   if (d == 0 || indptr == nullptr || indices == nullptr || out == nullptr) return BINSKETCH_EINVAL;
   if (d > 0x80000000ull) return BINSKETCH_EINVAL;  // int32 indices cannot address more
@@ -285,18 +287,21 @@ binsketch_status binsketch_bcs_build_seeded(uint64_t seed, uint64_t d, uint32_t 
 binsketch_status binsketch_popcount(const uint32_t* sk, uint64_t n, uint32_t N, int32_t* out,
                                     binsketch_stream_t stream) {
   if (N < 2) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_BUILD) return BINSKETCH_EUNSUPPORTED;
   if (n == 0) return BINSKETCH_OK;
   if (!sk || !out) return BINSKETCH_EINVAL;
   return cuda_status(bsk::launch_popcount(sk, n, binsketch_words(N), out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 size_t binsketch_workspace_bytes(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
+  if (N < 2 || N > BINSKETCH_MAX_N_PAIRS) return 0;
   return layout(op, na, nb, N, k).total;
 }
 
 binsketch_status binsketch_andpopc(const uint32_t* A, uint64_t na, const uint32_t* B, uint64_t nb, uint32_t N,
                                    int32_t* out, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
   if (N < 2) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   if (na == 0 || nb == 0) return BINSKETCH_OK;
   if (!A || !B || !out) return BINSKETCH_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -334,6 +339,7 @@ binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, con
                                     uint64_t nb, uint32_t N, uint64_t d, uint32_t measure, float* out, void* ws,
                                     size_t ws_bytes, binsketch_stream_t stream) {
   if (N < 2 || measure == 0 || (measure & ~15u)) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   if (na == 0 || nb == 0) return BINSKETCH_OK;
   if (!sketches_a || !sketches_b || !out || d == 0) return BINSKETCH_EINVAL;
   const Layout l = layout(BINSKETCH_OP_ESTIMATE, na, nb, N, 0);
@@ -371,6 +377,7 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
                                 uint64_t d, uint32_t measure, uint32_t k, uint32_t flags, int32_t* out_idx,
                                 float* out_score, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
   if (N < 2 || measure == 0 || (measure & ~15u) || (flags & ~1u)) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   if (nq == 0 || k == 0) return BINSKETCH_OK;
   if (k > BINSKETCH_MAX_K) return BINSKETCH_EUNSUPPORTED;
   if (!queries || !out_idx || !out_score || d == 0 || (ndb > 0 && !db)) return BINSKETCH_EINVAL;
@@ -457,6 +464,7 @@ binsketch_status binsketch_join(const uint32_t* queries, uint64_t nq, const uint
                                 uint64_t d, uint32_t measure, const double* thresholds, uint32_t nthr, uint32_t flags,
                                 uint32_t* out_bits, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
   if (N < 2 || !one_bit(measure) || (flags & ~3u)) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   if (nthr == 0 || nthr > BINSKETCH_MAX_THRESHOLDS || !thresholds) return BINSKETCH_EINVAL;
   for (uint32_t t = 0; t < nthr; ++t)
     if (std::isnan(thresholds[t])) return BINSKETCH_EINVAL;
@@ -503,6 +511,7 @@ binsketch_status binsketch_join_list(const uint32_t* bits, const uint32_t* queri
                                      int64_t* row_ptr, int32_t* out_j, float* out_score, uint64_t capacity, void* ws,
                                      size_t ws_bytes, binsketch_stream_t stream) {
   if (N < 2 || !one_bit(measure) || (flags & ~3u)) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   if (nq == 0) return BINSKETCH_OK;
   const bool exact = (flags & BINSKETCH_JOIN_EXACT) != 0;
   if (!row_ptr || (ndb > 0 && !bits)) return BINSKETCH_EINVAL;
@@ -541,6 +550,7 @@ binsketch_status binsketch_bcs_estimate(const uint32_t* sketches_a, uint64_t na,
                                         uint64_t nb, uint32_t N, uint64_t d, uint32_t measure, float* out, void* ws,
                                         size_t ws_bytes, binsketch_stream_t stream) {
   if (N < 2 || measure == 0 || (measure & ~15u)) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   if (na == 0 || nb == 0) return BINSKETCH_OK;
   if (!sketches_a || !sketches_b || !out || d == 0) return BINSKETCH_EINVAL;
   const Layout l = layout(BINSKETCH_OP_BCS_ESTIMATE, na, nb, N, 0);
@@ -571,6 +581,7 @@ binsketch_status binsketch_bcs_estimate(const uint32_t* sketches_a, uint64_t na,
 
 binsketch_status binsketch_bcs_table(uint32_t N, uint64_t d, double* host_out) {
   if (N < 2 || !host_out) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   const double* t = cache().get(N, d, 1);
   if (!t) return BINSKETCH_ECUDA;
   for (uint32_t k = 0; k <= N; ++k) host_out[k] = t[k];
@@ -582,6 +593,7 @@ binsketch_status binsketch_mse(const uint32_t* sketches, const uint32_t* exact, 
                                double* out_sse, uint64_t* out_count, void* ws, size_t ws_bytes,
                                binsketch_stream_t stream) {
   if (N < 2 || !one_bit(measure) || (flags & ~1u) || d == 0) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   if (nthr == 0 || nthr > BINSKETCH_MAX_THRESHOLDS || !thresholds || !out_sse || !out_count) return BINSKETCH_EINVAL;
   for (uint32_t t = 0; t < nthr; ++t)
     if (std::isnan(thresholds[t])) return BINSKETCH_EINVAL;
@@ -638,6 +650,7 @@ binsketch_status binsketch_categorical_estimate(const uint32_t* sketches_a, uint
                                                 uint64_t nb, uint32_t N, uint64_t d, float* out, void* ws,
                                                 size_t ws_bytes, binsketch_stream_t stream) {
   if (N < 2) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   if (na == 0 || nb == 0) return BINSKETCH_OK;
   if (!sketches_a || !sketches_b || !out || d == 0) return BINSKETCH_EINVAL;
   const Layout l = layout(BINSKETCH_OP_BCS_ESTIMATE, na, nb, N, 0);   // the tensor-core estimate layout
@@ -668,6 +681,7 @@ binsketch_status binsketch_categorical_estimate(const uint32_t* sketches_a, uint
 
 binsketch_status binsketch_card_table(uint32_t N, uint64_t d, double* host_out) {
   if (N < 2 || !host_out) return BINSKETCH_EINVAL;
+  if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   const double* t = cache().get(N, d);
   if (!t) return BINSKETCH_ECUDA;
   for (uint32_t k = 0; k <= N; ++k) host_out[k] = t[k];

@@ -83,6 +83,7 @@ cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8
 // the integer L[pab] bound (valid when L is non-decreasing and convex).
 uint32_t tc_topk_max_k();
 uint32_t tc_topk_max_n();
+bool tc_topk_fits(uint32_t N, uint32_t k);   // the fused kernel's shared memory fits (>= 2 stages)
 uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t N, uint32_t k);   // partial lists per query
 // db order: counting sort by popcount, descending (perm: sorted position -> db row; spb:
 // sorted popcounts; bins: N+1 words of scratch). Top-k uses it for N <= 65536 (tc_sortable).

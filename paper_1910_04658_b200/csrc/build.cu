@@ -36,12 +36,21 @@ static std::atomic<uint64_t> g_launches{0};
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+// The latched status word of the CURRENT device (a __device__ variable has one instance per
+// device): its address is cached per device ordinal; racing first calls store the same value.
 unsigned int* status_ptr() {
-  static unsigned int* p = nullptr;
-  if (!p) {
-    void* v = nullptr;
-    if (cudaGetSymbolAddress(&v, g_status) == cudaSuccess) p = static_cast<unsigned int*>(v);
+  constexpr int kMaxDev = 64;
+  static std::atomic<unsigned int*> cache[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (dev >= 0 && dev < kMaxDev) {
+    unsigned int* p = cache[dev].load(std::memory_order_acquire);
+    if (p) return p;
   }
+  void* v = nullptr;
+  if (cudaGetSymbolAddress(&v, g_status) != cudaSuccess) return nullptr;
+  unsigned int* p = static_cast<unsigned int*>(v);
+  if (dev >= 0 && dev < kMaxDev) cache[dev].store(p, std::memory_order_release);
   return p;
 }
 

@@ -1472,6 +1472,29 @@ cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8
                                     p.l_smem + TcRoles<kTcEstimate>::kEpi * 4 * 4 * 32 * (TcRoles<kTcEstimate>::kCW + 1), 0, s);   // table + 4-plane transposes
 }
 
+// The fused top-k keeps the query tile in TMEM (kTcTopkT) when its widened rows fit 256 columns;
+// BINSKETCH_TC_ATM=0 forces the shared-memory A operand (dev A/B).
+static bool tc_topk_atm(uint32_t N) {
+  if (const char* e = std::getenv("BINSKETCH_TC_ATM")) if (!std::strcmp(e, "0")) return false;
+  return tc_kpad(N) <= 1024u;
+}
+static uint32_t tc_topk_tn(uint32_t N) { return tc_topk_atm(N) ? 128u : (uint32_t)kTcN; }
+
+// Shared memory of the fused top-k besides the operand stages: per-row heaps (k x 128 x 12 B),
+// per-group scratch, metadata ring, per-warp queues / candidates / owner masks, row state; and
+// the staged cardinality table.
+static uint32_t topk_heap_smem(uint32_t N, uint32_t k) {
+  const uint32_t ne = tc_topk_atm(N) ? TcRoles<kTcTopkT>::kEpi : TcRoles<kTcTopk>::kEpi;
+  return k * kTcM * 12 + (ne / 4) * 32 * kTcM * 4 + 4 * kTcN * 8 + ne * 256 * 8 + ne * 32 * 16 + ne * 32 * 4 + kTcM * 20;
+}
+static uint32_t topk_table_smem(uint32_t N) { return (uint32_t)((((uint64_t)N + 1) * 8 + 15) / 16 * 16); }
+
+bool tc_topk_fits(uint32_t N, uint32_t k) {
+  if (k > tc_topk_max_k() || N > tc_topk_max_n()) return false;
+  const uint64_t stage = tc_topk_atm(N) ? 128ull * 128 : (uint64_t)TcGeom<64, 1>::kStageBytes;
+  return 2048ull + topk_heap_smem(N, k) + topk_table_smem(N) + 2 * stage <= kTcSmemMax;
+}
+
 uint32_t tc_topk_max_k() { return 64; }
 
 uint32_t tc_topk_max_n() { return 6143; }   // cardinality table (N+1 doubles) staged in shared memory
@@ -1491,13 +1514,6 @@ cudaError_t launch_sort_by_popcount(const int32_t* pb, uint64_t n, uint32_t N, u
   return cudaGetLastError();
 }
 
-// The fused top-k keeps the query tile in TMEM (kTcTopkT) when its widened rows fit 256 columns;
-// BINSKETCH_TC_ATM=0 forces the shared-memory A operand (dev A/B).
-static bool tc_topk_atm(uint32_t N) {
-  if (const char* e = std::getenv("BINSKETCH_TC_ATM")) if (!std::strcmp(e, "0")) return false;
-  return tc_kpad(N) <= 1024u;
-}
-static uint32_t tc_topk_tn(uint32_t N) { return tc_topk_atm(N) ? 128u : (uint32_t)kTcN; }
 
 uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t N, uint32_t k) {
   // partial lists per query in the workspace: 1 when the heaps are chained, else one per chunk
@@ -1519,12 +1535,10 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
   p.lc = std::log1p(-1.0 / (double)N);
   p.prefilter = (prefilter && perm) ? 1u : 0u;   // the per-tile bound needs the popcount-sorted db
   p.part_key = part_key; p.part_idx = part_idx;
-  // heaps, per-group scratch, metadata ring, per-warp queues / candidates / owner masks, row state
   const bool atm = tc_topk_atm(N);
-  const uint32_t ne = atm ? TcRoles<kTcTopkT>::kEpi : TcRoles<kTcTopk>::kEpi;
-  p.heap_smem = k * kTcM * 12 + (ne / 4) * 32 * kTcM * 4 + 4 * kTcN * 8 + ne * 256 * 8 + ne * 32 * 16 + ne * 32 * 4 + kTcM * 20;
-  const uint32_t lb = ((N + 1) * 8 + 15) / 16 * 16;
-  if (lb > 48 * 1024) return cudaErrorInvalidValue;   // caller keeps N <= tc_topk_max_n()
+  p.heap_smem = topk_heap_smem(N, k);
+  const uint32_t lb = topk_table_smem(N);
+  if (!tc_topk_fits(N, k)) return cudaErrorInvalidValue;   // the caller routes by tc_topk_fits
   p.l_topk_smem = lb;
   // splits computed with the device-independent rule (148) so the workspace matches
   const TcSplit sc = tc_split_rule(nq, ndb, N, true, k, tc_topk_tn(N));

@@ -148,6 +148,29 @@ def test_host_detected_errors(lib):
     assert lib.binsketch_join_confusion(None, None, 3, 5, vp(8), None) == EINVAL
 
 
+def test_size_limits(lib):
+    """N beyond the documented limits (binsketch.h BINSKETCH_MAX_N_*) is refused on the host with
+    EUNSUPPORTED, before any size arithmetic that could wrap."""
+    vp, u64, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32
+    EUNSUP = 5
+    big_pairs = 0x01000001
+    lib.binsketch_make_pi.argtypes = [u64, u64, u32, vp, vp]
+    assert lib.binsketch_make_pi(0, 0, 0xFFFFFFFF, None, None) == 0     # construction: every N (d = 0: no-op)
+    lib.binsketch_words.restype = u32
+    assert lib.binsketch_words(0xFFFFFFFF) == 0x08000000                # no 32-bit wrap
+    lib.binsketch_estimate.argtypes = [vp, u64, vp, u64, u32, u64, u32, vp, vp, ctypes.c_size_t, vp]
+    assert lib.binsketch_estimate(vp(8), 4, vp(8), 4, big_pairs, 10, 1, vp(8), vp(8), 0, None) == EUNSUP
+    lib.binsketch_topk.argtypes = [vp, u64, vp, u64, u32, u64, u32, u32, u32, vp, vp, vp, ctypes.c_size_t, vp]
+    assert lib.binsketch_topk(vp(8), 4, vp(8), 4, big_pairs, 10, 1, 5, 0, vp(8), vp(8), vp(8), 0, None) == EUNSUP
+    lib.binsketch_card_table.argtypes = [u32, u64, vp]
+    dummy = np.empty(1, dtype=np.float64)
+    assert lib.binsketch_card_table(big_pairs, 10, dummy.ctypes.data) == EUNSUP
+    lib.binsketch_workspace_bytes.restype = ctypes.c_size_t
+    lib.binsketch_workspace_bytes.argtypes = [ctypes.c_int, u64, u64, u32, u32]
+    assert lib.binsketch_workspace_bytes(2, 10, 10, big_pairs, 0) == 0
+    assert lib.binsketch_workspace_bytes(2, 10, 10, 0x01000000, 0) > 0            # the limit itself is accepted
+
+
 def test_product_shares_no_code_with_oracle():
     pkg = os.path.join(ROOT, "paper_1910_04658_b200")
     for dirpath, _, files in os.walk(pkg):

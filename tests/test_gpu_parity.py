@@ -445,3 +445,41 @@ def test_topk_pab_single_split_direct_outputs(measure, monkeypatch):
     D[40:60] = D[3]
     Q = _sketches(synth.scaled(synth.RANKING_Q, 4000, seed=58), N)
     _check_topk(Q, D, N, d, measure, 100)
+
+
+@pytest.mark.parametrize("N", [1024, 1025, 5600, 5700, 6143])
+def test_topk_k64_shared_memory_boundary(N):
+    """k = 64 across the fused kernel's shared-memory limit: N = 1024 keeps the query
+    tile in TMEM, N = 1025 / 5600 stage it in shared memory, and N = 5700 / 6143 no longer fit
+    (heaps + staged table + two stages > 227 KB) and are routed to the pab-table path: every case
+    returns the oracle's lists."""
+    d = 60_000
+    spec = synth.CSRSpec(n=700, d=d, kind=1, p1=120, p2=1.0, cap=900, zipf_s=1.1, seed=61)
+    D = _sketches(spec, N)
+    D[200:230] = D[9]
+    Q = D[:170].copy()
+    _check_topk(Q, D, N, d, 1, 64, exclude_self=True)
+    _check_topk(Q, D, N, d, 8, 64)
+
+
+def test_topk_from_host_csr_measure_order():
+    """topk_from_host_csr (the e2e call): measures deduplicated and stacked in IP, HAM, JS, COS
+    order whatever order the caller lists them in; lists identical to the oracle's."""
+    spec = synth.scaled(synth.RANKING_DB, 900, seed=63)
+    qspec = synth.scaled(synth.RANKING_Q, 60, seed=64)
+    N, d, k = synth.RANKING_N, spec.d, 30
+    ip, ix = synth.make_csr(spec)
+    qp, qx = synth.make_csr(qspec)
+    pi = oracle.make_pi(synth.PI_SEED, d, N)
+    (gi, gs), h2d, d2h = bs.topk_from_host_csr(torch.from_numpy(ip).pin_memory(), torch.from_numpy(ix).pin_memory(),
+                                               torch.from_numpy(pi.view(np.int32)).pin_memory(), d, N,
+                                               [bs.COS, bs.JS, bs.COS], k, q_indptr_h=torch.from_numpy(qp).pin_memory(),
+                                               q_indices_h=torch.from_numpy(qx).pin_memory())
+    torch.cuda.synchronize()
+    assert gi.shape == (2, 60, k) and d2h == 2 * 60 * k * 8
+    D, _ = oracle.sketch(pi, d, N, ip, ix)
+    Q, _ = oracle.sketch(pi, d, N, qp, qx)
+    for t, m in enumerate((4, 8)):          # JS plane first, then COS
+        ri, rs = oracle.topk(Q, D, N, d, m, k)
+        assert np.array_equal(gi[t].numpy(), ri)
+        assert_est_close(gs[t].numpy(), rs)
