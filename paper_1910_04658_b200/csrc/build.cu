@@ -809,8 +809,8 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
     if (!std::strcmp(f, "smem16") && N <= 65536 && smem16_bytes + 64 * 1024 <= (uint64_t)smem_optin) mode = kPiSmem16;
   }
   // compiled-in sketch widths: the configs' N = 1024 (W = 32) and 4096 (W = 128); the BCS
-  // parity variant is instantiated for the generic width only
-  const int logn = parity ? 0 : (N == 1024 ? 10 : (N == 4096 ? 12 : 0));
+  // parity variant for N = 1024 and the generic width
+  const int logn = N == 1024 ? 10 : ((N == 4096 && !parity) ? 12 : 0);
   const uint64_t Wb = 4 * W64;
 
   // Shared memory per block: [pi] [align slack] [rings: nwarps x RR x Wb] [aux: nwarps x (stages + bitmap + mbar)]
@@ -858,7 +858,8 @@ cudaError_t launch_build(const uint32_t* pi, uint64_t seed, uint64_t d, uint32_t
   } while (0)
 #define BSK_LAUNCH_BUILD(M)                                   \
   do {                                                        \
-    if (logn == 10) BSK_LAUNCH_BUILD3(M, 10, false);          \
+    if (logn == 10 && parity) BSK_LAUNCH_BUILD3(M, 10, true); \
+    else if (logn == 10) BSK_LAUNCH_BUILD3(M, 10, false);     \
     else if (logn == 12) BSK_LAUNCH_BUILD3(M, 12, false);     \
     else if (parity) BSK_LAUNCH_BUILD3(M, 0, true);           \
     else BSK_LAUNCH_BUILD3(M, 0, false);                      \

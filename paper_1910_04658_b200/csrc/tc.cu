@@ -55,6 +55,15 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done;
   do {
+#ifdef BSK_MBAR_NOHINT
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
@@ -62,6 +71,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "=r"(done)
         : "r"(bar), "r"(parity), "r"(0x100000u)   // suspend-time hint (ns): sleep, do not spin
         : "memory");
+#endif
   } while (!done);
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t x, int32_t y, uint32_t bar) {
@@ -1342,11 +1352,15 @@ cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* o
 struct TcSplit { uint32_t splits, chain; };
 static TcSplit tc_split_rule(uint64_t na, uint64_t nb, uint32_t N, bool topk, uint32_t k = 0, uint32_t tn = kTcN) {
   const uint64_t tiles_n = (nb + tn - 1) / tn, mtiles = (na + kTcM - 1) / kTcM, sms = 148;
-  const uint64_t chunk_bytes = 40ull << 20;
+  uint64_t chunk_bytes = 40ull << 20;
+  // dev knobs (sanitizer / A-B runs on small shapes): db chunk size in KB, forced heap chaining.
+  // Read here only, so workspace sizing and the launch always agree.
+  if (const char* e = std::getenv("BINSKETCH_TC_CHUNK_KB")) chunk_bytes = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 10;
   uint64_t s_l2 = (nb * tc_kpad(N) + chunk_bytes - 1) / chunk_bytes;
   uint64_t s_par = (2 * sms + mtiles - 1) / mtiles;
   TcSplit r;
   r.chain = (topk && mtiles >= 2 * sms) ? 1u : 0u;
+  if (const char* e = std::getenv("BINSKETCH_TC_CHAIN")) if (topk && !std::strcmp(e, "1")) r.chain = 1u;
   uint64_t splits = r.chain ? s_l2 : std::max(s_l2, s_par);
   if (topk && !r.chain && k) splits = std::min<uint64_t>(splits, std::max<uint32_t>(1, 8192 / k));   // merge capacity
   splits = std::max<uint64_t>(1, std::min<uint64_t>(splits, tiles_n));

@@ -483,3 +483,37 @@ def test_topk_from_host_csr_measure_order():
         ri, rs = oracle.topk(Q, D, N, d, m, k)
         assert np.array_equal(gi[t].numpy(), ri)
         assert_est_close(gs[t].numpy(), rs)
+
+
+def test_schedule_independence_stress(monkeypatch):
+    """Race / ordering stress in place of compute-sanitizer (closed on this pool,
+    profiles/r02_sanitize_memcheck_refused.log): the same inputs through every schedule knob —
+    persistent grid size, ring depth, db chunk size, forced heap chaining across chunks, CTA pairs —
+    must give bit-identical sketches, AND-popcounts and top-k lists, equal to the oracle's.
+    A missing barrier, a racy shared-memory OR or a heap update lost between the two epilogue
+    groups would show up as a schedule-dependent result."""
+    spec = synth.scaled(synth.LARGE, 2600, seed=71)
+    indptr, indices = synth.make_csr(spec)
+    N, d = synth.LARGE_N, spec.d
+    pi = oracle.make_pi(synth.PI_SEED, d, N)
+    ref_sk, _ = oracle.sketch(pi, d, N, indptr, indices)
+    ref_i, ref_s = oracle.topk(ref_sk[:700], ref_sk, N, d, 1, 50)
+    ref_j, _ = oracle.topk(ref_sk[:700], ref_sk, N, d, 4, 20)
+    ip, ix = csr_dev(indptr, indices)
+    knobs = [{}, {"BINSKETCH_TC_GRID": "7"}, {"BINSKETCH_TC_STAGES": "2"}, {"BINSKETCH_TC_CHUNK_KB": "384"},
+             {"BINSKETCH_TC_CHUNK_KB": "256", "BINSKETCH_TC_CHAIN": "1"},
+             {"BINSKETCH_TC_CHUNK_KB": "256", "BINSKETCH_TC_CHAIN": "1", "BINSKETCH_TC_GRID": "3"},
+             {"BINSKETCH_TC_ATM": "0", "BINSKETCH_TC_CG": "2"}, {"BINSKETCH_BUILD_MODE": "global"}]
+    for kn in knobs:
+        for key, val in kn.items():
+            monkeypatch.setenv(key, val)
+        sk = bs.build(dev(pi.view(np.int32)), d, N, ip, ix)
+        assert np.array_equal(u32(sk), ref_sk), kn
+        gi, gs = bs.topk(sk[:700], sk, N, d, 1, 50)
+        assert np.array_equal(gi.cpu().numpy(), ref_i), kn
+        assert_est_close(gs.cpu().numpy(), ref_s)
+        gj, _ = bs.topk(sk[:700], sk, N, d, 4, 20)
+        assert np.array_equal(gj.cpu().numpy(), ref_j), kn
+        bs.device_status()
+        for key in kn:
+            monkeypatch.delenv(key)
