@@ -55,6 +55,16 @@ struct TableCache {
     return ok;
   }
 
+  // L non-decreasing on [0, N): every estimator key is then non-decreasing in pab for fixed
+  // (pa, pb) — the condition of the pab-table top-k's integer screen (K4c).
+  bool monotone(uint32_t N, uint64_t d) {
+    const double* t = get(N, d);
+    if (!t) return false;
+    for (uint32_t k = 0; k + 1 < N; ++k)
+      if (t[k + 1] < t[k]) return false;
+    return true;
+  }
+
   const double* get(uint32_t N, uint64_t d, int kind = 0) {
     std::lock_guard<std::mutex> lock(mu);
     auto key = std::make_tuple(N, d, kind);
@@ -89,7 +99,7 @@ TableCache& cache() {
 
 struct Layout {
   size_t tmeta = 0, L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, qperm = 0, qspb = 0,
-         ctr = 0, done = 0, pab = 0, cnt = 0, x8 = 0, px = 0, pabx = 0, part = 0, total = 0;
+         ctr = 0, done = 0, pab = 0, cnt = 0, x8 = 0, px = 0, pabx = 0, part = 0, range = 0, scratch = 0, total = 0;
   uint32_t splits = 1;
 };
 
@@ -186,6 +196,10 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
     l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
     l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
     l.pab = off; off += align_up((size_t)na * nb * 4);
+    if (op == BINSKETCH_OP_TOPK) {   // pab-table top-k: db popcount range, pass-2 survivor scratch
+      l.range = off; off += kAlign;
+      l.scratch = off; off += align_up(bsk::topk_pab3_scratch_bytes(15u));
+    }
   }
   if (tc) {
     l.ctr = off; off += kAlign;
@@ -449,6 +463,12 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
       e = bsk::launch_tc_andpopc(q8, nq, d8, ndb, N, pabw, reinterpret_cast<unsigned long long*>(w + l.ctr), s);
     if (e != cudaSuccess) return cuda_status(e);
     pab = pabw;
+    const char* ps = std::getenv("BINSKETCH_PAB_SCREEN");   // dev A/B knob (0: the pre-test kernel)
+    if (!(ps && !std::strcmp(ps, "0")) && bsk::topk_pab3_fits(N, measure, k) && cache().monotone(N, d))
+      return cuda_status(bsk::launch_topk_pab3(pab, nq, ndb, N, measure, k, flags, pq, pd,
+                                               reinterpret_cast<const double*>(w + l.L),
+                                               reinterpret_cast<int32_t*>(w + l.range), w + l.scratch, out_idx,
+                                               out_score, s));
   }
   // the AND-popcount table (when used) serves every requested measure
   for (uint32_t mi = 0; mi < nm && e == cudaSuccess; ++mi)

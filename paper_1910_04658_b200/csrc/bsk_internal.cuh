@@ -63,6 +63,17 @@ cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint6
                         int32_t* out_idx, float* out_score, cudaStream_t s,
                         const int32_t* pab = nullptr);   // pab[nq][ndb] precomputed (tensor cores) or null
 
+// Top-k of every measure in `mask` from the pab table: sampled and screened histograms set an
+// integer screen pab >= T[pb] (per-query minimum-pab tables), then the survivors are ranked
+// exactly (K4c). pd_range: 2 int32 of workspace. Requires topk_pab3_fits and L
+// non-decreasing on [0, N) (the keys' monotonicity in pab).
+// scratch: topk_pab3_scratch_bytes(mask) of workspace (pass-2 survivors per block slot).
+bool topk_pab3_fits(uint32_t N, uint32_t mask, uint32_t k);
+size_t topk_pab3_scratch_bytes(uint32_t mask);
+cudaError_t launch_topk_pab3(const int32_t* pab, uint64_t nq, uint64_t ndb, uint32_t N, uint32_t mask, uint32_t k,
+                             uint32_t flags, const int32_t* pq, const int32_t* pd, const double* L, int32_t* pd_range,
+                             void* scratch, int32_t* out_idx, float* out_score, cudaStream_t s);
+
 // Tensor-core pair engine (tc.cu): sketches widened to {0,1} bytes, rows padded to
 // tc_kpad(N) bytes (multiple of 128), then tcgen05 kind::i8 all-pairs.
 uint32_t tc_kpad(uint32_t N);

@@ -549,6 +549,632 @@ uint32_t topk_splits(uint64_t nq, uint64_t ndb, uint32_t k) {
   return (uint32_t)std::max<uint64_t>(1, s);
 }
 
+// ------------------------------------------- pab-table top-k, integer screen (K4c) --
+// For fixed (pa, pb) every measure key is a non-decreasing function of pab: in estimate_pair
+// pu = pa + pb - pab falls as pab rises, so L[pu] falls and ip = S - L[pu] (clamped) rises;
+// JS = ip / (S - ip), COS = ip / sqrt(La Lb) and -HAM = 2 ip - S rise with ip; every fp64 step
+// is correctly rounded and hence monotone. So for a query row (pa fixed) and a threshold key t,
+// "key >= t" is exactly "pab >= T_t[pb]" with T_t[pb] the smallest pab whose key reaches t: the
+// scan over the table is one integer compare per pair and measure against a per-query table in
+// shared memory, and only the (few) pairs that pass are scored.
+#ifdef BSK_PABT_STATS   // dev: counters for tools/pabT_stats.py (variant library only)
+__device__ unsigned long long g_pabt[16];
+#define PABT_ADD(i, v) atomicAdd(&g_pabt[i], (unsigned long long)(v))
+#else
+#define PABT_ADD(i, v) ((void)0)
+#endif
+
+__device__ __forceinline__ double pab_key(int pa, int pb, int pab, int N, const double* __restrict__ L, uint32_t m) {
+  return measure_key(estimate_pair(pa, pb, pab, N, L, m), m);
+}
+
+// The smallest pab in [max(pa + pb - N, 0, from), min(pa, pb)] whose key reaches t, 0xFFFF if
+// none (no table value exceeds N <= 16383). `from` is a known lower bound of the answer (the
+// previous table value: t only rises). A guess from the inverted recipe — key >= t needs
+// ip >= ipmin (IP: t; -HAM: (S + t) / 2; JS: t S / (1 + t); COS: t sqrt(La Lb)), i.e.
+// L[pu] <= S - ipmin, the largest such pu by bisection of the (non-decreasing) L table, and
+// pab = pa + pb - pu — is then settled by the exact key, stepping down while the key still
+// reaches t and up while it does not (the guess is off by rounding only: a step or two).
+__device__ uint16_t min_pab(int pa, int pb, int N, const double* __restrict__ L, uint32_t m, double t, int from) {
+  const int lo = max(max(0, pa + pb - N), from);
+  const int hi = min(pa, pb);
+  if (lo > hi) return 0xFFFFu;
+  const double La = L[pa], Lb = L[pb];
+  const double S = La + Lb;
+  double ipmin;
+  if (m == 1u) ipmin = t;
+  else if (m == 2u) ipmin = 0.5 * (S + t);
+  else if (m == 4u) ipmin = t > 0.0 ? t * S / (1.0 + t) : -1.0;
+  else ipmin = t > 0.0 ? t * sqrt(La * Lb) : -1.0;
+  int g;   // guess
+  if (!(ipmin > 0.0)) {
+    g = lo;
+  } else {
+    // largest pu in [pa + pb - hi, pa + pb - lo] with L[pu] <= S - ipmin (pu = pa + pb - pab)
+    const double y = S - ipmin;
+    int plo = pa + pb - hi, phi = pa + pb - lo;
+    if (L[plo] > y) {
+      g = hi + 1;   // even the largest pab misses the target: check hi below
+    } else {
+      while (plo < phi) {
+        const int mid = (plo + phi + 1) >> 1;
+        if (L[mid] <= y) plo = mid;
+        else phi = mid - 1;
+      }
+      g = pa + pb - plo;
+    }
+  }
+  g = min(max(g, lo), hi);
+  if (pab_key(pa, pb, g, N, L, m) >= t) {
+    while (g > lo && pab_key(pa, pb, g - 1, N, L, m) >= t) --g;
+    return (uint16_t)g;
+  }
+  do {
+    ++g;
+  } while (g <= hi && pab_key(pa, pb, g, N, L, m) < t);
+  return g <= hi ? (uint16_t)g : (uint16_t)0xFFFFu;
+}
+
+// [min, max] of x[0..n) into out[0], out[1], which hold (INT_MAX-ish, INT_MIN-ish) byte patterns
+// on entry (0x7f7f7f7f, 0x80808080: two memsets).
+__global__ void __launch_bounds__(256) int_range_kernel(const int32_t* __restrict__ x, uint64_t n,
+                                                        int32_t* __restrict__ out) {
+  int lo = 0x7fffffff, hi = -0x7fffffff - 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const int v = __ldg(x + i);
+    lo = min(lo, v);
+    hi = max(hi, v);
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, lo);
+    atomicMax(out + 1, hi);
+  }
+}
+
+// One block per query row (grid-stride), every requested measure in the same passes over the
+// row's pab values, with no per-step block barriers:
+//  1. sample: exact keys of the first kPabSample columns into a kHB-bucket histogram over the
+//     measure's key range; t_s = the lower edge of the highest bucket with >= k sample pairs at
+//     or above it (so >= k pairs of the row have key >= t_s: a lower bound of its k-th key);
+//     T = the minimum-pab table for t_s.
+//  2. the whole row through the screen pab >= T[pb]; exact keys of the survivors into a
+//     histogram over [t_s, key max]; t0 >= t_s the same way; T raised to t0.
+//  3. the whole row through the raised screen; survivors that beat the running k-th (tk, ti)
+//     are buffered. Typically they number k plus one bucket's worth and fit; on an overflow the
+//     pass restarts in steps of 256 columns with a barrier each, cutting the buffer back to k
+//     (block bitonic sort) whenever the next step could overflow it.
+// The buffer is then sorted and its head written. Every compare is on the exact fp64 key, so
+// the result is the exact top-k whatever the histograms hold; they only set the screens.
+constexpr int kHB = 2048;               // histogram buckets (256 threads x 8)
+constexpr uint32_t kPabSample = 4096;   // pass-1 columns
+constexpr int kPab3Cap = 512;           // pass-3 buffer entries per measure (k <= 256)
+constexpr uint32_t kPab3Slow = 256;     // pass-3 step after an overflow (1 column per thread)
+constexpr uint32_t kPab3Keep = 8192;    // pass-2 survivors kept per (block, measure) in the scratch
+constexpr uint32_t kPab3Slots = 592;    // blocks (scratch slots) at most: 4 per SM on 148 SMs
+constexpr int kRing = 4;                // pab row ring: one-step chunks (256 threads x 16 B)
+
+__device__ __forceinline__ uint4 lds_v4u(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32u(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+#ifndef BSK_PAB3_MINB
+#define BSK_PAB3_MINB 3
+#endif
+
+template <int NM>
+__global__ void __launch_bounds__(256, BSK_PAB3_MINB)
+topk_pab3_kernel(const int32_t* __restrict__ pab, uint64_t nq, uint64_t ndb, uint32_t N, uint32_t mask, uint32_t k,
+                 uint32_t flags, const int32_t* __restrict__ pq, const int32_t* __restrict__ pd,
+                 const double* __restrict__ Lg, const int32_t* __restrict__ pdr, double* __restrict__ skey,
+                 int32_t* __restrict__ sidx, int32_t* __restrict__ out_idx, float* __restrict__ out_score) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int kQ = 32 + 128 * NM;   // per-warp survivor queue: < 32 waiting + one step's worth
+  uint32_t ms[NM];
+  {
+    uint32_t mm = mask, j = 0;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) { ms[i] = mm & (0u - mm); mm &= mm - 1; (void)j; }
+  }
+  const uint32_t TS = N + 1;
+  const size_t lbytes = 0;   // L stays in global memory (read through L1: 8(N+1) bytes, hot)
+  constexpr size_t hbytes = (size_t)NM * kHB * 4 > (size_t)NM * kPab3Cap * 12 ? (size_t)NM * kHB * 4
+                                                                              : (size_t)NM * kPab3Cap * 12;
+  const size_t tbytes = ((size_t)(NM == 3 ? 4 : NM) * TS * 2 + 15) & ~(size_t)15;
+  const double* __restrict__ L = Lg;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + lbytes);                  // [NM][kHB] (passes 1-2)
+  double* bkey = reinterpret_cast<double*>(smem + lbytes);                      // [NM][kPab3Cap] (pass 3)
+  int* bidx = reinterpret_cast<int*>(smem + lbytes + (size_t)NM * kPab3Cap * 8);
+  constexpr int NMP = NM == 3 ? 4 : NM;   // table entries per pb (one 2/4/8-byte load per column)
+  uint16_t* T = reinterpret_cast<uint16_t*>(smem + lbytes + hbytes);            // [N + 1][NMP]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint2* queue = reinterpret_cast<uint2*>(smem + lbytes + hbytes + tbytes) + warp * kQ;   // (column, v|b<<14|mi<<28)
+  __shared__ uint32_t cnt[NM];
+  __shared__ double tk[NM];
+  __shared__ int ti[NM];
+  __shared__ double lo_s[NM], sc_s[NM], tl_s[NM];
+  __shared__ uint32_t warp_sum[8];
+  __shared__ int found;
+  __shared__ int ovf;
+  __shared__ uint32_t scnt[NM];
+  __shared__ __align__(8) unsigned long long rbar[2 * kRing];   // full[kRing], empty[kRing]
+  const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(rbar);
+  const uint32_t ring_a = (uint32_t)__cvta_generic_to_shared(queue - warp * kQ + 8 * kQ);   // [kRing][blockDim.x * 4] int
+  uint32_t g0 = 0;   // row chunks streamed through the ring so far (block-uniform)
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(bar_a + 8u * i, 1);
+      mbar_init(bar_a + 8u * (kRing + i), blockDim.x / 32);
+    }
+    fence_proxy_async();
+  }
+  const double kNegInf = -__longlong_as_double(0x7ff0000000000000LL);
+  const int pdlo = pdr[0], pdhi = pdr[1];
+  const bool vec = (ndb & 3u) == 0 && (reinterpret_cast<uintptr_t>(pab) & 15u) == 0 &&
+                   (reinterpret_cast<uintptr_t>(pd) & 15u) == 0;
+  auto load = [&](const int32_t* prow, uint32_t cl, uint32_t cend, int (&v)[4], int (&b)[4]) {
+    if (vec && cl + 3 < cend) {
+      const int4 a4 = __ldcs(reinterpret_cast<const int4*>(prow + cl));
+      const int4 p4 = __ldg(reinterpret_cast<const int4*>(pd + cl));
+      v[0] = a4.x; v[1] = a4.y; v[2] = a4.z; v[3] = a4.w;
+      b[0] = p4.x; b[1] = p4.y; b[2] = p4.z; b[3] = p4.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        v[u] = cl + u < cend ? __ldcs(prow + cl + u) : 0;
+        b[u] = cl + u < cend ? __ldg(pd + cl + u) : 0;
+      }
+    }
+  };
+  // Walk columns [c, cend) of the row (32-bit indices: ndb < 2^31), 4 per thread per step,
+  // calling f(cl, v, b, ok) once per step with ok bit u set for the columns cl + u to consider
+  // (inside the range, not the excluded self pair). The pab values stream through a ring of
+  // kRing one-step chunks in shared memory, filled by 1-D bulk copies (TMA engine) that thread 0
+  // issues kRing - 1 steps ahead (the latency x bandwidth product needs tens of KB in flight per
+  // SM, far more than a register prefetch holds); the db popcounts (L2-resident) come through
+  // registers one step ahead. Unaligned rows take the register path for both.
+  auto walk = [&](const int32_t* prow, uint64_t r, uint32_t c, uint32_t cend, auto&& f) {
+    const uint32_t stride = 4 * blockDim.x;
+    const uint32_t self = (flags & 1u) ? (uint32_t)r : 0xffffffffu;
+    auto okmask = [&](uint32_t c0, uint32_t cl) -> uint32_t {
+      if (c0 + stride <= cend && (self < c0 || self >= c0 + stride)) return 0xfu;   // whole step inside
+      uint32_t ok = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (cl + u < cend && cl + u != self) ok |= 1u << u;
+      return ok;
+    };
+    if (c >= cend) return;
+    if (!vec) {
+      int va[4], ba[4], vb[4], bb[4];
+      uint32_t cl = c + 4 * threadIdx.x;
+      load(prow, cl, cend, va, ba);
+      for (uint32_t c0 = c; c0 < cend; c0 += 2 * stride, cl += 2 * stride) {
+        const bool m1 = c0 + stride < cend;
+        if (m1) load(prow, cl + stride, cend, vb, bb);
+        f(cl, va, ba, okmask(c0, cl));
+        if (!m1) break;
+        if (c0 + 2 * stride < cend) load(prow, cl + 2 * stride, cend, va, ba);
+        f(cl + stride, vb, bb, okmask(c0 + stride, cl + stride));
+      }
+      return;
+    }
+    const uint32_t nch = (cend - c + stride - 1) / stride;
+    // chunk j (global sequence number g0 + j) -> slot (g0 + j) % kRing; its 16-B part by bulk copy
+    auto issue = [&](uint32_t j) {
+      const uint32_t gj = g0 + j, slot = gj % kRing;
+      const uint32_t full = bar_a + 8u * slot, empty = bar_a + 8u * (kRing + slot);
+      if (gj >= kRing) mbar_wait(empty, ((gj / kRing) - 1) & 1u);   // the slot's previous chunk consumed
+      fence_proxy_async();
+      const uint32_t s0 = c + j * stride;
+      const uint32_t nb = (min(s0 + stride, cend) - s0) * 4 & ~15u;
+      if (nb > 0) {
+        mbar_expect_tx(full, nb);
+        bulk_load(ring_a + slot * 16u * blockDim.x, prow + s0, nb, full);
+      } else {
+        mbar_arrive(full);
+      }
+    };
+    if (threadIdx.x == 0)
+      for (uint32_t j = 0; j < min(nch, (uint32_t)kRing - 1); ++j) issue(j);
+    int b[4], bn[4];
+    uint32_t cl = c + 4 * threadIdx.x;
+    {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) b[u] = cl + u < cend ? __ldg(pd + cl + u) : 0;
+    }
+    for (uint32_t j = 0; j < nch; ++j, cl += stride) {
+      const uint32_t c0 = c + j * stride;
+      const bool more = j + 1 < nch;
+      if (more) {
+        if (cl + stride + 3 < cend) {
+          const int4 p4 = __ldg(reinterpret_cast<const int4*>(pd + cl + stride));
+          bn[0] = p4.x; bn[1] = p4.y; bn[2] = p4.z; bn[3] = p4.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) bn[u] = cl + stride + u < cend ? __ldg(pd + cl + stride + u) : 0;
+        }
+      }
+      if (threadIdx.x == 0 && j + kRing - 1 < nch) issue(j + kRing - 1);
+      const uint32_t gj = g0 + j, slot = gj % kRing;
+      mbar_wait(bar_a + 8u * slot, (gj / kRing) & 1u);
+      int v[4];
+      const uint32_t bulk_end = c0 + (((min(c0 + stride, cend) - c0) * 4 & ~15u) >> 2);
+      if (cl + 3 < bulk_end) {
+        const uint4 q = lds_v4u(ring_a + slot * 16u * blockDim.x + 16u * threadIdx.x);
+        v[0] = (int)q.x; v[1] = (int)q.y; v[2] = (int)q.z; v[3] = (int)q.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = cl + u < bulk_end ? (int)lds_u32u(ring_a + slot * 16u * blockDim.x + 4u * (threadIdx.x * 4 + u))
+                                   : (cl + u < cend ? __ldg(prow + cl + u) : 0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_a + 8u * (kRing + slot));   // this warp is done with the slot
+      f(cl, v, b, okmask(c0, cl));
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b[u] = bn[u];
+      }
+    }
+    g0 += nch;
+  };
+  // Screened walk: the (column, measure) items with pab >= T[mi][pb] go to the warp's queue;
+  // every full 32 are scored by the warp's 32 lanes together (dense fp64 work instead of one
+  // divergent lane per warp-step) and handed to g(column, mi, key); the rest at the end.
+  auto screened = [&](const int32_t* prow, uint64_t r, auto&& g) {
+    int qn = 0;   // warp-uniform
+    const int pa_ = pq[r];
+    auto drain = [&](int n) {   // score the top n (<= 32) queue entries
+      if (lane < n) {
+        const uint2 it = queue[qn - n + lane];
+        const int v = (int)(it.y & 0x3fffu), b = (int)((it.y >> 14) & 0x3fffu);
+        const uint32_t mi = it.y >> 28;
+        uint32_t m = ms[0];
+#pragma unroll
+        for (int i = 1; i < NM; ++i) m = mi == (uint32_t)i ? ms[i] : m;
+        g((uint64_t)it.x, mi, pab_key(pa_, b, v, (int)N, L, m));
+      }
+      qn -= n;
+      __syncwarp();
+    };
+    walk(prow, r, 0, (uint32_t)ndb, [&](uint32_t cl, const int (&v)[4], const int (&b)[4], uint32_t ok) {
+      uint32_t pm = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint16_t tv[NMP];
+        if constexpr (NMP == 1) {
+          tv[0] = T[b[u]];
+        } else if constexpr (NMP == 2) {
+          const ushort2 t2 = reinterpret_cast<const ushort2*>(T)[b[u]];
+          tv[0] = t2.x; tv[1] = t2.y;
+        } else {
+          const ushort4 t4 = reinterpret_cast<const ushort4*>(T)[b[u]];
+          tv[0] = t4.x; tv[1] = t4.y; tv[2] = t4.z; tv[3] = t4.w;
+        }
+#pragma unroll
+        for (int mi = 0; mi < NM; ++mi)
+          if (((ok >> u) & 1u) && v[u] >= (int)tv[mi]) pm |= 1u << (u * NM + mi);
+      }
+      const uint32_t n = __popc(pm);
+      if (__any_sync(0xffffffffu, n != 0)) {
+        uint32_t off = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, off, o); if (lane >= o) off += y; }
+        const uint32_t total = __shfl_sync(0xffffffffu, off, 31);
+        uint32_t pos = (uint32_t)qn + off - n;
+        while (pm) {
+          const int bit = __ffs(pm) - 1;
+          pm &= pm - 1;
+          const int u = bit / NM, mi = bit % NM;
+          queue[pos++] = make_uint2((uint32_t)(cl + u), (uint32_t)v[u] | ((uint32_t)b[u] << 14) | ((uint32_t)mi << 28));
+        }
+        qn += (int)total;
+        __syncwarp();
+        while (qn >= 32) drain(32);
+      }
+    });
+    if (qn > 0) drain(qn);
+  };
+  // Highest bucket h with >= k counts in buckets >= h, or -1 (block-wide; thread t owns buckets
+  // [kHB - 8(t+1), kHB - 8t), scanned from the top).
+  auto select = [&](const uint32_t* hm) -> int {
+    const int top = kHB - 8 * (int)threadIdx.x;
+    uint32_t loc = 0;
+#pragma unroll
+    for (int j = 1; j <= 8; ++j) loc += hm[top - j];
+    uint32_t inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+    if (lane == 31) warp_sum[warp] = inc;
+    if (threadIdx.x == 0) found = -1;
+    __syncthreads();
+    uint32_t before_w = 0;
+    for (int w = 0; w < warp; ++w) before_w += warp_sum[w];
+    const uint32_t excl = before_w + inc - loc;
+    if (excl < k && excl + loc >= k) {
+      uint32_t run = excl;
+      for (int j = 1; j <= 8; ++j) {
+        run += hm[top - j];
+        if (run >= k) { found = top - j; break; }
+      }
+    }
+    __syncthreads();
+    const int h = found;
+    __syncthreads();
+    return h;
+  };
+  auto bucket = [&](uint32_t mi, double key) -> int {
+    const double x = (key - lo_s[mi]) * sc_s[mi];
+    return x <= 0.0 ? 0 : (x >= (double)(kHB - 1) ? kHB - 1 : (int)x);
+  };
+  // lower bound from a selected bucket (h > 0): its lower edge less a rounding margin
+  auto edge = [&](uint32_t mi, int h) -> double {
+    if (h <= 0 || !(sc_s[mi] > 0.0)) return kNegInf;
+    const double e = lo_s[mi] + (double)h / sc_s[mi];
+    return e - 1e-12 * fmax(1.0, fmax(fabs(e), fabs(lo_s[mi])));
+  };
+  // sort measure mi's n buffered candidates, keep the best k, raise (tk, ti) and T (block-wide)
+  auto flush = [&](uint32_t mi, uint32_t n, int pa) {
+    double* key = bkey + mi * kPab3Cap;
+    int* idx = bidx + mi * kPab3Cap;
+    uint32_t P = 2;
+    while (P < n) P <<= 1;
+    for (uint32_t i = n + threadIdx.x; i < P; i += blockDim.x) { key[i] = kNegInf; idx[i] = kSentinelIdx; }
+    __syncthreads();
+    block_bitonic_sort(key, idx, (int)P);
+    const bool full = n >= k;
+    const double nt = full ? key[k - 1] : kNegInf;
+    const int nti = full ? idx[k - 1] : kSentinelIdx;
+    const bool raise = full && nt > tl_s[mi];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      cnt[mi] = full ? k : n;
+      tk[mi] = nt;
+      ti[mi] = nti;
+      if (raise) tl_s[mi] = nt;
+    }
+    if (raise)
+      for (int pb = pdlo + (int)threadIdx.x; pb <= pdhi; pb += (int)blockDim.x)
+        T[pb * NMP + mi] = min_pab(pa, pb, (int)N, L, ms[mi], nt, (int)T[pb * NMP + mi]);
+    __syncthreads();
+  };
+  // pass-3 consumer: buffer a survivor that beats the running k-th
+  auto collect = [&](uint64_t c, uint32_t mi, double key) {
+    PABT_ADD(3, 1);
+    if (!before(key, (int)c, tk[mi], ti[mi])) return;
+    const uint32_t pos = atomicAdd(&cnt[mi], 1u);
+    if (pos < (uint32_t)kPab3Cap) {
+      bkey[mi * kPab3Cap + pos] = key;
+      bidx[mi * kPab3Cap + pos] = (int)c;
+    } else {
+      ovf = 1;
+    }
+  };
+  for (uint64_t r = blockIdx.x; r < nq; r += gridDim.x) {
+    const int pa = pq[r];
+    const int32_t* prow = pab + r * ndb;
+    const double La = L[pa];
+#ifdef BSK_PABT_STATS
+    long long tph = clock64();
+#define PHASE(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); PABT_ADD(i, t_ - tph); tph = t_; } } while (0)
+#else
+#define PHASE(i) ((void)0)
+#endif
+    const double Lbmax = fmax(L[pdhi], L[pdhi < (int)N ? pdhi : (int)N - 1]);
+    // ---- pass 1: sample histogram over each measure's whole key range
+    for (uint32_t i = threadIdx.x; i < NM * kHB; i += blockDim.x) hist[i] = 0u;
+    if (threadIdx.x < NM) {
+      uint32_t m = ms[0];
+#pragma unroll
+      for (int i = 1; i < NM; ++i) m = threadIdx.x == (unsigned)i ? ms[i] : m;
+      const double lo = m == 2u ? -(La + Lbmax) : 0.0;
+      const double hi = m == 1u ? La : (m == 2u ? 0.0 : 1.0);
+      lo_s[threadIdx.x] = lo;
+      sc_s[threadIdx.x] = (hi > lo && hi - lo < 1e300) ? (double)kHB / (hi - lo) : 0.0;
+    }
+    __syncthreads();
+    walk(prow, r, 0, (uint32_t)min(ndb, (uint64_t)kPabSample), [&](uint32_t cl, const int (&v)[4], const int (&b)[4], uint32_t ok) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if ((ok >> u) & 1u)
+#pragma unroll
+          for (int mi = 0; mi < NM; ++mi)
+            atomicAdd(hist + mi * kHB + bucket(mi, pab_key(pa, b[u], v[u], (int)N, L, ms[mi])), 1u);
+    });
+    __syncthreads();
+    PHASE(5);
+#pragma unroll
+    for (int mi = 0; mi < NM; ++mi) {
+      const double ts = edge(mi, select(hist + mi * kHB));
+      if (threadIdx.x == 0) tl_s[mi] = ts;
+      for (int pb = pdlo + (int)threadIdx.x; pb <= pdhi; pb += (int)blockDim.x)
+        T[pb * NMP + mi] = ts == kNegInf ? (uint16_t)0 : min_pab(pa, pb, (int)N, L, ms[mi], ts, 0);
+    }
+    __syncthreads();
+    // ---- pass 2: screened histogram over [t_s, key max]
+    for (uint32_t i = threadIdx.x; i < NM * kHB; i += blockDim.x) hist[i] = 0u;
+    if (threadIdx.x < NM) {
+      uint32_t m = ms[0];
+#pragma unroll
+      for (int i = 1; i < NM; ++i) m = threadIdx.x == (unsigned)i ? ms[i] : m;
+      const double hi = m == 1u ? La : (m == 2u ? 0.0 : 1.0);
+      const double lo = tl_s[threadIdx.x] == kNegInf ? lo_s[threadIdx.x] : tl_s[threadIdx.x];
+      lo_s[threadIdx.x] = lo;
+      sc_s[threadIdx.x] = (hi > lo && hi - lo < 1e300) ? (double)kHB / (hi - lo) : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < NM) scnt[threadIdx.x] = 0;
+    __syncthreads();
+    PHASE(6);
+    screened(prow, r, [&](uint64_t c, uint32_t mi, double key) {
+      PABT_ADD(2, 1);
+      atomicAdd(hist + mi * kHB + bucket(mi, key), 1u);
+      const uint32_t pos = atomicAdd(&scnt[mi], 1u);   // keep it for pass 3 (this block's slot)
+      if (pos < kPab3Keep) {
+        skey[((size_t)blockIdx.x * NM + mi) * kPab3Keep + pos] = key;
+        sidx[((size_t)blockIdx.x * NM + mi) * kPab3Keep + pos] = (int)c;
+      }
+    });
+    __syncthreads();
+    PHASE(7);
+#pragma unroll
+    for (int mi = 0; mi < NM; ++mi) {
+      const double t0 = edge(mi, select(hist + mi * kHB));
+      const bool raise = t0 > tl_s[mi];
+      __syncthreads();
+      if (threadIdx.x == 0 && raise) tl_s[mi] = t0;
+      if (raise)
+        for (int pb = pdlo + (int)threadIdx.x; pb <= pdhi; pb += (int)blockDim.x)
+          T[pb * NMP + mi] = min_pab(pa, pb, (int)N, L, ms[mi], t0, (int)T[pb * NMP + mi]);
+    }
+    if (threadIdx.x < NM) { cnt[threadIdx.x] = 0; tk[threadIdx.x] = kNegInf; ti[threadIdx.x] = kSentinelIdx; }
+    if (threadIdx.x == 0) ovf = 0;
+    __syncthreads();   // (the buffers alias the histograms: every select is done)
+    PHASE(8);
+    // ---- pass 3: collect the survivors of the raised screen — from the pass-2 survivors kept
+    // in this block's scratch slot (key >= t0 <=> pab >= T[pb]), or by re-walking the row
+    // when more survived pass 2 than the slot holds
+    bool kept = true;
+#pragma unroll
+    for (int mi = 0; mi < NM; ++mi) kept = kept && scnt[mi] <= kPab3Keep;
+    if (kept) {
+#pragma unroll
+      for (int mi = 0; mi < NM; ++mi) {
+        const double t0 = tl_s[mi];
+        const double* sk = skey + ((size_t)blockIdx.x * NM + mi) * kPab3Keep;
+        const int* si = sidx + ((size_t)blockIdx.x * NM + mi) * kPab3Keep;
+        for (uint32_t i = threadIdx.x; i < scnt[mi]; i += blockDim.x) {
+          const double key = sk[i];
+          if (key >= t0) collect((uint64_t)si[i], mi, key);
+        }
+      }
+    } else {
+      screened(prow, r, collect);
+    }
+    __syncthreads();
+    PHASE(9);
+    if (ovf) {   // (uniform) rare: restart the pass in barrier-separated steps
+      PABT_ADD(4, threadIdx.x == 0);
+      if (threadIdx.x < NM) { cnt[threadIdx.x] = 0; tk[threadIdx.x] = kNegInf; ti[threadIdx.x] = kSentinelIdx; }
+      __syncthreads();
+      for (uint64_t c = 0; c < ndb; c += kPab3Slow) {
+        const uint64_t cc = c + threadIdx.x;
+        if (cc < ndb && !((flags & 1u) && cc == r)) {
+          const int v = __ldcs(prow + cc), b = __ldg(pd + cc);
+#pragma unroll
+          for (int mi = 0; mi < NM; ++mi)
+            if (v >= (int)T[b * NMP + mi]) collect(cc, mi, pab_key(pa, b, v, (int)N, L, ms[mi]));
+        }
+        __syncthreads();
+#pragma unroll
+        for (int mi = 0; mi < NM; ++mi) {
+          const uint32_t n = cnt[mi];
+          if (n > (uint32_t)kPab3Cap - kPab3Slow) flush(mi, n, pa);
+        }
+      }
+    }
+    // final ranking: warp mi sorts measure mi's buffer (no block barriers) and writes its head
+    if (warp < NM) {
+      const int mi = warp;
+      uint32_t m = ms[0];
+#pragma unroll
+      for (int i = 1; i < NM; ++i) m = mi == i ? ms[i] : m;
+      double* key = bkey + mi * kPab3Cap;
+      int* idx = bidx + mi * kPab3Cap;
+      const uint32_t n = min(cnt[mi], (uint32_t)kPab3Cap);
+      uint32_t P = 32;
+      while (P < n) P <<= 1;
+      for (uint32_t i = n + lane; i < P; i += 32) { key[i] = kNegInf; idx[i] = kSentinelIdx; }
+      __syncwarp();
+      warp_bitonic_sort(key, idx, (int)P);
+      for (uint32_t q = lane; q < k; q += 32) {
+        const bool valid = q < n && idx[q] != kSentinelIdx;
+        const size_t o = (size_t)mi * nq * k + r * k + q;
+        out_idx[o] = valid ? idx[q] : -1;
+        out_score[o] = valid ? key_to_score(key[q], m) : __int_as_float(0x7fc00000);
+      }
+    }
+    PABT_ADD(0, threadIdx.x == 0);
+    __syncthreads();
+    PHASE(10);
+  }
+}
+#undef PHASE
+
+#ifdef BSK_PABT_STATS
+}  // namespace bsk
+extern "C" void bsk_pabt_stats(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, bsk::g_pabt, sizeof(bsk::g_pabt));
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(bsk::g_pabt, z, sizeof(z));
+}
+namespace bsk {
+#endif
+
+static size_t topk_pab3_smem(uint32_t N, uint32_t nm) {
+  const size_t h = std::max<size_t>((size_t)nm * kHB * 4, (size_t)nm * kPab3Cap * 12);
+  return h + (((size_t)(nm == 3 ? 4 : nm) * (N + 1) * 2 + 15) & ~(size_t)15) +
+         (size_t)8 * (32 + 128 * nm) * 8 + (size_t)kRing * 256 * 16;
+}
+
+size_t topk_pab3_scratch_bytes(uint32_t mask) {
+  return (size_t)kPab3Slots * (size_t)__builtin_popcount(mask & 15u) * kPab3Keep * 12;
+}
+
+bool topk_pab3_fits(uint32_t N, uint32_t mask, uint32_t k) {
+  const uint32_t nm = (uint32_t)__builtin_popcount(mask & 15u);
+  return nm >= 1 && N <= 16383 && k >= 1 && k <= (uint32_t)kPab3Cap - kPab3Slow &&
+         topk_pab3_smem(N, nm) <= (size_t)227 * 1024;
+}
+
+template <int NM>
+static cudaError_t launch_topk_pab3_t(const int32_t* pab, uint64_t nq, uint64_t ndb, uint32_t N, uint32_t mask,
+                                      uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* pd, const double* L,
+                                      int32_t* pd_range, unsigned char* scratch, int32_t* out_idx, float* out_score,
+                                      cudaStream_t s) {
+  const size_t smem = topk_pab3_smem(N, NM);
+  cudaError_t e = cudaFuncSetAttribute(topk_pab3_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int bps = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, topk_pab3_kernel<NM>, 256, smem) != cudaSuccess || bps < 1)
+    bps = 1;
+  const uint64_t grid = std::min<uint64_t>({nq, (uint64_t)num_sms() * (uint64_t)bps, (uint64_t)kPab3Slots});
+  double* skey = reinterpret_cast<double*>(scratch);
+  int32_t* sidx = reinterpret_cast<int32_t*>(scratch + (size_t)kPab3Slots * NM * kPab3Keep * 8);
+  topk_pab3_kernel<NM><<<(unsigned)grid, 256, smem, s>>>(pab, nq, ndb, N, mask, k, flags, pq, pd, L, pd_range, skey,
+                                                         sidx, out_idx, out_score);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_pab3(const int32_t* pab, uint64_t nq, uint64_t ndb, uint32_t N, uint32_t mask, uint32_t k,
+                             uint32_t flags, const int32_t* pq, const int32_t* pd, const double* L, int32_t* pd_range,
+                             void* scratch_v, int32_t* out_idx, float* out_score, cudaStream_t s) {
+  if (nq == 0 || k == 0 || ndb == 0) return cudaSuccess;
+  unsigned char* scratch = static_cast<unsigned char*>(scratch_v);
+  cudaError_t e = cudaMemsetAsync(pd_range, 0x7f, 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(pd_range + 1, 0x80, 4, s);
+  if (e != cudaSuccess) return e;
+  int_range_kernel<<<(unsigned)std::min<uint64_t>((ndb + 255) / 256, (uint64_t)num_sms()), 256, 0, s>>>(pd, ndb,
+                                                                                                        pd_range);
+  count_launch();
+  mask &= 15u;
+  switch (__builtin_popcount(mask)) {
+    case 1: return launch_topk_pab3_t<1>(pab, nq, ndb, N, mask, k, flags, pq, pd, L, pd_range, scratch, out_idx, out_score, s);
+    case 2: return launch_topk_pab3_t<2>(pab, nq, ndb, N, mask, k, flags, pq, pd, L, pd_range, scratch, out_idx, out_score, s);
+    case 3: return launch_topk_pab3_t<3>(pab, nq, ndb, N, mask, k, flags, pq, pd, L, pd_range, scratch, out_idx, out_score, s);
+    default: return launch_topk_pab3_t<4>(pab, nq, ndb, N, mask, k, flags, pq, pd, L, pd_range, scratch, out_idx, out_score, s);
+  }
+}
+
 // Top-k from a precomputed AND-popcount table pab[nq][ndb] (tensor cores): one warp per
 // (query row, db split) streams its pab row (16-B loads, 128 columns per step), keeps a running
 // threshold (its current k-th best), screens every pair with the division-free pre-test, scores

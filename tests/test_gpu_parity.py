@@ -447,6 +447,44 @@ def test_topk_pab_single_split_direct_outputs(measure, monkeypatch):
     _check_topk(Q, D, N, d, measure, 100)
 
 
+@pytest.mark.parametrize("screen", ["1", "0"])
+def test_topk_pab_screen_paths(screen, monkeypatch):
+    """The pab-table top-k (k > 64 or N > 6143): the integer-screen kernel (sampled + screened
+    histograms, survivors kept in scratch; K4c) and the pre-test kernel it replaces
+    (BINSKETCH_PAB_SCREEN=0) on the cases that leave the common path: a query whose 700 exact
+    copies in the db all tie above its threshold (pass-3 buffer overflow -> barrier-stepped
+    re-walk), one with 9000 copies (pass-2 survivors beyond the scratch slot -> screened re-walk),
+    an empty query row, an unaligned db (ndb % 4 != 0: register path), self exclusion, every
+    measure alone and all four together."""
+    monkeypatch.setenv("BINSKETCH_ENGINE", "tc")
+    monkeypatch.setenv("BINSKETCH_PAB_SCREEN", screen)
+    N, d = synth.RANKING_N, synth.RANKING_DB.d
+    D = _sketches(synth.scaled(synth.RANKING_DB, 12_003, seed=71), N)
+    D[1000:1700] = D[7]
+    D[2000:11000] = D[8]
+    D[5] = 0
+    Q = D[:40].copy()
+    for m in (bs.IP, bs.HAM, bs.JS, bs.COS):
+        _check_topk(Q, D, N, d, m, 100, exclude_self=True)
+    _check_topk(Q, D[:12_000], N, d, bs.JS, 256)
+    Qd, Dd = dev(Q.view(np.int32)), dev(D.view(np.int32))
+    gi, gs = bs.topk(Qd, Dd, N, d, bs.IP | bs.HAM | bs.JS | bs.COS, 90)
+    for t, m in enumerate((bs.IP, bs.HAM, bs.JS, bs.COS)):
+        ri, rs = oracle.topk(Q, D, N, d, m, 90)
+        assert np.array_equal(gi[t].cpu().numpy(), ri)
+        assert_est_close(gs[t].cpu().numpy(), rs)
+
+
+@pytest.mark.parametrize("N", [16383, 16384])
+def test_topk_pab_screen_n_limit(N):
+    """The integer-screen kernel's 14-bit table entries end at N = 16383; N = 16384 takes the
+    pre-test pab kernel. Both exact, ties included."""
+    d = 102_660
+    D = _sketches(synth.scaled(synth.RANKING_DB, 1_500, seed=73), N)
+    D[100:400] = D[3]
+    _check_topk(D[:30].copy(), D, N, d, bs.COS, 100)
+
+
 @pytest.mark.parametrize("N", [1024, 1025, 5600, 5700, 6143])
 def test_topk_k64_shared_memory_boundary(N):
     """k = 64 across the fused kernel's shared-memory limit: N = 1024 keeps the query
