@@ -46,12 +46,12 @@ POPC_BASIS = "K9 measured 15.11 POPC/clk/SM (profiles/r02_microbench_k9.jsonl) x
 TOPK_NCU = {"source": "profiles/r02_topk_final_summary.txt", "tensor_pipe_active_pct": 43.4,
             "issue_active_pct": 20.9, "dram_bytes_per_launch": 2.369e9 + 0.586e9, "kernel_share_of_stage": "98.3 %",
             "launch_list": "profiles/r02_launches_large_summary.txt"}
-# Ranking: the dominant kernel of the top-k call is the pab-table top-k (topk_pab3_kernel, K4c);
-# its share of the call from the committed launch list (cold-cache, serialised: 0.6925 of 1.074 ms per
-# call = expand 2 x 0.057 + popcount 2 x 0.008 + int_range 0.004 + tc_pairs 0.247 + topk_pab3 0.6925)
-# and its DRAM traffic per launch from one ncu --set full capture.
-RANK_NCU = {"source": "profiles/r02_topk_pab3_summary.txt", "kernel_share_of_stage": 0.6925 / 1.074,
-            "dram_bytes_per_launch": 428.6e6 + 52.2e6, "issue_active_pct": 50.2,
+# Ranking: the dominant kernel of the top-k call is the tensor-core AND-popcount with the integer
+# screen in its epilogue (tc_pairs_kernel<kTcScreen>, K4d); its share of the call from the
+# committed launch list (cold-cache, serialised; per call: screen 0.3297, list top-k 0.1087,
+# thresholds 0.0670, expand 0.0570 + 2 x 0.005, popcount sort 0.0472, sample AND-popcount 0.0205,
+# popcounts 0.0166, range 0.0046 ms) and its ncu capture.
+RANK_NCU = {"source": "profiles/r02_tc_screen_summary.txt", "kernel_share_of_stage": 0.3297 / 0.6963,
             "launch_list": "profiles/r02_launches_ranking_summary.txt"}
 HBM_FALLBACK_GBS = 6650.0     # B200_PROFILING.md fallback
 
@@ -363,25 +363,22 @@ def run_ours(args):
             roofline["traffic"] = TOPK_NCU["dram_bytes_per_launch"]
             roofline["traffic_unit"] = "DRAM bytes per launch (ncu; operands are L2-resident)"
     elif engine != "cuda":
-        # k > 64 or N > 6143: tensor-core AND-popcount into the pab table, then the pab-table top-k, which
-        # dominates the call. Its algorithmic bytes: the table read once (4 B per pair) + the db popcounts
-        # once (re-read per query row from L2, not counted); time = the live top-k stage time x the
-        # kernel's launch-list share.
+        # k > 64 or N > 6143: sample thresholds, the tensor-core AND-popcount with the integer screen
+        # in its epilogue (survivor lists), the exact list top-k. The screen kernel dominates; its
+        # work is the whole contraction (2 * pairs * N int8 ops per measure set), time = the live
+        # top-k stage time x its launch-list share.
         share = RANK_NCU["kernel_share_of_stage"]
-        alg_bytes = nq * n * 4 + n * 4
-        t_kernel = t_topk / args.steps * share
-        roofline = {"bound": "hbm", "kernel": "topk_pab3_kernel (pab-table top-k, integer screen; DESIGN.md K4c)",
-                    "achieved": alg_bytes / t_kernel / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": alg_bytes / t_kernel / 1e9 / pk["hbm_gbs"],
-                    "algorithmic_bytes": "pab table (nq*ndb*4) + db popcounts (ndb*4)",
-                    "traffic": RANK_NCU["dram_bytes_per_launch"],
-                    "traffic_unit": "DRAM bytes per launch (ncu --set full)",
+        pairs_once = nq * n   # the contraction runs once for every requested measure
+        ach_k = 2.0 * pairs_once * N * args.steps / (t_topk * share) / 1e12
+        roofline = {"bound": "tensor", "kernel": "tc_pairs_kernel<kTcScreen> (AND-popcount + integer screen epilogue; DESIGN.md K4d)",
+                    "achieved": ach_k, "peak": burst, "unit": "TOPS (int8)", "frac": ach_k / burst,
+                    "peak_basis": "2 x MEASURED_PEAKS bf16_tflops (burst)", "peak_sustained": sust,
+                    "frac_of_sustained": ach_k / sust, "traffic": None,
                     "time_basis": "live top-k stage time x the kernel's share of it in the launch list ("
                                   + RANK_NCU["launch_list"] + "): " + f"{share:.3f}",
-                    "note": "issue / latency bound (ncu issue-active " + str(RANK_NCU["issue_active_pct"])
-                            + " %): three passes of integer screens and exact fp64 scoring of the survivors",
-                    "whole_call_tensor": {**tc_common,
-                                          "time_basis": "whole top-k call (expand + tensor-core AND-popcount + pab-table top-k)"}}
+                    "whole_call": {"achieved": 2.0 * pairs_once * N * args.steps / t_topk / 1e12, "unit": "TOPS (int8)",
+                                   "frac_of_burst": 2.0 * pairs_once * N * args.steps / t_topk / 1e12 / burst,
+                                   "time_basis": "whole top-k call (popcounts, sort, expand, sample thresholds, screen, list top-k)"}}
     else:
         roofline = {"bound": "alu", "kernel": "topk_kernel (LOP3+POPC mainloop + fp64 epilogue)",
                     "achieved": popc["achieved"], "peak": popc["peak"], "unit": "Tword-popc/s", "frac": popc["frac"],

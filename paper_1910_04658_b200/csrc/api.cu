@@ -99,7 +99,8 @@ TableCache& cache() {
 
 struct Layout {
   size_t tmeta = 0, L = 0, pa = 0, pb = 0, pkey = 0, pidx = 0, a8 = 0, b8 = 0, bins = 0, perm = 0, spb = 0, qperm = 0, qspb = 0,
-         ctr = 0, done = 0, pab = 0, cnt = 0, x8 = 0, px = 0, pabx = 0, part = 0, range = 0, scratch = 0, total = 0;
+         ctr = 0, done = 0, pab = 0, cnt = 0, x8 = 0, px = 0, pabx = 0, part = 0, range = 0, scratch = 0, s8 = 0, pabs = 0, ts = 0, tsuf = 0,
+         lcnt = 0, total = 0;
   uint32_t splits = 1;
 };
 
@@ -128,6 +129,17 @@ bool use_tc(int op, uint32_t N, uint32_t k = 0) {
 constexpr size_t kPabBudget = size_t(4) << 30;
 bool use_tc_pab(uint32_t N, uint64_t nq, uint64_t ndb, uint32_t k) {
   return !engine_cuda() && !use_tc(BINSKETCH_OP_TOPK, N, k) && nq * ndb * 4 <= kPabBudget;
+}
+
+// Top-k through the fused tensor-core screen (K4d): sample thresholds and minimum-pab
+// tables, the AND-popcount with the screen in its epilogue (survivor lists, no table), the exact
+// ranking of the survivors. Sizes that allow it (the lists take 8 B per pair, in the budget);
+// the call also needs L non-decreasing on [0, N) (checked per (N, d)). BINSKETCH_TOPK_SCREEN=0
+// selects the pab-table kernels instead (dev A/B).
+constexpr uint64_t kScreenSample = 4096;   // db rows [0, S) sampled for the thresholds
+bool screen_size_ok(uint32_t N, uint64_t nq, uint64_t ndb, uint32_t k) {
+  if (const char* e = std::getenv("BINSKETCH_TOPK_SCREEN")) if (!std::strcmp(e, "0")) return false;
+  return N <= 16383 && k >= 1 && k <= 256 && bsk::tc_sortable(N) && nq * ndb * 8 <= kPabBudget;
 }
 
 // All-pairs estimate planes through a pab table: tensor-core AND-popcount into pab[na][nb], then the
@@ -195,10 +207,23 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
     l.ctr = off; off += kAlign;
     l.a8 = off; off += align_up((size_t)na * bsk::tc_kpad(N));
     l.b8 = off; off += align_up((size_t)nb * bsk::tc_kpad(N));
-    l.pab = off; off += align_up((size_t)na * nb * 4);
+    // the pab table, or (fused-screen top-k) the survivor lists [na][nb] uint2 in the same place
+    const bool scr = op == BINSKETCH_OP_TOPK && screen_size_ok(N, na, nb, k);
+    l.pab = off; off += align_up((size_t)na * nb * (scr ? 8 : 4));
     if (op == BINSKETCH_OP_TOPK) {   // pab-table top-k: db popcount range, pass-2 survivor scratch
       l.range = off; off += kAlign;
       l.scratch = off; off += align_up(bsk::topk_pab3_scratch_bytes(15u));
+    }
+    if (scr) {   // fused screen: sample operand + table, thresholds, tables, list counts, db sort
+      const uint64_t S = std::min<uint64_t>(nb, kScreenSample);
+      l.s8 = off; off += align_up((size_t)S * bsk::tc_kpad(N));
+      l.pabs = off; off += align_up((size_t)na * S * 4);
+      l.ts = off; off += align_up((size_t)na * 4 * 8);
+      l.tsuf = off; off += align_up((size_t)na * (N + 1) * 4 * 2);
+      l.lcnt = off; off += align_up((size_t)na * ((nb + 255) / 256) * 4);   // [na][db chunks]
+      l.bins = off; off += align_up((size_t)(N + 1) * 4);
+      l.perm = off; off += align_up((size_t)nb * 4);
+      l.spb = off; off += align_up((size_t)nb * 4);
     }
   }
   if (tc) {
@@ -455,6 +480,39 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
   const int32_t* pab = nullptr;
   if (ndb > 0 && use_tc_pab(N, nq, ndb, k)) {
     uint8_t* q8 = reinterpret_cast<uint8_t*>(w + l.a8);
+    if (screen_size_ok(N, nq, ndb, k) && cache().monotone(N, d)) {
+      // fused screen (K4d): the table region holds the survivor lists, b8 the sorted db
+      uint8_t* d8 = reinterpret_cast<uint8_t*>(w + l.b8);
+      uint2* lists = reinterpret_cast<uint2*>(w + l.pab);
+      int32_t* perm = reinterpret_cast<int32_t*>(w + l.perm);
+      int32_t* spb = reinterpret_cast<int32_t*>(w + l.spb);
+      uint8_t* s8 = reinterpret_cast<uint8_t*>(w + l.s8);
+      int32_t* pabs = reinterpret_cast<int32_t*>(w + l.pabs);
+      double* ts = reinterpret_cast<double*>(w + l.ts);
+      uint16_t* tsuf = reinterpret_cast<uint16_t*>(w + l.tsuf);
+      uint32_t* lcnt = reinterpret_cast<uint32_t*>(w + l.lcnt);
+      int32_t* range = reinterpret_cast<int32_t*>(w + l.range);
+      unsigned long long* ctr = reinterpret_cast<unsigned long long*>(w + l.ctr);
+      const double* Ld = reinterpret_cast<const double*>(w + l.L);
+      const uint32_t S = (uint32_t)std::min<uint64_t>(ndb, kScreenSample);
+      const uint32_t nmp = nm == 3 ? 4u : nm;
+      e = bsk::launch_expand(queries, nq, N, q8, s);
+      if (e == cudaSuccess)
+        e = bsk::launch_sort_by_popcount(pd, ndb, N, reinterpret_cast<uint32_t*>(w + l.bins), perm, spb, s, false);
+      if (e == cudaSuccess) e = bsk::launch_expand(db, ndb, N, d8, s, perm);
+      if (e == cudaSuccess) e = bsk::launch_expand(db, S, N, s8, s);
+      if (e == cudaSuccess) e = bsk::launch_tc_andpopc(q8, nq, s8, S, N, pabs, ctr, s);
+      if (e == cudaSuccess) e = bsk::launch_int_range(pd, ndb, range, s);
+      if (e == cudaSuccess)
+        e = bsk::launch_screen_threshold(pabs, nq, S, N, measure, k, flags, pq, pd, Ld, range, tsuf, ts, s);
+      uint32_t splits = 0, seg_cols = 0;
+      if (e == cudaSuccess)
+        e = bsk::launch_tc_screen(q8, nq, d8, ndb, N, spb, perm, tsuf, nmp, lists, lcnt, ctr, splits, seg_cols, s);
+      if (e == cudaSuccess)
+        e = bsk::launch_topk_list(lists, lcnt, splits, seg_cols, nq, ndb, N, measure, k, flags, pq, spb, perm, Ld,
+                                  ts, w + l.scratch, out_idx, out_score, s);
+      return cuda_status(e);
+    }
     uint8_t* d8 = self ? q8 : reinterpret_cast<uint8_t*>(w + l.b8);
     int32_t* pabw = reinterpret_cast<int32_t*>(w + l.pab);
     e = bsk::launch_expand(queries, nq, N, q8, s);

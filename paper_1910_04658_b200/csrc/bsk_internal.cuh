@@ -63,6 +63,12 @@ cudaError_t launch_topk(const uint32_t* Q, uint64_t nq, const uint32_t* D, uint6
                         int32_t* out_idx, float* out_score, cudaStream_t s,
                         const int32_t* pab = nullptr);   // pab[nq][ndb] precomputed (tensor cores) or null
 
+// lcnt: [na][ceil(nb / 256)] at least; returns the db chunks (list segments) per row and the
+// columns per chunk (segment sp of row r starts at lists[r * nb + sp * seg_cols]).
+cudaError_t launch_tc_screen(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
+                             const int32_t* spb, const int32_t* perm, const uint16_t* tsuf, uint32_t nmp, uint2* lists,
+                             uint32_t* lcnt, unsigned long long* ctr, uint32_t& splits, uint32_t& seg_cols,
+                             cudaStream_t s);
 // Top-k of every measure in `mask` from the pab table: sampled and screened histograms set an
 // integer screen pab >= T[pb] (per-query minimum-pab tables), then the survivors are ranked
 // exactly (K4c). pd_range: 2 int32 of workspace. Requires topk_pab3_fits and L
@@ -73,6 +79,22 @@ size_t topk_pab3_scratch_bytes(uint32_t mask);
 cudaError_t launch_topk_pab3(const int32_t* pab, uint64_t nq, uint64_t ndb, uint32_t N, uint32_t mask, uint32_t k,
                              uint32_t flags, const int32_t* pq, const int32_t* pd, const double* L, int32_t* pd_range,
                              void* scratch, int32_t* out_idx, float* out_score, cudaStream_t s);
+
+// Fused-screen top-k (K4d): per query the sample threshold t_s and the suffix-min
+// minimum-pab tables tsuf[nq][N + 1][nmp] (nmp = popcount(mask), 4 for 3) from the sample's
+// AND-popcounts pab_s[nq][S] (the db rows [0, S) in their own order, popcounts pd[0, S));
+// the tensor-core screen (launch_tc_screen) appends survivors to per-row lists; the list
+// top-k ranks them exactly.
+size_t screen_threshold_smem(uint32_t N, uint32_t nm, uint32_t S);
+cudaError_t launch_screen_threshold(const int32_t* pab_s, uint64_t nq, uint32_t S, uint32_t N, uint32_t mask,
+                                    uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* pd, const double* L,
+                                    const int32_t* pd_range, uint16_t* tsuf, double* ts, cudaStream_t s);
+cudaError_t launch_topk_list(const uint2* lists, const uint32_t* lcnt, uint32_t splits, uint32_t seg_cols,
+                             uint64_t nq, uint64_t ndb, uint32_t N,
+                             uint32_t mask, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* spb,
+                             const int32_t* perm, const double* L, const double* ts, void* scratch, int32_t* out_idx,
+                             float* out_score, cudaStream_t s);   // scratch: topk_pab3_scratch_bytes(15)
+cudaError_t launch_int_range(const int32_t* x, uint64_t n, int32_t* out, cudaStream_t s);
 
 // Tensor-core pair engine (tc.cu): sketches widened to {0,1} bytes, rows padded to
 // tc_kpad(N) bytes (multiple of 128), then tcgen05 kind::i8 all-pairs.

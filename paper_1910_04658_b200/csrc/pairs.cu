@@ -1119,6 +1119,16 @@ extern "C" void bsk_pabt_stats(unsigned long long* out) {
 namespace bsk {
 #endif
 
+cudaError_t launch_int_range(const int32_t* x, uint64_t n, int32_t* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(out, 0x7f, 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(out + 1, 0x80, 4, s);
+  if (e != cudaSuccess) return e;
+  int_range_kernel<<<(unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms()), 256, 0, s>>>(x, n, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
 static size_t topk_pab3_smem(uint32_t N, uint32_t nm) {
   const size_t h = std::max<size_t>((size_t)nm * kHB * 4, (size_t)nm * kPab3Cap * 12);
   return h + (((size_t)(nm == 3 ? 4 : nm) * (N + 1) * 2 + 15) & ~(size_t)15) +
@@ -1173,6 +1183,550 @@ cudaError_t launch_topk_pab3(const int32_t* pab, uint64_t nq, uint64_t ndb, uint
     case 3: return launch_topk_pab3_t<3>(pab, nq, ndb, N, mask, k, flags, pq, pd, L, pd_range, scratch, out_idx, out_score, s);
     default: return launch_topk_pab3_t<4>(pab, nq, ndb, N, mask, k, flags, pq, pd, L, pd_range, scratch, out_idx, out_score, s);
   }
+}
+
+// ------------------------------------- fused screen: thresholds + survivor lists (K4d) --
+// Shared pieces of the two kernels around the tensor-core screen (tc.cu kTcScreen).
+struct ListHist {   // kHB-bucket histogram of keys over [lo, lo + kHB / sc)
+  __device__ static int bucket(double key, double lo, double sc) {
+    const double x = (key - lo) * sc;
+    return x <= 0.0 ? 0 : (x >= (double)(kHB - 1) ? kHB - 1 : (int)x);
+  }
+  // a lower bound of the k-th key from a selected bucket h (> 0): its lower edge less a margin
+  __device__ static double edge(int h, double lo, double sc) {
+    if (h <= 0 || !(sc > 0.0)) return -__longlong_as_double(0x7ff0000000000000LL);
+    const double e = lo + (double)h / sc;
+    return e - 1e-12 * fmax(1.0, fmax(fabs(e), fabs(lo)));
+  }
+};
+
+// The recipe's IP part (estimate_pair's exact fp64 operations) and, from it, every key: IP and -HAM
+// exactly, JS and COS within kApproxEps (fp32 quotient of the recipe's fp64 operands: fast
+// division / reciprocal square root, keys in [0, 1]). Used only to set thresholds and to skip
+// pairs that cannot reach one (with the margin); every ranked key is the exact one.
+constexpr double kApproxEps = 4e-6;
+__device__ __forceinline__ double approx_key(int pa, int pb, int pab, int N, const double* __restrict__ L, uint32_t m) {
+  const int pu = pa + pb - pab;
+  const double La = L[pa], Lb = L[pb];
+  const double S = __dadd_rn(La, Lb);
+  double ip = 0.0;
+  if (!(pu == N && pa < N && pb < N)) {
+    const double raw = __dsub_rn(S, L[pu]);
+    const double lo = raw > 0.0 ? raw : 0.0;
+    const double cap = La < Lb ? La : Lb;
+    ip = lo < cap ? lo : cap;
+  }
+  if (m == 1u) return ip;
+  if (m == 2u) {
+    double h = __dsub_rn(S, __dmul_rn(2.0, ip));
+    h = h > 0.0 ? h : 0.0;
+    return -(h < S ? h : S);
+  }
+  float v;
+  if (m == 4u) v = (pa == 0 && pb == 0) ? 1.0f : __fdividef((float)ip, (float)__dsub_rn(S, ip));
+  else v = (pa == 0 || pb == 0) ? 0.0f : (float)ip * rsqrtf((float)La * (float)Lb);
+  return (double)fminf(fmaxf(v, 0.0f), 1.0f);
+}
+__device__ __forceinline__ double approx_eps(uint32_t m) { return m >= 4u ? kApproxEps : 0.0; }
+
+// Highest bucket h with >= k counts in buckets >= h, or -1 (block-wide, 256 threads; thread t owns
+// buckets [kHB - 8(t+1), kHB - 8t), scanned from the top). warp_sum: 8 words, found: 1 word.
+__device__ int block_select_bucket(const uint32_t* hm, uint32_t k, uint32_t* warp_sum, int* found) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int top = kHB - 8 * (int)threadIdx.x;
+  uint32_t loc = 0;
+#pragma unroll
+  for (int j = 1; j <= 8; ++j) loc += hm[top - j];
+  uint32_t inc = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+  if (lane == 31) warp_sum[warp] = inc;
+  if (threadIdx.x == 0) *found = -1;
+  __syncthreads();
+  uint32_t before_w = 0;
+  for (int w = 0; w < warp; ++w) before_w += warp_sum[w];
+  const uint32_t excl = before_w + inc - loc;
+  if (excl < k && excl + loc >= k) {
+    uint32_t run = excl;
+    for (int j = 1; j <= 8; ++j) {
+      run += hm[top - j];
+      if (run >= k) { *found = top - j; break; }
+    }
+  }
+  __syncthreads();
+  const int h = *found;
+  __syncthreads();
+  return h;
+}
+
+// Per query row (one block, grid-stride): exact keys of the sample pab row [S] (the first S db
+// rows) into a kHB-bucket histogram over each measure's key range; t_s = the lower edge of the
+// highest bucket with >= k sample pairs at or above it (as K4c pass 1: >= k pairs of the row reach
+// it, so it is a lower bound of the row's k-th key); the minimum-pab table
+// T_{t_s}[pb] over the db's popcount range, then its suffix minimum Tsuf[pb] = min_{pb' >= pb}
+// T[pb'] (a tile of the popcount-sorted db with smallest |b_s| = lo holds no pair with
+// pab < Tsuf[lo] whose key reaches t_s) -> tsuf[row][pb][NMP], ts[measure][row].
+template <int NM>
+__global__ void __launch_bounds__(256)
+screen_threshold_kernel(const int32_t* __restrict__ pab_s, uint64_t nq, uint32_t S, uint32_t N, uint32_t mask,
+                        uint32_t k, uint32_t flags, const int32_t* __restrict__ pq, const int32_t* __restrict__ pd,
+                        const double* __restrict__ L, const int32_t* __restrict__ pdr, uint16_t* __restrict__ tsuf,
+                        double* __restrict__ ts) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int NMP = NM == 3 ? 4 : NM;
+  uint32_t ms[NM];
+  {
+    uint32_t mm = mask;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) { ms[i] = mm & (0u - mm); mm &= mm - 1; }
+  }
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);                          // [NM][kHB]
+  uint16_t* T = reinterpret_cast<uint16_t*>(smem + (size_t)NM * kHB * 4);       // [range][NM]
+  __shared__ uint32_t warp_sum[8];
+  __shared__ int found;
+  __shared__ double lo_s[NM], sc_s[NM], t_s[NM];
+  __shared__ uint32_t wmin[NM][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pdlo = pdr[0], pdhi = pdr[1];
+  const int R = pdhi - pdlo + 1;
+  const double kNegInf = -__longlong_as_double(0x7ff0000000000000LL);
+  for (uint64_t r = blockIdx.x; r < nq; r += gridDim.x) {
+    const int pa = pq[r];
+    const double La = L[pa];
+    const double Lbmax = fmax(L[pdhi], L[pdhi < (int)N ? pdhi : (int)N - 1]);
+#ifdef BSK_PABT_STATS
+    long long tq = clock64();
+#define TPH(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); PABT_ADD(i, t_ - tq); tq = t_; } } while (0)
+#else
+#define TPH(i) ((void)0)
+#endif
+    for (uint32_t i = threadIdx.x; i < NM * kHB; i += blockDim.x) hist[i] = 0u;
+    if (threadIdx.x < NM) {
+      uint32_t m = ms[0];
+#pragma unroll
+      for (int i = 1; i < NM; ++i) m = threadIdx.x == (unsigned)i ? ms[i] : m;
+      const double lo = m == 2u ? -(La + Lbmax) : 0.0;
+      const double hi = m == 1u ? La : (m == 2u ? 0.0 : 1.0);
+      lo_s[threadIdx.x] = lo;
+      sc_s[threadIdx.x] = (hi > lo && hi - lo < 1e300) ? (double)kHB / (hi - lo) : 0.0;
+    }
+    __syncthreads();
+    const int32_t* row = pab_s + r * S;
+    // four columns per thread and step, loads and key evaluations independent (ILP), then the
+    // histogram updates
+    for (uint32_t c0 = threadIdx.x; c0 < S; c0 += 4 * blockDim.x) {
+      int v[4], pb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t c = c0 + u * blockDim.x;
+        v[u] = c < S ? __ldcs(row + c) : 0;
+        pb[u] = c < S ? __ldg(pd + c) : 0;   // the sample: db rows [0, S) in their own order
+      }
+      int bk[4][NM];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int mi = 0; mi < NM; ++mi)
+          bk[u][mi] = ListHist::bucket(approx_key(pa, pb[u], v[u], (int)N, L, ms[mi]), lo_s[mi], sc_s[mi]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t c = c0 + u * blockDim.x;
+        if (c < S && !((flags & 1u) && c == r))
+#pragma unroll
+          for (int mi = 0; mi < NM; ++mi) atomicAdd(hist + mi * kHB + bk[u][mi], 1u);
+      }
+    }
+    __syncthreads();
+    TPH(10);
+#pragma unroll
+    for (int mi = 0; mi < NM; ++mi) {
+      const double t = ListHist::edge(block_select_bucket(hist + mi * kHB, k, warp_sum, &found), lo_s[mi], sc_s[mi]);
+      if (threadIdx.x == 0) t_s[mi] = t - approx_eps(ms[mi]);   // (the histogram holds approximate keys)
+    }
+    __syncthreads();
+    TPH(11);
+    // T over the popcount range, then its suffix minimum: thread t owns the contiguous chunk
+    // [t * per, (t+1) * per); chunk minima combined by a reverse scan across the block
+    for (int i = threadIdx.x; i < R; i += blockDim.x)
+#pragma unroll
+      for (int mi = 0; mi < NM; ++mi)
+        T[i * NM + mi] = t_s[mi] == kNegInf ? (uint16_t)0 : min_pab(pa, pdlo + i, (int)N, L, ms[mi], t_s[mi], 0);
+    __syncthreads();
+    TPH(12);
+    const int per = (R + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int c0 = (int)threadIdx.x * per, c1 = min(R, c0 + per);
+    uint32_t later[NM];   // min over the chunks after this thread's
+#pragma unroll
+    for (int mi = 0; mi < NM; ++mi) {
+      uint32_t mn = 0xFFFFu;
+      for (int i = c1 - 1; i >= c0; --i) mn = min(mn, (uint32_t)T[i * NM + mi]);
+      uint32_t x = mn;   // inclusive suffix minimum within the warp
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_down_sync(0xffffffffu, x, o); if (lane + o < 32) x = min(x, y); }
+      if (lane == 0) wmin[mi][warp] = x;
+      const uint32_t nxt = __shfl_down_sync(0xffffffffu, x, 1);
+      later[mi] = lane < 31 ? nxt : 0xFFFFu;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int mi = 0; mi < NM; ++mi)
+      for (int w = warp + 1; w < 8; ++w) later[mi] = min(later[mi], wmin[mi][w]);
+    uint16_t* out = tsuf + (size_t)r * (N + 1) * NMP;
+#pragma unroll
+    for (int mi = 0; mi < NM; ++mi) {
+      uint32_t run = later[mi];
+      for (int i = c1 - 1; i >= c0; --i) {
+        run = min(run, (uint32_t)T[i * NM + mi]);
+        out[(size_t)(pdlo + i) * NMP + mi] = (uint16_t)run;
+      }
+    }
+    if (threadIdx.x < NM) ts[(size_t)threadIdx.x * nq + r] = t_s[threadIdx.x];
+    if (NMP > NM)   // (NM = 3: the fourth entry never screens anything out)
+      for (int i = threadIdx.x; i < R; i += blockDim.x) out[(size_t)(pdlo + i) * NMP + 3] = 0xFFFFu;
+    __syncthreads();
+    TPH(13);
+  }
+}
+#undef TPH
+
+size_t screen_threshold_smem(uint32_t N, uint32_t nm, uint32_t S) {
+  (void)S;
+  return (size_t)nm * kHB * 4 + (size_t)(N + 1) * nm * 2;
+}
+
+cudaError_t launch_screen_threshold(const int32_t* pab_s, uint64_t nq, uint32_t S, uint32_t N, uint32_t mask,
+                                    uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* pd, const double* L,
+                                    const int32_t* pd_range, uint16_t* tsuf, double* ts, cudaStream_t s) {
+  if (nq == 0) return cudaSuccess;
+  const uint32_t nm = (uint32_t)__builtin_popcount(mask & 15u);
+  const size_t smem = screen_threshold_smem(N, nm, S);
+  const unsigned grid = (unsigned)std::min<uint64_t>(nq, (uint64_t)num_sms() * 8);
+  cudaError_t e = cudaSuccess;
+#define BSK_SCREEN_T(NMV)                                                                                       \
+  do {                                                                                                          \
+    e = cudaFuncSetAttribute(screen_threshold_kernel<NMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                             \
+    screen_threshold_kernel<NMV><<<grid, 256, smem, s>>>(pab_s, nq, S, N, mask & 15u, k, flags, pq, pd, L,    \
+                                                         pd_range, tsuf, ts);                                   \
+  } while (0)
+  switch (nm) {
+    case 1: BSK_SCREEN_T(1); break;
+    case 2: BSK_SCREEN_T(2); break;
+    case 3: BSK_SCREEN_T(3); break;
+    default: BSK_SCREEN_T(4); break;
+  }
+#undef BSK_SCREEN_T
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Per query row (one block, grid-stride): its screen survivors (sorted db position, pab) from the
+// tensor-core screen, ranked exactly for every measure. Pass A: each thread walks a contiguous run
+// of the row's list (its segments seen as one index range), four entries at a time with their
+// loads issued together, scores them (exact fp64 recipe), histograms the keys that reach t_s over
+// [t_s, key max] and keeps (key, db index) of those in the block's scratch slot; t0 (a lower
+// bound of the k-th key) from the histogram. Pass B: the kept pairs reaching t0 that beat the
+// running k-th go to a 512-entry buffer, which a warp per measure sorts at the end. A slot
+// overflow makes pass B re-score the list; a buffer overflow restarts pass B in 256-entry steps
+// with a barrier each, cutting the buffer back to k (block bitonic sort) when it could overflow.
+template <int NM>
+__global__ void __launch_bounds__(256)
+topk_list_kernel(const uint2* __restrict__ lists, const uint32_t* __restrict__ lcnt, uint32_t splits,
+                 uint32_t seg_cols, uint64_t nq, uint64_t ndb,
+                 uint32_t N, uint32_t mask, uint32_t k, uint32_t flags, const int32_t* __restrict__ pq,
+                 const int32_t* __restrict__ spb, const int32_t* __restrict__ perm, const double* __restrict__ L,
+                 const double* __restrict__ ts, double* __restrict__ skey, int32_t* __restrict__ sidx,
+                 int32_t* __restrict__ out_idx, float* __restrict__ out_score) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t ms[NM];
+  {
+    uint32_t mm = mask;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) { ms[i] = mm & (0u - mm); mm &= mm - 1; }
+  }
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);                        // [NM][kHB] (pass A)
+  double* bkey = reinterpret_cast<double*>(smem);                            // [NM][kPab3Cap] (pass B)
+  int* bidx = reinterpret_cast<int*>(smem + (size_t)NM * kPab3Cap * 8);
+  const size_t hb = (size_t)NM * kHB * 4 > (size_t)NM * kPab3Cap * 12 ? (size_t)NM * kHB * 4 : (size_t)NM * kPab3Cap * 12;
+  uint32_t* segp = reinterpret_cast<uint32_t*>(smem + hb);                   // [splits + 1]
+  __shared__ uint32_t cnt[NM], kcnt[NM];
+  __shared__ double tk[NM];
+  __shared__ int ti[NM];
+  __shared__ double lo_s[NM], sc_s[NM], tl_s[NM];
+  __shared__ uint32_t warp_sum[8];
+  __shared__ int found;
+  __shared__ int ovf;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double kNegInf = -__longlong_as_double(0x7ff0000000000000LL);
+  double* sk = skey + (size_t)blockIdx.x * NM * kPab3Keep;                   // this block's slot
+  int32_t* si = sidx + (size_t)blockIdx.x * NM * kPab3Keep;
+  for (uint64_t r = blockIdx.x; r < nq; r += gridDim.x) {
+    const int pa = pq[r];
+    const double La = L[pa];
+    const uint2* lst = lists + r * ndb;
+    const uint32_t* cnts = lcnt + r * splits;
+    // the row's list segments (segment sp: up to seg_cols entries from sp * seg_cols) as one flat
+    // index range: exclusive prefix sums of the segment counts in shared memory (warp 0)
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t run = 0;
+      for (uint32_t b = 0; b < splits; b += 32) {
+        const uint32_t x = b + lane < splits ? cnts[b + lane] : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += y; }
+        if (b + lane < splits) segp[b + lane] = run + inc - x;
+        run += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) segp[splits] = run;
+    }
+    if (threadIdx.x < NM) {
+      uint32_t m = ms[0];
+#pragma unroll
+      for (int i = 1; i < NM; ++i) m = threadIdx.x == (unsigned)i ? ms[i] : m;
+      const double t = ts[(size_t)threadIdx.x * nq + r];
+      const double hi = m == 1u ? La : (m == 2u ? 0.0 : 1.0);
+      // (keys below lo land in bucket 0, which never yields a bound: any lo is safe)
+      const double lo = t != kNegInf ? t : (m == 2u ? -(La + fmax(L[N], L[N - 1])) : 0.0);
+      tl_s[threadIdx.x] = t;
+      lo_s[threadIdx.x] = lo;
+      sc_s[threadIdx.x] = (hi > lo && hi - lo < 1e300) ? (double)kHB / (hi - lo) : 0.0;
+      kcnt[threadIdx.x] = 0;
+    }
+    for (uint32_t i = threadIdx.x; i < NM * kHB; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    const uint32_t total = segp[splits];
+#ifdef BSK_PABT_STATS
+    long long tq = clock64();
+    if (threadIdx.x == 0) { PABT_ADD(0, 1); PABT_ADD(1, total); }
+#define LPH(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); PABT_ADD(i, t_ - tq); tq = t_; } } while (0)
+#else
+#define LPH(i) ((void)0)
+#endif
+    // thread t's run [t * per_t, ...): locate its first segment once, then step through
+    const uint32_t per_t = (total + blockDim.x - 1) / blockDim.x;
+    const uint32_t i0 = min(total, threadIdx.x * per_t), i1 = min(total, i0 + per_t);
+    auto run_entries = [&](auto&& f) {   // f(orig, pb, pab) per entry of the run, 4 loads in flight
+      if (i0 >= i1) return;
+      uint32_t lo = 0, hi = splits;      // segp[lo] <= i0 < segp[hi]
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (segp[mid] <= i0) lo = mid;
+        else hi = mid;
+      }
+      uint32_t sp = lo, off = i0 - segp[lo];
+      for (uint32_t i = i0; i < i1; i += 4) {
+        uint2 e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          e[u] = make_uint2(0u, 0xFFFFFFFFu);
+          if (i + u < i1) {
+            while (segp[sp] + off >= segp[sp + 1]) { ++sp; off = 0; }
+            e[u] = lst[(size_t)sp * seg_cols + off];
+            ++off;
+          }
+        }
+        int orig[4], pb[4], v[4];   // entry: (original db index, |b_s| << 14 | pab)
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          orig[u] = (int)e[u].x;
+          pb[u] = (int)(e[u].y >> 14) & 0x3FFF;
+          v[u] = (int)(e[u].y & 0x3FFFu);
+          ok[u] = e[u].y != 0xFFFFFFFFu && !((flags & 1u) && (uint64_t)orig[u] == r);
+        }
+        f(ok, orig, pb, v);
+      }
+    };
+    // pass A on approximate keys (approx_key: IP / -HAM exact, JS / COS within kApproxEps): the
+    // histogram and the kept records (approximate key, pb:pab, db index) of pairs that may reach t_s
+    run_entries([&](const bool (&ok)[4], const int (&orig)[4], const int (&pb)[4], const int (&v)[4]) {
+      double key[4][NM];   // all keys of the batch first (independent chains), then the updates
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int mi = 0; mi < NM; ++mi) key[u][mi] = approx_key(pa, pb[u], v[u], (int)N, L, ms[mi]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (!ok[u]) continue;
+#pragma unroll
+        for (int mi = 0; mi < NM; ++mi) {
+          if (key[u][mi] < tl_s[mi] - approx_eps(ms[mi])) continue;
+          atomicAdd(hist + mi * kHB + ListHist::bucket(key[u][mi], lo_s[mi], sc_s[mi]), 1u);
+          const uint32_t pos = atomicAdd(&kcnt[mi], 1u);
+          if (pos < kPab3Keep) {
+            uint32_t* rec = reinterpret_cast<uint32_t*>(sk + (size_t)mi * kPab3Keep + pos);
+            rec[0] = __float_as_uint(__double2float_rd(key[u][mi]));   // (rounded down: still <= the key + eps)
+            rec[1] = ((uint32_t)pb[u] << 14) | (uint32_t)v[u];       // (pb, pab <= N <= 16383)
+            si[(size_t)mi * kPab3Keep + pos] = orig[u];
+          }
+        }
+      }
+    });
+    __syncthreads();
+    LPH(5);
+#pragma unroll
+    for (int mi = 0; mi < NM; ++mi) {
+      const double t0 = ListHist::edge(block_select_bucket(hist + mi * kHB, k, warp_sum, &found), lo_s[mi], sc_s[mi]) -
+                        approx_eps(ms[mi]);   // (the histogram holds approximate keys)
+      if (threadIdx.x == 0 && t0 > tl_s[mi]) tl_s[mi] = t0;
+    }
+    if (threadIdx.x < NM) { cnt[threadIdx.x] = 0; tk[threadIdx.x] = kNegInf; ti[threadIdx.x] = kSentinelIdx; }
+    if (threadIdx.x == 0) ovf = 0;
+    __syncthreads();   // (the buffers alias the histograms)
+    LPH(6);
+    auto collect = [&](int mi, int orig, double key) {
+      if (key < tl_s[mi] || !before(key, orig, tk[mi], ti[mi])) return;
+      const uint32_t pos = atomicAdd(&cnt[mi], 1u);
+      if (pos < (uint32_t)kPab3Cap) {
+        bkey[mi * kPab3Cap + pos] = key;
+        bidx[mi * kPab3Cap + pos] = orig;
+      } else {
+        ovf = 1;
+      }
+    };
+    auto collect_all = [&](int orig, int pb, int v) {
+#pragma unroll
+      for (int mi = 0; mi < NM; ++mi) collect(mi, orig, pab_key(pa, pb, v, (int)N, L, ms[mi]));
+    };
+    auto collect_batch = [&](const bool (&ok)[4], const int (&orig)[4], const int (&pb)[4], const int (&v)[4]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (ok[u]) collect_all(orig[u], pb[u], v[u]);
+    };
+    // sort measure mi's nb buffered candidates, keep the best k, raise (tk, ti) (block-wide)
+    auto flush = [&](int mi, uint32_t nb) {
+      double* key = bkey + mi * kPab3Cap;
+      int* idx = bidx + mi * kPab3Cap;
+      uint32_t P = 2;
+      while (P < nb) P <<= 1;
+      for (uint32_t i = nb + threadIdx.x; i < P; i += blockDim.x) { key[i] = kNegInf; idx[i] = kSentinelIdx; }
+      __syncthreads();
+      block_bitonic_sort(key, idx, (int)P);
+      const bool full = nb >= k;
+      const double nt = full ? key[k - 1] : kNegInf;
+      const int nti = full ? idx[k - 1] : kSentinelIdx;
+      __syncthreads();
+      if (threadIdx.x == 0) { cnt[mi] = full ? k : nb; tk[mi] = nt; ti[mi] = nti; }
+      __syncthreads();
+    };
+    bool kept = true;
+#pragma unroll
+    for (int mi = 0; mi < NM; ++mi) kept = kept && kcnt[mi] <= kPab3Keep;
+    if (kept) {
+#pragma unroll
+      for (int mi = 0; mi < NM; ++mi) {
+        const uint2* recs = reinterpret_cast<const uint2*>(sk + (size_t)mi * kPab3Keep);
+        const double tcut = tl_s[mi] - approx_eps(ms[mi]);
+        const uint32_t nk = kcnt[mi];
+        for (uint32_t i0 = threadIdx.x; i0 < nk; i0 += 4 * blockDim.x) {
+          uint2 rc[4];   // four records' loads in flight
+#pragma unroll
+          for (int u = 0; u < 4; ++u) rc[u] = i0 + u * blockDim.x < nk ? recs[i0 + u * blockDim.x] : make_uint2(0xFF800000u, 0u);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if ((double)__uint_as_float(rc[u].x) < tcut) continue;   // cannot reach t0
+            const uint32_t i = i0 + u * blockDim.x;
+            const int pb = (int)(rc[u].y >> 14), v = (int)(rc[u].y & 0x3FFFu);
+            collect(mi, si[(size_t)mi * kPab3Keep + i], pab_key(pa, pb, v, (int)N, L, ms[mi]));   // the exact key
+          }
+        }
+      }
+    } else {
+      run_entries(collect_batch);
+    }
+    __syncthreads();
+    LPH(7);
+    if (ovf) {   // (uniform) rare: restart pass B in barrier-separated steps over the list
+      if (threadIdx.x < NM) { cnt[threadIdx.x] = 0; tk[threadIdx.x] = kNegInf; ti[threadIdx.x] = kSentinelIdx; }
+      __syncthreads();
+      for (uint32_t c = 0; c < total; c += kPab3Slow) {
+        const uint32_t i = c + threadIdx.x;
+        if (i < total) {
+          uint32_t lo = 0, hi = splits;
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (segp[mid] <= i) lo = mid;
+            else hi = mid;
+          }
+          const uint2 e = lst[(size_t)lo * seg_cols + (i - segp[lo])];
+          const int orig = (int)e.x;
+          if (!((flags & 1u) && (uint64_t)orig == r)) collect_all(orig, (int)(e.y >> 14) & 0x3FFF, (int)(e.y & 0x3FFFu));
+        }
+        __syncthreads();
+#pragma unroll
+        for (int mi = 0; mi < NM; ++mi) {
+          const uint32_t nb = cnt[mi];
+          if (nb > (uint32_t)kPab3Cap - kPab3Slow) flush(mi, nb);
+        }
+      }
+    }
+    LPH(8);
+    // final ranking: every candidate's rank in the (key desc, index asc) order by counting (the
+    // order is strict: indices are distinct), written straight to its output slot; threads
+    // [mi * G, (mi + 1) * G) take measure mi
+    {
+      constexpr int NMP = NM == 3 ? 4 : NM;
+      constexpr uint32_t G = 256 / NMP;
+      const int mi = (int)(threadIdx.x / G);
+      if (mi < NM) {
+        uint32_t m = ms[0];
+#pragma unroll
+        for (int i = 1; i < NM; ++i) m = mi == i ? ms[i] : m;
+        const double* key = bkey + mi * kPab3Cap;
+        const int* idx = bidx + mi * kPab3Cap;
+        const uint32_t nb = min(cnt[mi], (uint32_t)kPab3Cap);
+        if (threadIdx.x % G == 0) PABT_ADD(3, nb);
+        const size_t ob = (size_t)mi * nq * k + r * k;
+        for (uint32_t c = threadIdx.x % G; c < nb; c += G) {
+          const double kc = key[c];
+          const int ic = idx[c];
+          uint32_t rank = 0;
+          for (uint32_t j = 0; j < nb; ++j) rank += before(key[j], idx[j], kc, ic) ? 1u : 0u;
+          if (rank < k) { out_idx[ob + rank] = ic; out_score[ob + rank] = key_to_score(kc, m); }
+        }
+        for (uint32_t q = nb + threadIdx.x % G; q < k; q += G) { out_idx[ob + q] = -1; out_score[ob + q] = __int_as_float(0x7fc00000); }
+      }
+    }
+    __syncthreads();
+    LPH(9);
+  }
+}
+#undef LPH
+
+cudaError_t launch_topk_list(const uint2* lists, const uint32_t* lcnt, uint32_t splits, uint32_t seg_cols,
+                             uint64_t nq, uint64_t ndb, uint32_t N,
+                             uint32_t mask, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* spb,
+                             const int32_t* perm, const double* L, const double* ts, void* scratch_v, int32_t* out_idx,
+                             float* out_score, cudaStream_t s) {
+  unsigned char* scratch = static_cast<unsigned char*>(scratch_v);   // topk_pab3_scratch_bytes(15) (slots)
+  if (nq == 0 || k == 0) return cudaSuccess;
+  const uint32_t nm = (uint32_t)__builtin_popcount(mask & 15u);
+  const size_t smem = std::max<size_t>((size_t)nm * kHB * 4, (size_t)nm * kPab3Cap * 12) + ((size_t)splits + 1) * 4;
+  int bps = 0;
+  cudaError_t e = cudaSuccess;
+#define BSK_LIST_T(NMV)                                                                                          \
+  do {                                                                                                           \
+    e = cudaFuncSetAttribute(topk_list_kernel<NMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    if (e != cudaSuccess) return e;                                                                              \
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, topk_list_kernel<NMV>, 256, smem) != cudaSuccess ||  \
+        bps < 1)                                                                                                 \
+      bps = 1;                                                                                                   \
+    topk_list_kernel<NMV><<<(unsigned)std::min<uint64_t>({nq, (uint64_t)num_sms() * bps, (uint64_t)kPab3Slots}),  \
+                            256, smem, s>>>(lists, lcnt, splits, seg_cols, nq, ndb, N, mask & 15u, k, flags, pq, spb, \
+                                            perm, L, ts, reinterpret_cast<double*>(scratch),                      \
+                                            reinterpret_cast<int32_t*>(scratch + (size_t)kPab3Slots * NMV * kPab3Keep * 8), \
+                                            out_idx, out_score);                                                  \
+  } while (0)
+  switch (nm) {
+    case 1: BSK_LIST_T(1); break;
+    case 2: BSK_LIST_T(2); break;
+    case 3: BSK_LIST_T(3); break;
+    default: BSK_LIST_T(4); break;
+  }
+#undef BSK_LIST_T
+  count_launch();
+  return cudaGetLastError();
 }
 
 // Top-k from a precomputed AND-popcount table pab[nq][ndb] (tensor cores): one warp per

@@ -351,7 +351,11 @@ __global__ void pb_scatter_kernel(const int32_t* __restrict__ pb, uint64_t n, ui
 constexpr int kTcM = 128, kTcN = 256;
 constexpr int kTcAcc = 512 / kTcN;   // TMEM accumulators (512 columns)
 constexpr uint32_t kTcSmemMax = 227 * 1024;
-enum TcMode { kTcAndPopc = 0, kTcEstimate = 1, kTcTopk = 2, kTcJoin = 3, kTcTopkT = 4 };
+enum TcMode { kTcAndPopc = 0, kTcEstimate = 1, kTcTopk = 2, kTcJoin = 3, kTcTopkT = 4, kTcScreen = 5 };
+// kTcScreen: the AND-popcount with an integer screen in the epilogue instead of the table store:
+// per (query row, 256-wide tile of the popcount-sorted db) pmin = the suffix minimum of the row's
+// minimum-pab tables at the tile's smallest |b_s| (K4d), and every pair with pab >= pmin
+// is appended (original db index, |b_s| << 14 | pab) to the row's survivor list.
 // kTcTopkT: the fused top-k with the query tile A resident in TMEM (columns [0, Kp/4), Kp <= 1024)
 // for the whole work item and 128-wide db tiles (two 128-column accumulators after it): only B
 // streams through shared memory, so each MMA's operand traffic drops from A + B to B.
@@ -398,6 +402,10 @@ struct TcParams {
   uint32_t chain;         // kTcTopk: heaps persist across chunks in part_key/idx (one list per row)
   unsigned int* done;     // kTcTopk chained: per m-tile count of finished (chunk, epilogue warp) pairs
   int32_t* out_i32;       // kTcAndPopc: int32 [na][nb]
+  const uint16_t* tsuf;   // kTcScreen: suffix-min minimum-pab tables [na][N + 1][nmp] (u16)
+  uint32_t nmp;           // kTcScreen: table entries per (row, pb)
+  uint2* lists;           // kTcScreen: survivors [na][nb] (original db index, |b_s| << 14 | pab)
+  uint32_t* lcnt;         // kTcScreen: survivors per (row, db chunk) [na][splits]
   float* out_f32;         // kTcEstimate: float [popcount(measure)][na][nb]
   uint32_t measure, N, k, flags, prefilter;
   const int32_t* pa;      // |a_s| per A row
@@ -1195,8 +1203,29 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const uint64_t r0 = mt * kTcM + lb;             // first row of this warp's quadrant
       const uint32_t nrows = r0 < p.na ? (uint32_t)min((uint64_t)32, p.na - r0) : 0u;
       const bool vec_rows = (p.nb & 3u) == 0 && (reinterpret_cast<uintptr_t>(p.out_f32) & 15u) == 0;
+      // kTcScreen: this row's survivors of the item's db chunk go to the list segment that starts
+      // at the chunk's first column (a chunk of w columns holds at most w survivors of a row), so
+      // the lane appends with a private counter — no atomics — and stores the count at item end
+      uint32_t lc = 0;
+      const uint64_t lbase = (uint64_t)nt0 * kTcN;
       for (uint32_t nt = nt0; nt < nt1; ++nt) {
         const uint64_t n0 = (uint64_t)nt * kTcN;
+        uint32_t pmin = 0xFFFFFFFFu;   // kTcScreen: this row's screen for the tile (none for padding rows)
+        int2* tmeta_w = reinterpret_cast<int2*>(extra) + (size_t)ew * kTcN;   // kTcScreen: per warp
+        if constexpr (MODE == kTcScreen) {
+          // the tile's (original index, |b_s|) per column into this warp's shared buffer while the
+          // MMA runs (survivors then carry them: the list top-k needs no gathers)
+          for (uint32_t c = (uint32_t)lane; c < kTcN; c += 32) {
+            const uint64_t col = n0 + c;
+            tmeta_w[c] = col < p.nb ? make_int2(__ldg(p.perm + col), __ldg(p.pb + col)) : make_int2(0, 0);
+          }
+          __syncwarp();
+          if (valid && n0 < p.nb) {
+            const uint32_t lo = (uint32_t)tmeta_w[0].y;   // the tile's smallest |b_s| (ascending sort)
+            const uint16_t* t = p.tsuf + ((size_t)r * (p.N + 1) + lo) * p.nmp;
+            for (uint32_t i = 0; i < p.nmp; ++i) pmin = min(pmin, (uint32_t)__ldg(t + i));
+          }
+        }
         tc::mbar_wait(tfull(acc), aphase);
         tc::fence_after();
 #pragma unroll 1
@@ -1207,6 +1236,23 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           if (n0 + c >= p.nb || nrows == 0) continue;    // warp-uniform
           const uint64_t cb = n0 + c;
           const uint32_t left = (uint32_t)min((uint64_t)CW, p.nb - cb);
+          if constexpr (MODE == kTcScreen) {
+            uint32_t sm = 0;
+#pragma unroll
+            for (int j = 0; j < CW; ++j) sm |= ((uint32_t)j < left && v[j] >= pmin ? 1u : 0u) << j;
+            if (sm) {
+              uint64_t pos = lbase + lc;
+              lc += (uint32_t)__popc(sm);
+              uint2* o = p.lists + r * p.nb;
+#pragma unroll
+              for (int j = 0; j < CW; ++j)
+                if ((sm >> j) & 1u) {   // (original db index, |b_s| << 14 | pab): N <= 16383
+                  const int2 mt_ = tmeta_w[c + (uint32_t)j];
+                  o[pos++] = make_uint2((uint32_t)mt_.x, ((uint32_t)mt_.y << 14) | v[j]);
+                }
+            }
+            continue;
+          }
           if (MODE == kTcAndPopc) {
 #pragma unroll
             for (int j = 0; j < CW; ++j) tr[lane * (CW + 1) + j] = v[j];
@@ -1280,6 +1326,8 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         release_acc(acc);
         if (++acc == kTcAcc) { acc = 0; aphase ^= 1u; }
       }
+      if constexpr (MODE == kTcScreen)
+        if (valid) p.lcnt[r * p.splits + sp] = lc;
     }
   }
 #ifdef BSK_TOPK_PROF
@@ -1380,7 +1428,7 @@ template <int MODE>
 static int tc_cg(uint32_t Kp) {
   if (MODE == kTcTopkT) return 1;
   if (const char* e = std::getenv("BINSKETCH_TC_CG")) return std::atoi(e) == 2 ? 2 : 1;
-  return (Kp >= 16384u || (MODE == kTcAndPopc && Kp >= 4096u)) ? 2 : 1;
+  return (Kp >= 16384u || ((MODE == kTcAndPopc || MODE == kTcScreen) && Kp >= 4096u)) ? 2 : 1;
 }
 
 // Shared launcher: pick ring depth from the shared memory left after `extra_bytes`, build
@@ -1470,6 +1518,23 @@ cudaError_t launch_tc_andpopc(const uint8_t* A8, uint64_t na, const uint8_t* B8,
   TcParams p = {};
   p.na = na; p.nb = nb; p.N = N; p.out_i32 = out; p.item_ctr = ctr;
   return tc_launch<kTcAndPopc, 128>(A8, B8, p, N, TcRoles<kTcAndPopc>::kEpi * 4 * 32 * (TcRoles<kTcAndPopc>::kCW + 1), 0, s);   // transposes
+}
+
+cudaError_t launch_tc_screen(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,
+                             const int32_t* spb, const int32_t* perm, const uint16_t* tsuf, uint32_t nmp, uint2* lists,
+                             uint32_t* lcnt, unsigned long long* ctr, uint32_t& splits, uint32_t& seg_cols,
+                             cudaStream_t s) {
+  splits = 0;
+  seg_cols = 0;
+  if (na == 0 || nb == 0) return cudaSuccess;
+  TcParams p = {};
+  p.na = na; p.nb = nb; p.N = N; p.pb = spb; p.perm = perm; p.tsuf = tsuf; p.nmp = nmp; p.lists = lists;
+  p.lcnt = lcnt;
+  p.item_ctr = ctr;
+  const cudaError_t e = tc_launch<kTcScreen, 128>(A8, B8, p, N, TcRoles<kTcScreen>::kEpi * kTcN * 8, 0, s);   // tile metadata
+  splits = p.splits;
+  seg_cols = p.per * kTcN;   // list segment sp starts at column sp * seg_cols
+  return e;
 }
 
 cudaError_t launch_tc_estimate(const uint8_t* A8, uint64_t na, const uint8_t* B8, uint64_t nb, uint32_t N,

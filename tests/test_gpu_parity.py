@@ -447,17 +447,19 @@ def test_topk_pab_single_split_direct_outputs(measure, monkeypatch):
     _check_topk(Q, D, N, d, measure, 100)
 
 
-@pytest.mark.parametrize("screen", ["1", "0"])
-def test_topk_pab_screen_paths(screen, monkeypatch):
-    """The pab-table top-k (k > 64 or N > 6143): the integer-screen kernel (sampled + screened
-    histograms, survivors kept in scratch; K4c) and the pre-test kernel it replaces
-    (BINSKETCH_PAB_SCREEN=0) on the cases that leave the common path: a query whose 700 exact
-    copies in the db all tie above its threshold (pass-3 buffer overflow -> barrier-stepped
-    re-walk), one with 9000 copies (pass-2 survivors beyond the scratch slot -> screened re-walk),
-    an empty query row, an unaligned db (ndb % 4 != 0: register path), self exclusion, every
-    measure alone and all four together."""
+@pytest.mark.parametrize("path", ["fused-screen", "pab-screen", "pab-pretest"])
+def test_topk_pab_screen_paths(path, monkeypatch):
+    """Top-k beyond the fused kernel (k > 64 or N > 6143): the fused tensor-core screen with
+    survivor lists (K4d), the pab-table integer-screen kernel (K4c,
+    BINSKETCH_TOPK_SCREEN=0) and the pab-table pre-test kernel (K4b, also BINSKETCH_PAB_SCREEN=0)
+    on the cases that leave the common path: a query whose 700 exact copies in the db all tie
+    above its threshold (buffer overflow -> barrier-stepped re-walk), one with 9000 copies (pass-2
+    survivors beyond the scratch slot -> screened re-walk), an empty query row, an unaligned db
+    (ndb % 4 != 0), self exclusion, every measure alone and all four together."""
     monkeypatch.setenv("BINSKETCH_ENGINE", "tc")
-    monkeypatch.setenv("BINSKETCH_PAB_SCREEN", screen)
+    if path != "fused-screen":
+        monkeypatch.setenv("BINSKETCH_TOPK_SCREEN", "0")
+    monkeypatch.setenv("BINSKETCH_PAB_SCREEN", "0" if path == "pab-pretest" else "1")
     N, d = synth.RANKING_N, synth.RANKING_DB.d
     D = _sketches(synth.scaled(synth.RANKING_DB, 12_003, seed=71), N)
     D[1000:1700] = D[7]

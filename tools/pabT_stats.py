@@ -36,6 +36,6 @@ e1.synchronize()
 out = {"ms": e0.elapsed_time(e1), "mask": mask}
 if stats:
     lib.bsk_pabt_stats(buf)
-    names = ["queries", "flushes", "scored2", "scored3", "overflows", "cyc_pass1", "cyc_T1", "cyc_pass2", "cyc_T2", "cyc_pass3", "cyc_final"]
+    names = ["queries", "entries", "keys_ge_ts", "final_buf", "x4", "cyc_passA", "cyc_select", "cyc_passB", "cyc_ovf", "cyc_final", "thr_hist", "thr_select", "thr_T", "thr_suffix"]
     out.update({n: int(buf[i]) for i, n in enumerate(names)})
 print(json.dumps(out), flush=True)
