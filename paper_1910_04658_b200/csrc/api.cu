@@ -137,6 +137,30 @@ bool use_tc_pab(uint32_t N, uint64_t nq, uint64_t ndb, uint32_t k) {
 // the call also needs L non-decreasing on [0, N) (checked per (N, d)). BINSKETCH_TOPK_SCREEN=0
 // selects the pab-table kernels instead (dev A/B).
 constexpr uint64_t kScreenSample = 4096;   // db rows [0, S) sampled for the thresholds
+
+// A second stream (and fork / join events) per host thread and device, for the fused screen's
+// independent branches (never destroyed: they may back in-flight work at exit).
+struct Fork {
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+Fork* fork_for_device() {
+  constexpr int kMaxDev = 64;
+  thread_local Fork f[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  Fork& x = f[dev];
+  if (!x.s2) {
+    if (cudaStreamCreateWithFlags(&x.s2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      x = Fork{};
+      return nullptr;
+    }
+  }
+  return &x;
+}
 bool screen_size_ok(uint32_t N, uint64_t nq, uint64_t ndb, uint32_t k) {
   if (const char* e = std::getenv("BINSKETCH_TOPK_SCREEN")) if (!std::strcmp(e, "0")) return false;
   return N <= 16383 && k >= 1 && k <= 256 && bsk::tc_sortable(N) && nq * ndb * 8 <= kPabBudget;
@@ -496,16 +520,26 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
       const double* Ld = reinterpret_cast<const double*>(w + l.L);
       const uint32_t S = (uint32_t)std::min<uint64_t>(ndb, kScreenSample);
       const uint32_t nmp = nm == 3 ? 4u : nm;
-      e = bsk::launch_expand(queries, nq, N, q8, s);
-      if (e == cudaSuccess)
-        e = bsk::launch_sort_by_popcount(pd, ndb, N, reinterpret_cast<uint32_t*>(w + l.bins), perm, spb, s, false);
-      if (e == cudaSuccess) e = bsk::launch_expand(db, ndb, N, d8, s, perm);
+      // two independent branches until the screen: the db's popcount sort + widening on a second
+      // stream (when one is available), the sample thresholds on the caller's stream
+      Fork* fk = fork_for_device();
+      cudaStream_t s2 = fk ? fk->s2 : s;
+      if (fk) {
+        e = cudaEventRecord(fk->fork, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s2, fk->fork, 0);
+        if (e != cudaSuccess) return cuda_status(e);
+      }
+      e = bsk::launch_sort_by_popcount(pd, ndb, N, reinterpret_cast<uint32_t*>(w + l.bins), perm, spb, s2, false);
+      if (e == cudaSuccess) e = bsk::launch_expand(db, ndb, N, d8, s2, perm);
+      if (fk && e == cudaSuccess) e = cudaEventRecord(fk->join, s2);
+      if (e == cudaSuccess) e = bsk::launch_expand(queries, nq, N, q8, s);
       if (e == cudaSuccess) e = bsk::launch_expand(db, S, N, s8, s);
       if (e == cudaSuccess) e = bsk::launch_tc_andpopc(q8, nq, s8, S, N, pabs, ctr, s);
       if (e == cudaSuccess) e = bsk::launch_int_range(pd, ndb, range, s);
       if (e == cudaSuccess)
         e = bsk::launch_screen_threshold(pabs, nq, S, N, measure, k, flags, pq, pd, Ld, range, tsuf, ts, s);
       uint32_t splits = 0, seg_cols = 0;
+      if (fk && e == cudaSuccess) e = cudaStreamWaitEvent(s, fk->join, 0);   // join before the screen
       if (e == cudaSuccess)
         e = bsk::launch_tc_screen(q8, nq, d8, ndb, N, spb, perm, tsuf, nmp, lists, lcnt, ctr, splits, seg_cols, s);
       if (e == cudaSuccess)
