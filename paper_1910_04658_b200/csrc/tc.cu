@@ -1237,20 +1237,25 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           const uint64_t cb = n0 + c;
           const uint32_t left = (uint32_t)min((uint64_t)CW, p.nb - cb);
           if constexpr (MODE == kTcScreen) {
-            uint32_t sm = 0;
+            const uint32_t sm = ge_mask32(v, pmin) & (left >= 32u ? 0xFFFFFFFFu : ((1u << left) - 1u));
+            if (!__any_sync(0xffffffffu, sm != 0u)) continue;
+            // the chunk's values through this warp's shared row (conflict-free: lane * 33 + j), so
+            // each lane walks only its own survivors
+            uint32_t* vs = reinterpret_cast<uint32_t*>(reinterpret_cast<int2*>(extra) + 4 * kTcN) + (size_t)ew * 32 * 33;
 #pragma unroll
-            for (int j = 0; j < CW; ++j) sm |= ((uint32_t)j < left && v[j] >= pmin ? 1u : 0u) << j;
-            if (sm) {
-              uint64_t pos = lbase + lc;
-              lc += (uint32_t)__popc(sm);
-              uint2* o = p.lists + r * p.nb;
-#pragma unroll
-              for (int j = 0; j < CW; ++j)
-                if ((sm >> j) & 1u) {   // (original db index, |b_s| << 14 | pab): N <= 16383
-                  const int2 mt_ = tmeta_w[c + (uint32_t)j];
-                  o[pos++] = make_uint2((uint32_t)mt_.x, ((uint32_t)mt_.y << 14) | v[j]);
-                }
+            for (int j = 0; j < CW; ++j) vs[lane * 33 + j] = v[j];
+            __syncwarp();
+            uint64_t pos = lbase + lc;
+            lc += (uint32_t)__popc(sm);
+            uint2* o = p.lists + r * p.nb;
+            uint32_t mm = sm;
+            while (mm) {   // (original db index, |b_s| << 14 | pab): N <= 16383
+              const uint32_t j = (uint32_t)__ffs(mm) - 1u;
+              mm &= mm - 1u;
+              const int2 mt_ = tmeta_w[c + j];
+              o[pos++] = make_uint2((uint32_t)mt_.x, ((uint32_t)mt_.y << 14) | vs[lane * 33 + j]);
             }
+            __syncwarp();
             continue;
           }
           if (MODE == kTcAndPopc) {
@@ -1531,7 +1536,8 @@ cudaError_t launch_tc_screen(const uint8_t* A8, uint64_t na, const uint8_t* B8, 
   p.na = na; p.nb = nb; p.N = N; p.pb = spb; p.perm = perm; p.tsuf = tsuf; p.nmp = nmp; p.lists = lists;
   p.lcnt = lcnt;
   p.item_ctr = ctr;
-  const cudaError_t e = tc_launch<kTcScreen, 128>(A8, B8, p, N, TcRoles<kTcScreen>::kEpi * kTcN * 8, 0, s);   // tile metadata
+  // per epilogue warp: the tile's metadata (kTcN int2) and a 32 x 33 chunk of values
+  const cudaError_t e = tc_launch<kTcScreen, 128>(A8, B8, p, N, TcRoles<kTcScreen>::kEpi * (kTcN * 8 + 32 * 33 * 4), 0, s);
   splits = p.splits;
   seg_cols = p.per * kTcN;   // list segment sp starts at column sp * seg_cols
   return e;
