@@ -47,11 +47,13 @@ TOPK_NCU = {"source": "profiles/r02_topk_final_summary.txt", "tensor_pipe_active
             "issue_active_pct": 20.9, "dram_bytes_per_launch": 2.369e9 + 0.586e9, "kernel_share_of_stage": "98.3 %",
             "launch_list": "profiles/r02_launches_large_summary.txt"}
 # Ranking: the dominant kernel of the top-k call is the tensor-core AND-popcount with the integer
-# screen in its epilogue (tc_pairs_kernel<kTcScreen>, K4d); its share of the call from the
-# committed launch list (cold-cache, serialised; per call: screen 0.3297, list top-k 0.1087,
-# thresholds 0.0670, expand 0.0570 + 2 x 0.005, popcount sort 0.0472, sample AND-popcount 0.0205,
-# popcounts 0.0166, range 0.0046 ms) and its ncu capture.
-RANK_NCU = {"source": "profiles/r02_tc_screen_summary.txt", "kernel_share_of_stage": 0.3297 / 0.6963,
+# screen in its epilogue (tc_pairs_kernel<kTcScreen>, K4d). Its share of the call's
+# critical path from the committed launch list (cold-cache, serialised, ms per call): popcounts
+# 0.0168; then max(sample branch: query + sample widening ~0.010, sample AND-popcount 0.0205, range
+# 0.0045, thresholds 0.0666 = 0.1016; db branch on the second stream: popcount sort 0.0475, db
+# widening ~0.110 = 0.158); screen 0.2237; list top-k 0.1071 -> 0.506 ms, screen share 0.442.
+RANK_NCU = {"source": "profiles/r02_tc_screen_summary.txt", "kernel_share_of_stage": 0.2237 / 0.506,
+            "dram_bytes_per_launch": 431.3e6 + 25.7e6, "tensor_pipe_active_pct": 93.2,
             "launch_list": "profiles/r02_launches_ranking_summary.txt"}
 HBM_FALLBACK_GBS = 6650.0     # B200_PROFILING.md fallback
 
@@ -373,8 +375,10 @@ def run_ours(args):
         roofline = {"bound": "tensor", "kernel": "tc_pairs_kernel<kTcScreen> (AND-popcount + integer screen epilogue; DESIGN.md K4d)",
                     "achieved": ach_k, "peak": burst, "unit": "TOPS (int8)", "frac": ach_k / burst,
                     "peak_basis": "2 x MEASURED_PEAKS bf16_tflops (burst)", "peak_sustained": sust,
-                    "frac_of_sustained": ach_k / sust, "traffic": None,
-                    "time_basis": "live top-k stage time x the kernel's share of it in the launch list ("
+                    "frac_of_sustained": ach_k / sust, "traffic": RANK_NCU["dram_bytes_per_launch"],
+                    "traffic_unit": "DRAM bytes per launch (ncu --set full): the widened db operand once",
+                    "ncu_tensor_pipe_active_pct": RANK_NCU["tensor_pipe_active_pct"],
+                    "time_basis": "live top-k stage time x the kernel's share of the call's critical path in the launch list ("
                                   + RANK_NCU["launch_list"] + "): " + f"{share:.3f}",
                     "whole_call": {"achieved": 2.0 * pairs_once * N * args.steps / t_topk / 1e12, "unit": "TOPS (int8)",
                                    "frac_of_burst": 2.0 * pairs_once * N * args.steps / t_topk / 1e12 / burst,
