@@ -543,8 +543,8 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
       if (e == cudaSuccess)
         e = bsk::launch_tc_screen(q8, nq, d8, ndb, N, spb, perm, tsuf, nmp, lists, lcnt, ctr, splits, seg_cols, s);
       if (e == cudaSuccess)
-        e = bsk::launch_topk_list(lists, lcnt, splits, seg_cols, nq, ndb, N, measure, k, flags, pq, spb, perm, Ld,
-                                  ts, w + l.scratch, out_idx, out_score, s);
+        e = bsk::launch_topk_list(lists, lcnt, splits, seg_cols, nq, ndb, N, measure, k, flags, pq, Ld, ts,
+                                  w + l.scratch, out_idx, out_score, s);
       return cuda_status(e);
     }
     uint8_t* d8 = self ? q8 : reinterpret_cast<uint8_t*>(w + l.b8);

@@ -91,9 +91,9 @@ cudaError_t launch_screen_threshold(const int32_t* pab_s, uint64_t nq, uint32_t 
                                     const int32_t* pd_range, uint16_t* tsuf, double* ts, cudaStream_t s);
 cudaError_t launch_topk_list(const uint2* lists, const uint32_t* lcnt, uint32_t splits, uint32_t seg_cols,
                              uint64_t nq, uint64_t ndb, uint32_t N,
-                             uint32_t mask, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* spb,
-                             const int32_t* perm, const double* L, const double* ts, void* scratch, int32_t* out_idx,
-                             float* out_score, cudaStream_t s);   // scratch: topk_pab3_scratch_bytes(15)
+                             uint32_t mask, uint32_t k, uint32_t flags, const int32_t* pq, const double* L,
+                             const double* ts, void* scratch, int32_t* out_idx, float* out_score,
+                             cudaStream_t s);   // lists: (original db index, |b_s| << 14 | pab); scratch: topk_pab3_scratch_bytes(15)
 cudaError_t launch_int_range(const int32_t* x, uint64_t n, int32_t* out, cudaStream_t s);
 
 // Tensor-core pair engine (tc.cu): sketches widened to {0,1} bytes, rows padded to

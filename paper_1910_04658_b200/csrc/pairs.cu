@@ -1420,7 +1420,7 @@ cudaError_t launch_screen_threshold(const int32_t* pab_s, uint64_t nq, uint32_t 
   return cudaGetLastError();
 }
 
-// Per query row (one block, grid-stride): its screen survivors (sorted db position, pab) from the
+// Per query row (one block, grid-stride): its screen survivors (original db index, |b_s| << 14 | pab) from the
 // tensor-core screen, ranked exactly for every measure. Pass A: each thread walks a contiguous run
 // of the row's list (its segments seen as one index range), four entries at a time with their
 // loads issued together, scores them (exact fp64 recipe), histograms the keys that reach t_s over
@@ -1434,7 +1434,7 @@ __global__ void __launch_bounds__(256)
 topk_list_kernel(const uint2* __restrict__ lists, const uint32_t* __restrict__ lcnt, uint32_t splits,
                  uint32_t seg_cols, uint64_t nq, uint64_t ndb,
                  uint32_t N, uint32_t mask, uint32_t k, uint32_t flags, const int32_t* __restrict__ pq,
-                 const int32_t* __restrict__ spb, const int32_t* __restrict__ perm, const double* __restrict__ L,
+                 const double* __restrict__ L,
                  const double* __restrict__ ts, double* __restrict__ skey, int32_t* __restrict__ sidx,
                  int32_t* __restrict__ out_idx, float* __restrict__ out_score) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1696,9 +1696,8 @@ topk_list_kernel(const uint2* __restrict__ lists, const uint32_t* __restrict__ l
 
 cudaError_t launch_topk_list(const uint2* lists, const uint32_t* lcnt, uint32_t splits, uint32_t seg_cols,
                              uint64_t nq, uint64_t ndb, uint32_t N,
-                             uint32_t mask, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* spb,
-                             const int32_t* perm, const double* L, const double* ts, void* scratch_v, int32_t* out_idx,
-                             float* out_score, cudaStream_t s) {
+                             uint32_t mask, uint32_t k, uint32_t flags, const int32_t* pq, const double* L,
+                             const double* ts, void* scratch_v, int32_t* out_idx, float* out_score, cudaStream_t s) {
   unsigned char* scratch = static_cast<unsigned char*>(scratch_v);   // topk_pab3_scratch_bytes(15) (slots)
   if (nq == 0 || k == 0) return cudaSuccess;
   const uint32_t nm = (uint32_t)__builtin_popcount(mask & 15u);
@@ -1713,8 +1712,8 @@ cudaError_t launch_topk_list(const uint2* lists, const uint32_t* lcnt, uint32_t 
         bps < 1)                                                                                                 \
       bps = 1;                                                                                                   \
     topk_list_kernel<NMV><<<(unsigned)std::min<uint64_t>({nq, (uint64_t)num_sms() * bps, (uint64_t)kPab3Slots}),  \
-                            256, smem, s>>>(lists, lcnt, splits, seg_cols, nq, ndb, N, mask & 15u, k, flags, pq, spb, \
-                                            perm, L, ts, reinterpret_cast<double*>(scratch),                      \
+                            256, smem, s>>>(lists, lcnt, splits, seg_cols, nq, ndb, N, mask & 15u, k, flags, pq, L,   \
+                                            ts, reinterpret_cast<double*>(scratch),                               \
                                             reinterpret_cast<int32_t*>(scratch + (size_t)kPab3Slots * NMV * kPab3Keep * 8), \
                                             out_idx, out_score);                                                  \
   } while (0)
