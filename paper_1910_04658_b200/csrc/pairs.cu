@@ -1420,15 +1420,16 @@ cudaError_t launch_screen_threshold(const int32_t* pab_s, uint64_t nq, uint32_t 
   return cudaGetLastError();
 }
 
-// Per query row (one block, grid-stride): its screen survivors (original db index, |b_s| << 14 | pab) from the
-// tensor-core screen, ranked exactly for every measure. Pass A: each thread walks a contiguous run
-// of the row's list (its segments seen as one index range), four entries at a time with their
-// loads issued together, scores them (exact fp64 recipe), histograms the keys that reach t_s over
-// [t_s, key max] and keeps (key, db index) of those in the block's scratch slot; t0 (a lower
-// bound of the k-th key) from the histogram. Pass B: the kept pairs reaching t0 that beat the
-// running k-th go to a 512-entry buffer, which a warp per measure sorts at the end. A slot
-// overflow makes pass B re-score the list; a buffer overflow restarts pass B in 256-entry steps
-// with a barrier each, cutting the buffer back to k (block bitonic sort) when it could overflow.
+// Per query row (one block, grid-stride): its screen survivors (original db index, |b_s| << 14 |
+// pab) from the tensor-core screen, ranked exactly for every measure. Pass A: each thread walks a
+// contiguous run of the row's list (its segments seen as one index range), four entries at a time
+// with their loads issued together; approximate keys (approx_key: IP / -HAM exact, JS / COS within
+// kApproxEps) of the pairs that may reach t_s go into a histogram over [t_s, key max] and, as
+// (approximate key, |b_s|:pab, index) records, into the block's scratch slot; t0 = the histogram's
+// lower bound of the k-th key less the margin. Pass B: the records that may reach t0 get their
+// EXACT key (fp64 recipe); those that beat the running k-th go to a 512-entry buffer, ranked at the
+// end by counting (the order is strict). A slot overflow makes pass B re-score the list exactly; a
+// buffer overflow restarts pass B in 256-entry steps with a barrier each, cutting back to k.
 template <int NM>
 __global__ void __launch_bounds__(256)
 topk_list_kernel(const uint2* __restrict__ lists, const uint32_t* __restrict__ lcnt, uint32_t splits,
