@@ -1626,8 +1626,8 @@ topk_list_kernel(const uint2* __restrict__ lists, const uint32_t* __restrict__ l
           for (int u = 0; u < 4; ++u) rc[u] = i0 + u * blockDim.x < nk ? recs[i0 + u * blockDim.x] : make_uint2(0xFF800000u, 0u);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            if ((double)__uint_as_float(rc[u].x) < tcut) continue;   // cannot reach t0
             const uint32_t i = i0 + u * blockDim.x;
+            if (i >= nk || (double)__uint_as_float(rc[u].x) < tcut) continue;   // (none) / cannot reach t0
             const int pb = (int)(rc[u].y >> 14), v = (int)(rc[u].y & 0x3FFFu);
             collect(mi, si[(size_t)mi * kPab3Keep + i], pab_key(pa, pb, v, (int)N, L, ms[mi]));   // the exact key
           }

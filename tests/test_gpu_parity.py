@@ -477,6 +477,24 @@ def test_topk_pab_screen_paths(path, monkeypatch):
         assert_est_close(gs[t].cpu().numpy(), rs)
 
 
+@pytest.mark.parametrize("path", ["fused-screen", "pab-screen"])
+def test_topk_screen_small_and_padded(path, monkeypatch):
+    """Top-k beyond the fused kernel on degenerate shapes: fewer db rows than k (lists padded with
+    -1 / NaN), a single query, a db smaller than the threshold sample, an all-zero query, self
+    exclusion with k > ndb - 1, an odd sketch length (ragged last word)."""
+    monkeypatch.setenv("BINSKETCH_ENGINE", "tc")
+    if path != "fused-screen":
+        monkeypatch.setenv("BINSKETCH_TOPK_SCREEN", "0")
+    d = synth.RANKING_DB.d
+    for N, ndb, nq in ((4096, 50, 7), (4095, 300, 1), (1000, 999, 30)):
+        D = _sketches(synth.scaled(synth.RANKING_DB, ndb, seed=90 + ndb), N)
+        Q = D[: max(nq, 1)].copy()
+        Q[0] = 0
+        _check_topk(Q, D, N, d, bs.JS, 100)
+        _check_topk(D, D, N, d, bs.COS, 120, exclude_self=True)
+        _check_topk(Q, D, N, d, bs.IP | 0, 90)
+
+
 @pytest.mark.parametrize("N", [16383, 16384])
 def test_topk_pab_screen_n_limit(N):
     """The integer-screen kernel's 14-bit table entries end at N = 16383; N = 16384 takes the
