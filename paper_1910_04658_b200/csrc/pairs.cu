@@ -1431,7 +1431,7 @@ cudaError_t launch_screen_threshold(const int32_t* pab_s, uint64_t nq, uint32_t 
 // end by counting (the order is strict). A slot overflow makes pass B re-score the list exactly; a
 // buffer overflow restarts pass B in 256-entry steps with a barrier each, cutting back to k.
 template <int NM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 topk_list_kernel(const uint2* __restrict__ lists, const uint32_t* __restrict__ lcnt, uint32_t splits,
                  uint32_t seg_cols, uint64_t nq, uint64_t ndb,
                  uint32_t N, uint32_t mask, uint32_t k, uint32_t flags, const int32_t* __restrict__ pq,
