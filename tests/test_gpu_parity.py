@@ -495,6 +495,32 @@ def test_topk_screen_small_and_padded(path, monkeypatch):
         _check_topk(Q, D, N, d, bs.IP | 0, 90)
 
 
+def test_topk_screen_extremes():
+    """The fused-screen top-k at its limits: N = 16383 (14-bit table entries), k = 256, all four
+    measures in one call (three and four tables per pb), an empty and a saturated db row, a
+    one-popcount cluster, more queries than 4 x 148 list-kernel slots, self exclusion."""
+    N, d = 16383, 60_000
+    spec = synth.CSRSpec(n=3000, d=d, kind=1, p1=150, p2=1.0, cap=900, zipf_s=1.05, seed=97)
+    D = _sketches(spec, N)
+    D[5] = 0
+    D[6] = 0xFFFFFFFF
+    D[6, -1] = (1 << (N % 32)) - 1
+    D[100:160] = D[7]
+    Q = D[:700].copy()
+    Qd, Dd = dev(Q.view(np.int32)), dev(D.view(np.int32))
+    for ms, k in (((bs.IP, bs.HAM, bs.JS, bs.COS), 256), ((bs.IP, bs.JS, bs.COS), 130)):
+        mask = 0
+        for m in ms:
+            mask |= m
+        gi, gs = bs.topk(Qd, Dd, N, d, mask, k, exclude_self=True)
+        for t, m in enumerate(ms):
+            ri, rs = oracle.topk(Q, D, N, d, m, k, exclude_self=True)
+            assert np.array_equal(gi[t].cpu().numpy(), ri)
+            g, rr = gs[t].cpu().numpy(), rs
+            assert np.array_equal(np.isnan(g), np.isnan(rr))
+            assert_est_close(g[~np.isnan(rr)], rr[~np.isnan(rr)])
+
+
 @pytest.mark.parametrize("N", [16383, 16384])
 def test_topk_pab_screen_n_limit(N):
     """The integer-screen kernel's 14-bit table entries end at N = 16383; N = 16384 takes the
