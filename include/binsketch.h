@@ -167,9 +167,14 @@ binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, con
  * out_idx: device int32[nq][k]; out_score: device float[nq][k] per measure (the measure's
  * value, not the key). Slots beyond the number of eligible db rows hold
  * idx = -1 and score = NaN.
- * Engine (results identical either way): k <= 64 and N <= 6143 — the fused tensor-core
- * top-k (K10; per-row heaps in shared memory, db popcount-sorted for the bound);
- * otherwise the tensor-core AND-popcount into a workspace table + the streaming top-k (K4b). */
+ * Engine (results identical either way): k <= 64 and N <= 6143 (and the heaps fit shared
+ * memory) — the fused tensor-core top-k (K10; per-row heaps in shared memory, db
+ * popcount-sorted for the bound); otherwise, for N <= 16383, the fused tensor-core screen
+ * (K4d: sample thresholds, the AND-popcount with an integer screen in its epilogue
+ * writing survivor lists into the workspace, an exact list top-k), else the tensor-core
+ * AND-popcount into a workspace table + the pab-table top-k (K4c / K4b). The screen path runs
+ * two independent branches on an internal stream forked from and joined back to `stream` with
+ * events, so the call stays ordered on `stream` like every other call. */
 binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb,
                                 uint32_t N, uint64_t d, uint32_t measure, uint32_t k, uint32_t flags,
                                 int32_t* out_idx, float* out_score, void* ws, size_t ws_bytes,
