@@ -320,18 +320,31 @@ build_kernel(const BuildParams p) {
 
   unsigned bad = 0;
   uint32_t maxj = 0, maxidx = 0;
-  if (MODE == kPiSmem16) {
-    for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
-      const uint32_t v = __ldg(p.pi + i);
-      maxj = max(maxj, v);
-      sts_u16(pi_a + 2 * i, min(v, N - 1));
+  if (MODE == kPiSmem16 || MODE == kPiCache16 || MODE == kPiCache32) {
+    // the shared copy of the table (whole, or its first kSlots entries as the cache's initial
+    // contents: tag 0), four entries per 16-B load: this fill is a fixed cost of every launch
+    // (the whole cost of a small build), so it runs at load width with four loads in flight
+    const uint32_t n_fill = MODE == kPiSmem16 ? d : kSlots;
+    const uint32_t n_src = min(n_fill, d);
+    const bool pv = (reinterpret_cast<uintptr_t>(p.pi) & 15u) == 0;
+    const uint32_t g4 = pv ? n_src / 4 : 0;   // whole 4-entry groups read as uint4
+#pragma unroll 4
+    for (uint32_t g = threadIdx.x; g < g4; g += blockDim.x) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(p.pi) + g);
+      maxj = max(maxj, max(max(x.x, x.y), max(x.z, x.w)));
+      const uint32_t a = min(x.x, N - 1), b = min(x.y, N - 1), c = min(x.z, N - 1), e = min(x.w, N - 1);
+      if (MODE == kPiCache32) {
+        sts_v4(pi_a + 16 * g, a, b, c, e);
+      } else {
+        sts_u32(pi_a + 8 * g, a | (b << 16));
+        sts_u32(pi_a + 8 * g + 4, c | (e << 16));
+      }
     }
-  } else if (MODE == kPiCache16 || MODE == kPiCache32) {
-    for (uint32_t s = threadIdx.x; s < kSlots; s += blockDim.x) {
+    for (uint32_t s = 4 * g4 + threadIdx.x; s < n_fill; s += blockDim.x) {
       uint32_t v = s < d ? __ldg(p.pi + s) : 0u;
       maxj = max(maxj, v);
       v = min(v, N - 1);
-      if (MODE == kPiCache16) sts_u16(pi_a + 2 * s, v); else sts_u32(pi_a + 4 * s, v);
+      if (MODE == kPiCache32) sts_u32(pi_a + 4 * s, v); else sts_u16(pi_a + 2 * s, v);
     }
   }
   for (uint32_t w = 4 * lane; w < RR * W; w += 128) sts_v4(ring_a + 4 * w, 0u, 0u, 0u, 0u);
