@@ -12,7 +12,9 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <string>
 #include <tuple>
+#include <unistd.h>   // environ
 #include <utility>
 
 #include "binsketch.h"
@@ -436,9 +438,9 @@ binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, con
   return cuda_status(e);
 }
 
-binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb, uint32_t N,
-                                uint64_t d, uint32_t measure, uint32_t k, uint32_t flags, int32_t* out_idx,
-                                float* out_score, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
+static binsketch_status topk_impl(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb, uint32_t N,
+                                  uint64_t d, uint32_t measure, uint32_t k, uint32_t flags, int32_t* out_idx,
+                                  float* out_score, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
   if (N < 2 || measure == 0 || (measure & ~15u) || (flags & ~1u)) return BINSKETCH_EINVAL;
   if (N > BINSKETCH_MAX_N_PAIRS) return BINSKETCH_EUNSUPPORTED;
   if (nq == 0 || k == 0) return BINSKETCH_OK;
@@ -570,6 +572,98 @@ binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint
                          l.splits > 1 ? reinterpret_cast<int32_t*>(w + l.pidx) : nullptr,
                          out_idx + (size_t)mi * nq * k, out_score + (size_t)mi * nq * k, s, pab);
   return cuda_status(e);
+}
+
+// binsketch_topk replays a CUDA graph of the call when it was made before with the same arguments
+// (pointers, sizes, measure, k, flags, workspace) by this host thread on this device: a call is
+// 5-20 kernel launches and memsets, several of them a few microseconds long, so launch gaps are a
+// visible part of small and mid-size calls. The graph is captured on an internal stream (relaxed
+// mode) and launched on the caller's stream; any capture failure falls back to the direct launches.
+// Nothing in the call depends on the data (no host synchronisation), so a replay is the same
+// computation on the current contents of the inputs. BINSKETCH_GRAPH=0 disables (dev A/B).
+namespace {
+struct TopkKey {
+  const void *q, *db, *oi, *os, *ws;
+  uint64_t nq, ndb, d, ws_bytes;
+  uint32_t N, measure, k, flags;
+  int dev;
+  std::string knobs;   // the BINSKETCH_* environment (the A/B knobs steer the captured path)
+  bool operator<(const TopkKey& o) const {
+    return std::tie(q, db, oi, os, ws, nq, ndb, d, ws_bytes, N, measure, k, flags, dev, knobs) <
+           std::tie(o.q, o.db, o.oi, o.os, o.ws, o.nq, o.ndb, o.d, o.ws_bytes, o.N, o.measure, o.k, o.flags, o.dev,
+                    o.knobs);
+  }
+};
+std::string binsketch_knobs() {
+  std::string r;
+  for (char** e = environ; e && *e; ++e)
+    if (!std::strncmp(*e, "BINSKETCH_", 10)) { r += *e; r += '\n'; }
+  return r;
+}
+struct TopkGraph {
+  cudaGraphExec_t exec = nullptr;
+  uint64_t launches = 0;
+};
+bool graphs_enabled() {
+  const char* e = std::getenv("BINSKETCH_GRAPH");
+  return !(e && !std::strcmp(e, "0"));
+}
+}  // namespace
+
+binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb, uint32_t N,
+                                uint64_t d, uint32_t measure, uint32_t k, uint32_t flags, int32_t* out_idx,
+                                float* out_score, void* ws, size_t ws_bytes, binsketch_stream_t stream) {
+  int dev = 0;
+  if (!graphs_enabled() || nq == 0 || k == 0 || cudaGetDevice(&dev) != cudaSuccess)
+    return topk_impl(queries, nq, db, ndb, N, d, measure, k, flags, out_idx, out_score, ws, ws_bytes, stream);
+  constexpr size_t kMaxGraphs = 16;   // per host thread (oldest entries dropped)
+  thread_local std::map<TopkKey, TopkGraph> graphs;
+  thread_local cudaStream_t cap[64] = {};
+  const TopkKey key{queries, db, out_idx, out_score, ws, nq, ndb, d, ws_bytes, N, measure, k, flags, dev,
+                    binsketch_knobs()};
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  auto it = graphs.find(key);
+  if (it != graphs.end()) {
+    const cudaError_t e = cudaGraphLaunch(it->second.exec, s);
+    if (e == cudaSuccess) {
+      bsk::count_launch(it->second.launches);
+      return BINSKETCH_OK;
+    }
+    cudaGetLastError();
+    cudaGraphExecDestroy(it->second.exec);
+    graphs.erase(it);
+    return topk_impl(queries, nq, db, ndb, N, d, measure, k, flags, out_idx, out_score, ws, ws_bytes, stream);
+  }
+  if (dev < 0 || dev >= 64 ||
+      (!cap[dev] && cudaStreamCreateWithFlags(&cap[dev], cudaStreamNonBlocking) != cudaSuccess)) {
+    cudaGetLastError();
+    return topk_impl(queries, nq, db, ndb, N, d, measure, k, flags, out_idx, out_score, ws, ws_bytes, stream);
+  }
+  const uint64_t before = bsk::launch_count();
+  cudaGraph_t g = nullptr;
+  binsketch_status st = BINSKETCH_ECUDA;
+  if (cudaStreamBeginCapture(cap[dev], cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+    st = topk_impl(queries, nq, db, ndb, N, d, measure, k, flags, out_idx, out_score, ws, ws_bytes,
+                   reinterpret_cast<binsketch_stream_t>(cap[dev]));
+    if (cudaStreamEndCapture(cap[dev], &g) != cudaSuccess) st = BINSKETCH_ECUDA;
+  }
+  const uint64_t launches = bsk::launch_count() - before;
+  cudaGraphExec_t exec = nullptr;
+  if (st == BINSKETCH_OK && g && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess &&
+      cudaGraphLaunch(exec, s) == cudaSuccess) {
+    cudaGraphDestroy(g);
+    if (graphs.size() >= kMaxGraphs) {
+      cudaGraphExecDestroy(graphs.begin()->second.exec);
+      graphs.erase(graphs.begin());
+    }
+    graphs[key] = TopkGraph{exec, launches};
+    return BINSKETCH_OK;
+  }
+  // capture unavailable (or an argument error, which the direct call reports the same way)
+  cudaGetLastError();
+  if (exec) cudaGraphExecDestroy(exec);
+  if (g) cudaGraphDestroy(g);
+  return topk_impl(queries, nq, db, ndb, N, d, measure, k, flags, out_idx, out_score, ws, ws_bytes, stream);
 }
 
 binsketch_status binsketch_join(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb, uint32_t N,
