@@ -1,7 +1,7 @@
 #!/bin/bash
 # Final verification session: GPU suite (with the full-size tests), smoke, whole-output Large parity,
 # every bench line, launch lists, the Large top-k ncu capture, and the secondary workloads.
-T=gpurun_out/r02_final
+T=gpurun_out/${TAG:-r02_final}
 mkdir -p $T
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $T/gpu.txt 2>&1
 nproc > $T/host.txt; grep -m1 "model name" /proc/cpuinfo >> $T/host.txt
