@@ -521,6 +521,33 @@ def test_topk_screen_extremes():
             assert_est_close(g[~np.isnan(rr)], rr[~np.isnan(rr)])
 
 
+@pytest.mark.parametrize("k, N", [(100, 4096), (50, 1024)])
+def test_topk_graph_replay(k, N, monkeypatch):
+    """binsketch_topk replays a captured CUDA graph when called again with the same buffers: the
+    replay computes on the buffers' CURRENT contents (new queries and db rows in place), and a
+    changed BINSKETCH_* knob selects a new capture (here: the pab-table path instead of the fused
+    screen, or the CUDA-core engine); every result identical to the oracle."""
+    monkeypatch.setenv("BINSKETCH_ENGINE", "tc")
+    d = synth.RANKING_DB.d
+    D1 = _sketches(synth.scaled(synth.RANKING_DB, 3000, seed=101), N)
+    D2 = _sketches(synth.scaled(synth.RANKING_DB, 3000, seed=102), N)
+    Qd, Dd = dev(D1[:200].view(np.int32)), dev(D1.view(np.int32))
+    oi = torch.empty((200, k), dtype=torch.int32, device="cuda")
+    os_ = torch.empty((200, k), dtype=torch.float32, device="cuda")
+    ws = torch.empty(bs.workspace_bytes(bs.OP_TOPK, 200, 3000, N, k), dtype=torch.uint8, device="cuda")
+    cases = [(D1, None), (D2, None), (D1, ("BINSKETCH_TOPK_SCREEN", "0")), (D2, ("BINSKETCH_ENGINE", "cuda"))]
+    for D, knob in cases:
+        if knob:
+            monkeypatch.setenv(*knob)
+        Qd.copy_(dev(D[:200].view(np.int32)))
+        Dd.copy_(dev(D.view(np.int32)))
+        for _ in range(2):   # capture, then replay
+            gi, gs = bs.topk(Qd, Dd, N, d, bs.JS, k, exclude_self=True, out_idx=oi, out_score=os_, ws=ws)
+            ri, rs = oracle.topk(D[:200], D, N, d, bs.JS, k, exclude_self=True)
+            assert np.array_equal(gi.cpu().numpy(), ri)
+            assert_est_close(gs.cpu().numpy(), rs)
+
+
 @pytest.mark.parametrize("N", [16383, 16384])
 def test_topk_pab_screen_n_limit(N):
     """The integer-screen kernel's 14-bit table entries end at N = 16383; N = 16384 takes the
