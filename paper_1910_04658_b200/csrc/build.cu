@@ -140,6 +140,9 @@ constexpr uint32_t kAuxFixed = kMetaBytes + 16 * kNS;  // bitmap + mbarriers (pe
 #ifndef BSK_BUILD_PI_STAGE
 #define BSK_BUILD_PI_STAGE 256    // elements per stage (shared-memory pi modes)
 #endif
+#ifndef BSK_BUILD_FILL_STAGES
+#define BSK_BUILD_FILL_STAGES 0   // cache modes: stages per warp that fill the cache on a miss (0: all)
+#endif
 #ifndef BSK_BUILD_PI_THREADS
 #define BSK_BUILD_PI_THREADS 384
 #endif
@@ -564,6 +567,9 @@ build_kernel(const BuildParams p) {
         __syncwarp();
       };
 
+      // cache modes: misses fill the shared cache only in the warp's first kFillStages stages
+      // (0: always); afterwards the cache is read-only (warp-uniform)
+      bool fill_on = true;
       // one 256-element half of a stage: off = stage-relative offset of the half, wb = its
       // bitmap-relative offset; PRED: only elements at stage offsets [lo, hi) take effect
       auto half_step = [&](const uint32_t slot, const int off, const int wb, const int lo, const int hi,
@@ -629,15 +635,24 @@ build_kernel(const BuildParams p) {
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) j[u] = ldg_if(p.pi + x[u], miss[u], c[u] & vmask);
-            // fill every missed slot (branch-free: predicated stores). Measured: a probabilistic
+            // fill every missed slot (branch-free: predicated stores) while the warp is in its
+            // warm-up stages; afterwards the cache is read-only. Measured: a probabilistic
             // fill (1/4 of misses, hashed) keeps the simulated hit rate but was slower (1.75 vs 1.68 ms).
+            if (fill_on) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              maxj = max(maxj, (ok[u] && miss[u]) ? j[u] : 0u);
-              if (!POW2) j[u] = min(j[u], N - 1);      // POW2: the ring mask keeps any j in bounds
-              const uint32_t ent = ((x[u] >> kSlotBits) << vb) | (j[u] & vmask);
-              if (MODE == kPiCache16) sts_u16_if(miss[u], pi_a + 2 * slot_[u], ent);
-              else sts_u32_if(miss[u], pi_a + 4 * slot_[u], ent);
+              for (int u = 0; u < 8; ++u) {
+                maxj = max(maxj, (ok[u] && miss[u]) ? j[u] : 0u);
+                if (!POW2) j[u] = min(j[u], N - 1);      // POW2: the ring mask keeps any j in bounds
+                const uint32_t ent = ((x[u] >> kSlotBits) << vb) | (j[u] & vmask);
+                if (MODE == kPiCache16) sts_u16_if(miss[u], pi_a + 2 * slot_[u], ent);
+                else sts_u32_if(miss[u], pi_a + 4 * slot_[u], ent);
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                maxj = max(maxj, (ok[u] && miss[u]) ? j[u] : 0u);
+                if (!POW2) j[u] = min(j[u], N - 1);
+              }
             }
           }
 #pragma unroll
@@ -676,6 +691,7 @@ build_kernel(const BuildParams p) {
         fast_lim = bm_ok ? min(min(wend, end), b0 + kChunk) : 0;
       };
       for (int k = 0; k < nst; ++k) {
+        if (BSK_BUILD_FILL_STAGES > 0) fill_on = k < BSK_BUILD_FILL_STAGES;
         issue(k + kNS - 1);
         const uint32_t slot = stage_a + (uint32_t)(k % kNS) * SB;
         mbar_wait(mbar_a + 8u * (uint32_t)(k % kNS), (uint32_t)(k / kNS) & 1u);

@@ -245,8 +245,34 @@ __device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[32]) {
       : "memory");
 }
 
+
+// 32 lanes x 32 columns of 32-bit TMEM packed to 16 bits (.pack::16b keeps the low half of
+// each column; register i = column 2i in bits 0-15, column 2i+1 in bits 16-31) -> 16
+// registers, issued without waiting (tmem_ld_wait16x2 waits for both of a pair).
+__device__ __forceinline__ void tmem_ld16p_issue(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait16x2(uint32_t (&a)[16], uint32_t (&b)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+      : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+        "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]), "+r"(a[13]), "+r"(a[14]), "+r"(a[15]),
+        "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7]),
+        "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]), "+r"(b[12]), "+r"(b[13]), "+r"(b[14]), "+r"(b[15])
+      :
+      : "memory");
+}
+
 }  // namespace tc
 
+#ifndef BSK_TOPK_PACK
+#define BSK_TOPK_PACK 0   // fused top-k: 16-bit packed TMEM loads, two per wait (measured slower: DESIGN.md K10)
+#endif
 #ifdef BSK_TOPK_PROF
 #define BSK_T0(v) const long long v = clock64()
 #define BSK_TADD(slot, t0) (pacc[(slot) - 6] += (unsigned long long)(clock64() - (t0)))
@@ -443,6 +469,16 @@ __device__ __forceinline__ uint32_t max32(const uint32_t (&v)[32]) {
   const uint32_t b0 = __vimax3_u32(a[0], a[1], a[2]), b1 = __vimax3_u32(a[3], a[4], a[5]);
   const uint32_t b2 = __vimax3_u32(a[6], a[7], a[8]), b3 = max(a[9], a[10]);
   return max(__vimax3_u32(b0, b1, b2), b3);
+}
+// Max of 32 16-bit values packed two per register (the high and low halves of 16 words):
+// a 3-input tree of paired 16-bit maxima (VIMNMX3 .U16x2), then the larger half.
+__device__ __forceinline__ uint32_t max16p(const uint32_t (&v)[16]) {
+  uint32_t a[6];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) a[i] = __vimax3_u16x2(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  a[5] = v[15];
+  const uint32_t m = __vmaxu2(__vimax3_u16x2(a[0], a[1], a[2]), __vimax3_u16x2(a[3], a[4], a[5]));
+  return max(m & 0xffffu, m >> 16);
 }
 // Bit j set iff v[j] >= t, built in four independent partial masks.
 __device__ __forceinline__ uint32_t ge_mask32(const uint32_t (&v)[32], uint32_t t) {
@@ -864,6 +900,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #else
         if (lo == c_lo && hi_ == c_hi && T == c_T) return c_pmin;   // sorted db: runs of equal ranges
 #endif
+#ifdef BSK_TOPK_STATS
+        atomicAdd(&g_tkstats[15], 1ull);   // (lane, tile) bound recomputations
+#endif
         const double g = T - 1e-9 * fmax(1.0, fabs(T));
         const uint32_t pmax = min((uint32_t)pa, hi_);
         const double Llo = Ls[lo];
@@ -911,6 +950,10 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int2* tm = meta_s + ms * TN;
         const uint32_t nval = (uint32_t)min((uint64_t)TN, p.nb - n0);
         // the tile's popcount range (the db is popcount-sorted, descending or ascending)
+#ifdef BSK_TOPK_PROF
+        { const uint32_t x0 = (uint32_t)tm[nval - 1].x + (uint32_t)tm[0].x; if (x0 == 0xFFFFFFFFu) pmin = 1u; }
+        if (lane == 0) BSK_TADD(13, te0);
+#endif
         if (valid) pmin = tile_pmin(min((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x), max((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x));
         const bool direct = __any_sync(0xffffffffu, cnt < K);
 #ifdef BSK_TOPK_STATS
@@ -972,14 +1015,20 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           qn = 0;
         };
         // one 32-column chunk (values v): prefilter, then survivors
-        auto chunk = [&](const uint32_t c, uint32_t (&v)[32]) {
+        // (V(j): the pab of column c + j of this lane's row; mx: the max of V over the chunk)
+        auto chunk = [&](const uint32_t c, const uint32_t mx, auto&& V) {
           if (c >= nval) return;
           const uint32_t left = nval - c;
-          const uint32_t mx = max32(v);
           const bool pass = valid && mx >= pmin;
           if (!__any_sync(0xffffffffu, pass)) return;
-          // survivor mask of this lane
-          const uint32_t sm = pass ? ge_mask32(v, pmin) & (left >= 32 ? 0xffffffffu : ((1u << left) - 1u)) : 0u;
+          // survivor mask of this lane (four independent partial masks)
+          uint32_t sm = 0u;
+          if (pass) {
+            uint32_t mk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int j = 0; j < 32; ++j) mk[j & 3] |= (V(j) >= pmin ? 1u : 0u) << j;
+            sm = ((mk[0] | mk[1]) | (mk[2] | mk[3])) & (left >= 32 ? 0xffffffffu : ((1u << left) - 1u));
+          }
           const uint32_t ns = __popc(sm);
 #ifdef BSK_TOPK_STATS
           {
@@ -996,7 +1045,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             // per-lane: each lane walks its own survivors (heap filling, or a burst)
             if (ns) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) scr[j * kTcM + rt] = v[j];
+              for (int j = 0; j < 32; ++j) scr[j * kTcM + rt] = V(j);
               uint32_t mm = sm;
               while (mm) {   // four independent fp64 evaluations in flight, then the offers
                 double kk[4];
@@ -1026,7 +1075,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           off += qn;
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if ((sm >> j) & 1u) q[off++] = make_uint2(c + (uint32_t)j, ((uint32_t)lane << 24) | v[j]);
+            if ((sm >> j) & 1u) q[off++] = make_uint2(c + (uint32_t)j, ((uint32_t)lane << 24) | V(j));
           qn += total;
           __syncwarp();
                 };
@@ -1040,6 +1089,26 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #else
         if (__any_sync(0xffffffffu, valid && (cnt < K || pmin <= min((uint32_t)pa, tile_hi)))) {
 #endif
+#if BSK_TOPK_PACK
+          // 64 columns per TMEM wait: two 32-column loads packed to 16 bits (pab <= N <= 1024;
+          // LDTM .PACK16BIT, register i = columns 2i | 2i+1 << 16) in flight together, in the
+          // register footprint of one unpacked chunk; one vote rejects both chunks
+          uint32_t pk0[16], pk1[16];
+#pragma unroll 1
+          for (uint32_t c = 0; c < nval; c += 64) {
+            tc::tmem_ld16p_issue(tb + c, pk0);
+            if (c + 32 < nval) tc::tmem_ld16p_issue(tb + c + 32, pk1);   // (warp-uniform)
+            else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pk1[i] = 0u;
+            }
+            tc::tmem_ld_wait16x2(pk0, pk1);
+            const uint32_t m0 = max16p(pk0), m1 = max16p(pk1);
+            if (!__any_sync(0xffffffffu, valid && max(m0, m1) >= pmin)) continue;
+            chunk(c, m0, [&](int j) { return (j & 1) ? (pk0[j >> 1] >> 16) : (pk0[j >> 1] & 0xffffu); });
+            chunk(c + 32, m1, [&](int j) { return (j & 1) ? (pk1[j >> 1] >> 16) : (pk1[j >> 1] & 0xffffu); });
+          }
+#else
           uint32_t va[32];
 #pragma unroll 1
           for (uint32_t c = 0; c < nval; c += 32) {   // one 32-column chunk at a time (register budget)
@@ -1049,8 +1118,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             if (va[0] == 0xdeadbeefu && va[31] == 0x12345678u) pmin = 0;   // dev: keep the loads, skip the filter
             continue;
 #endif
-            chunk(c, va);
+            chunk(c, max32(va), [&](int j) { return va[j]; });
           }
+#endif
         }
         release_acc(acc);
         if (lane == 0) BSK_TADD(7, te2);

@@ -176,6 +176,61 @@ __global__ void k_hash(uint64_t seed, uint64_t M, uint32_t N, uint32_t* out, uns
   RECORD(cyc, t0, t1);
 }
 
+
+// Legacy warp-level binary MMA (mma.sync m16n8k256 b1, AND + POPC): 4 independent accumulator
+// sets per warp. One instruction = 16 x 8 x 256 = 32768 AND-popcount bit pairs per warp (1024
+// per thread). ptxas lowers it on sm_100a to an emulation subroutine (MOVM.U4TO8 + 8 x
+// IMMA.16832.U8.U8), so this measures what the toolchain actually offers for binary MMA.
+__global__ void k_b1mma(uint32_t seed, uint32_t* out, unsigned long long* cyc) {
+  uint32_t a[4], b[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = seed * (threadIdx.x + i + 1);
+  b[0] = seed ^ threadIdx.x; b[1] = seed + 7u * threadIdx.x;
+  int c[4][4] = {};
+  __syncthreads();
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < ITERS / 16; ++it) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      asm volatile("mma.sync.aligned.m16n8k256.row.col.s32.b1.b1.s32.and.popc {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                   : "+r"(c[s][0]), "+r"(c[s][1]), "+r"(c[s][2]), "+r"(c[s][3])
+                   : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  }
+  __syncthreads();
+  unsigned long long t1 = clock64();
+  int sum = 0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) sum += c[s][0] + c[s][1] + c[s][2] + c[s][3];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (uint32_t)sum;
+  RECORD(cyc, t0, t1);
+}
+
+// Legacy warp-level int8 MMA (mma.sync m16n8k32 u8): 16 x 8 x 32 = 4096 MACs per warp instruction
+// (128 per thread), 4 independent accumulator sets — the baseline the b1 emulation is built on.
+__global__ void k_i8mma(uint32_t seed, uint32_t* out, unsigned long long* cyc) {
+  uint32_t a[4], b[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = seed * (threadIdx.x + i + 1);
+  b[0] = seed ^ threadIdx.x; b[1] = seed + 7u * threadIdx.x;
+  int c[4][4] = {};
+  __syncthreads();
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                   : "+r"(c[s][0]), "+r"(c[s][1]), "+r"(c[s][2]), "+r"(c[s][3])
+                   : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  }
+  __syncthreads();
+  unsigned long long t1 = clock64();
+  int sum = 0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) sum += c[s][0] + c[s][1] + c[s][2] + c[s][3];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (uint32_t)sum;
+  RECORD(cyc, t0, t1);
+}
+
 template <typename F>
 static int run(const char* name, double ops_per_thread, int blocks, int threads, F launch, int sms) {
   uint32_t* out;
@@ -265,5 +320,10 @@ int main() {
   run("splitmix64_pi_eval", ITERS / 16.0 * 4, B, T,
       [&](uint32_t* o, unsigned long long* c) { k_hash<<<B, T>>>(1ull, ~0ull / N, N, o, c); }, sms);
   cudaFree(tab);
+  // binary / int8 warp MMA (legacy mma.sync): "ops" = AND-popcount bit pairs resp. u8 MACs
+  run("mma_sync_b1_andpopc_bitpairs (emulated on sm_100a)", (ITERS / 16) * 4 * 1024.0, B, T,
+      [&](uint32_t* o, unsigned long long* c) { k_b1mma<<<B, T>>>(0x9e3779b9u, o, c); }, sms);
+  run("mma_sync_u8_macs", ITERS * 4 * 128.0, B, T,
+      [&](uint32_t* o, unsigned long long* c) { k_i8mma<<<B, T>>>(0x9e3779b9u, o, c); }, sms);
   return 0;
 }

@@ -35,7 +35,7 @@ e1.synchronize()
 lib.bsk_topk_stats(buf)
 names = ["warp_tiles", "skippable_warp_tiles", "passing_chunks", "survivors", "direct_warp_tiles", "candidates",
          "epi_wait_tfull", "epi_filter", "epi_score", "epi_setup", "mma_wait_tempty", "mma_wait_full", "prod_wait_empty",
-         "epi_loop", "mma_total"]
+         "epi_setup_loads", "mma_total", "pmin_recomputes"]
 out = {n: int(buf[i]) for i, n in enumerate(names)}
 out.update(k=a.k, measure=a.measure, qsort=os.environ.get("BINSKETCH_TC_QSORT", "default"), ms=e0.elapsed_time(e1))
 print(json.dumps(out), flush=True)
