@@ -141,7 +141,7 @@ constexpr uint32_t kAuxFixed = kMetaBytes + 16 * kNS;  // bitmap + mbarriers (pe
 #define BSK_BUILD_PI_STAGE 256    // elements per stage (shared-memory pi modes)
 #endif
 #ifndef BSK_BUILD_FILL_STAGES
-#define BSK_BUILD_FILL_STAGES 0   // cache modes: stages per warp that fill the cache on a miss (0: all)
+#define BSK_BUILD_FILL_STAGES 0   // cache modes: stages per warp that fill the cache on a miss (0: all, < 0: none)
 #endif
 #ifndef BSK_BUILD_PI_THREADS
 #define BSK_BUILD_PI_THREADS 384
@@ -691,7 +691,7 @@ build_kernel(const BuildParams p) {
         fast_lim = bm_ok ? min(min(wend, end), b0 + kChunk) : 0;
       };
       for (int k = 0; k < nst; ++k) {
-        if (BSK_BUILD_FILL_STAGES > 0) fill_on = k < BSK_BUILD_FILL_STAGES;
+        if (BSK_BUILD_FILL_STAGES != 0) fill_on = k < BSK_BUILD_FILL_STAGES;   // (< 0: never)
         issue(k + kNS - 1);
         const uint32_t slot = stage_a + (uint32_t)(k % kNS) * SB;
         mbar_wait(mbar_a + 8u * (uint32_t)(k % kNS), (uint32_t)(k / kNS) & 1u);

@@ -270,6 +270,12 @@ __device__ __forceinline__ void tmem_ld_wait16x2(uint32_t (&a)[16], uint32_t (&b
 
 }  // namespace tc
 
+#ifndef BSK_PMIN_FAST
+#define BSK_PMIN_FAST 1   // fused top-k: tile bound start by MUFU exp, IP refinement on the hoisted sum (A/B: DESIGN.md K10)
+#endif
+#ifndef BSK_TOPK_QCAP
+#define BSK_TOPK_QCAP 256 // fused top-k: per-warp survivor queue entries
+#endif
 #ifndef BSK_TOPK_PACK
 #define BSK_TOPK_PACK 0   // fused top-k: 16-bit packed TMEM loads, two per wait (measured slower: DESIGN.md K10)
 #endif
@@ -748,7 +754,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t rt = lb + (uint32_t)lane;          // row within the tile
     const uint32_t grp = (uint32_t)(warp - 2) >> 2;   // this warp's group
     const uint32_t m = p.measure, K = p.k;
-    constexpr uint32_t kQCap = 256;                   // per-warp survivor queue entries
+    constexpr uint32_t kQCap = BSK_TOPK_QCAP;         // per-warp survivor queue entries
     // shared-memory layout (host: topk_heap_smem): heaps | per-group scratch | metadata ring |
     // per-warp queues, candidates, owner masks | per-row count, threshold, lock
     uint8_t* xp = extra;
@@ -915,15 +921,32 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (fmin(La, Ls[hi_]) < t) return pmax + 1;               // no pair of the tile can enter
         // fp32 start (hardware exp); its error is far below the 2-step margin, and the
         // result is made exact by the table refinement below
+#if BSK_PMIN_FAST
+        // (MUFU exp: the absolute error of pr stays below 1e-3 for N <= 65536)
+        const float pr = (float)p.N * (1.0f - __expf((float)((La + Llo - t) * p.lc)));
+#else
         const float pr = -(float)p.N * expm1f((float)((La + Llo - t) * p.lc));
+#endif
         const float q0 = (float)pa + (float)lo - fminf(floorf(pr) + 2.0f, (float)p.N);
         // q0 is a lower bound of the exact answer (the fp32 error of pr is < 0.01, far below the
         // 2-step margin), so only the upward refinement is needed
         uint32_t qq = q0 <= 0.0f ? 0u : min((uint32_t)q0, pmax);
         // refinement, four candidates per step evaluated independently (the answer is
         // typically within q0 + 3): the first qq with key_bound(qq) >= g
+#if BSK_PMIN_FAST
+        // IP: with t = g > 0 and min(La, L[hi]) >= g checked above, key_bound(pab) >= g is
+        // exactly (La + L[lo]) - L[pu(pab)] >= g — the same fp64 expression, the rest hoisted
+        const double sab = La + Llo;
+        const uint32_t pl = pa + lo;
+#endif
         for (;;) {
           bool ok[4];
+#if BSK_PMIN_FAST
+          if (m == 1u) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ok[u] = qq + u > pmax || sab - Ls[min(pl - min(qq + u, pl), p.N)] >= g;
+          } else
+#endif
 #pragma unroll
           for (int u = 0; u < 4; ++u) ok[u] = qq + u > pmax || key_bound(qq + u, lo, hi_) >= g;
           if (ok[0] || ok[1] || ok[2] || ok[3]) {
@@ -1640,7 +1663,7 @@ static uint32_t tc_topk_tn(uint32_t N) { return tc_topk_atm(N) ? 128u : (uint32_
 // the staged cardinality table.
 static uint32_t topk_heap_smem(uint32_t N, uint32_t k) {
   const uint32_t ne = tc_topk_atm(N) ? TcRoles<kTcTopkT>::kEpi : TcRoles<kTcTopk>::kEpi;
-  return k * kTcM * 12 + (ne / 4) * 32 * kTcM * 4 + 4 * kTcN * 8 + ne * 256 * 8 + ne * 32 * 16 + ne * 32 * 4 + kTcM * 20;
+  return k * kTcM * 12 + (ne / 4) * 32 * kTcM * 4 + 4 * kTcN * 8 + ne * BSK_TOPK_QCAP * 8 + ne * 32 * 16 + ne * 32 * 4 + kTcM * 20;
 }
 static uint32_t topk_table_smem(uint32_t N) { return (uint32_t)((((uint64_t)N + 1) * 8 + 15) / 16 * 16); }
 

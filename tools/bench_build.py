@@ -20,9 +20,14 @@ ap.add_argument("--config", default="buildonly")
 ap.add_argument("--modes", default="auto,global,cache,seeded")
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--bcs", action="store_true", help="BCS parity sketch (XOR) instead of BinSketch (OR)")
+ap.add_argument("--perm", type=int, default=1,
+                help="1: seeded Zipf rank -> id permutation (default); 0: identity (hot ids first: the "
+                     "cache-sensitivity row of SURVEY.md 8(d))")
 a = ap.parse_args()
 spec, N = {"buildonly": (synth.BUILD_ONLY, synth.BUILD_ONLY_N), "large": (synth.LARGE, synth.LARGE_N),
            "ranking": (synth.RANKING_DB, synth.RANKING_N), "medium": (synth.MEDIUM, 1000)}[a.config]
+import dataclasses
+spec = dataclasses.replace(spec, perm=a.perm)
 ip_h, ix_h = synth.make_csr(spec)
 n, d, W, nnz = spec.n, spec.d, (N + 31) // 32, int(ip_h[-1])
 ip, ix = torch.from_numpy(ip_h).cuda(), torch.from_numpy(ix_h).cuda()
@@ -53,5 +58,5 @@ for mode in a.modes.split(","):
     bs.device_status()
     ok = np.array_equal(out[torch.from_numpy(rows).cuda()].cpu().numpy().view(np.uint32), ref)
     t = statistics.median(ts)
-    print(json.dumps({"config": a.config, "sketch": "bcs" if a.bcs else "binsketch", "mode": mode, "ms": t * 1e3, "rows_per_s": n / t,
+    print(json.dumps({"config": a.config, "perm": a.perm, "sketch": "bcs" if a.bcs else "binsketch", "mode": mode, "ms": t * 1e3, "rows_per_s": n / t,
                       "alg_GBps": alg / t / 1e9, "frac_hbm_6555": alg / t / 6555.2e9, "parity_sampled": ok}), flush=True)
