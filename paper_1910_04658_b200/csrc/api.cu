@@ -263,7 +263,8 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
     l.spb = off; off += align_up((size_t)nb * 4);
     l.qperm = off; off += align_up((size_t)na * 4);
     l.qspb = off; off += align_up((size_t)na * 4);
-    l.tmeta = off; off += align_up((size_t)((nb + 255) / 256) * 256 * 8);   // per-tile db metadata
+    l.tmeta = off; off += align_up((size_t)((nb + 255) / 256) * 256 * 8 +     // per-tile db metadata
+                                   (size_t)((nb + 255) / 256) * 2 * 4);        // + per-tile smallest db index
   }
   if (op == BINSKETCH_OP_TOPK) {
     l.splits = tc ? bsk::tc_topk_splits(na, nb, N, k) : bsk::topk_splits(na, nb, k);

@@ -273,6 +273,9 @@ __device__ __forceinline__ void tmem_ld_wait16x2(uint32_t (&a)[16], uint32_t (&b
 #ifndef BSK_PMIN_FAST
 #define BSK_PMIN_FAST 1   // fused top-k: tile bound start by MUFU exp, IP refinement on the hoisted sum (A/B: DESIGN.md K10)
 #endif
+#ifndef BSK_TOPK_STRICT
+#define BSK_TOPK_STRICT 1 // fused top-k (IP): exact strict bound on single-popcount tiles where no tie can enter
+#endif
 #ifndef BSK_TOPK_QCAP
 #define BSK_TOPK_QCAP 256 // fused top-k: per-warp survivor queue entries
 #endif
@@ -366,6 +369,18 @@ __global__ void pb_scan_kernel(uint32_t* __restrict__ bins, uint32_t nbins) {   
   for (uint32_t i = b0; i < b1; ++i) { const uint32_t c = bins[i]; bins[i] = run; run += c; }
 }
 
+// Smallest original db index of each TN-row db tile (one block of TN threads per tile).
+__global__ void tile_min_kernel(const int2* __restrict__ meta, int32_t* __restrict__ tmin) {
+  __shared__ int32_t wm[8];
+  const int2 e = meta[(uint64_t)blockIdx.x * blockDim.x + threadIdx.x];
+  int32_t v = __reduce_min_sync(0xffffffffu, e.y < 0 ? 0x7fffffff : e.y);
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < blockDim.x / 32; ++w) v = min(v, wm[w]);
+    tmin[blockIdx.x] = v;
+  }
+}
 __global__ void pb_scatter_kernel(const int32_t* __restrict__ pb, uint64_t n, uint32_t N, uint32_t desc,
                                   uint32_t* __restrict__ cursor, int32_t* __restrict__ perm, int32_t* __restrict__ spb) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -448,6 +463,7 @@ struct TcParams {
   uint32_t l_smem;        // kTcEstimate: table staged in shared memory (bytes, 0 = not staged)
   uint32_t heap_smem;     // kTcTopk: per-row heaps + survivor scratch in shared memory (bytes)
   const int2* meta;       // kTcTopk: per db tile [256] (|b_s|, original index), padded to whole tiles
+  const int32_t* tmin;    // kTcTopk: per db tile (TN rows) the smallest original index
   const int32_t* perm;    // kTcTopk: B row (sorted by |b_s|, descending for IP, else ascending) -> original db index
   uint32_t l_topk_smem;   // kTcTopk: table staged after the heaps (bytes, 0 = global)
   double lc;              // log1p(-1/N): closed-form inverse of the table for the tile bound
@@ -897,14 +913,19 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       // smallest pab whose bound reaches the current threshold g (slack for fp64 rounding):
       // closed-form start from the inverse of L(p) = log1p(-p/N)/log1p(-1/N) with a 2-step
       // low margin, then exact refinement on the staged table (typically 1-3 evaluations)
-      uint32_t c_lo = 0xFFFFFFFFu, c_hi = 0, c_pmin = 0;   // last (lo, hi, T) -> pmin
+      uint32_t c_lo = 0xFFFFFFFFu, c_hi = 0, c_pmin = 0;   // last (lo, hi, T, strict) -> pmin
+      bool c_strict = false;
       double c_T = 0.0;
-      auto tile_pmin = [&](uint32_t lo, uint32_t hi_) -> uint32_t {
+      // strict (IP, a single-popcount tile whose db indices all exceed the row's k-th index):
+      // the bound is then the exact key (same fp64 expression) and a tie cannot enter, so the
+      // smallest pab whose bound EXCEEDS the threshold is taken (no rounding slack needed)
+      auto tile_pmin = [&](uint32_t lo, uint32_t hi_, bool strict) -> uint32_t {
         if (!filt || cnt < K || lo == 0) return 0u;
+        strict = strict && T >= 0.0;
 #ifdef BSK_PMIN_STALE
         if (lo == c_lo && hi_ == c_hi) return c_pmin;   // dev A/B: a stale (lower) threshold is conservative
 #else
-        if (lo == c_lo && hi_ == c_hi && T == c_T) return c_pmin;   // sorted db: runs of equal ranges
+        if (lo == c_lo && hi_ == c_hi && T == c_T && strict == c_strict) return c_pmin;   // sorted db: runs of equal ranges
 #endif
 #ifdef BSK_TOPK_STATS
         atomicAdd(&g_tkstats[15], 1ull);   // (lane, tile) bound recomputations
@@ -912,6 +933,26 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const double g = T - 1e-9 * fmax(1.0, fabs(T));
         const uint32_t pmax = min((uint32_t)pa, hi_);
         const double Llo = Ls[lo];
+#if BSK_TOPK_STRICT
+        if (strict) {   // (m == 1, lo == hi, T >= 0): U(pab) = the key, exactly; find the first U > T
+          if (fmin(La, Ls[hi_]) <= T) { c_lo = lo; c_hi = hi_; c_T = T; c_strict = true; c_pmin = pmax + 1; return pmax + 1; }
+          const float prs = (float)p.N * (1.0f - __expf((float)((La + Llo - T) * p.lc)));
+          const float q0s = (float)pa + (float)lo - fminf(floorf(prs) + 2.0f, (float)p.N);
+          uint32_t qs = q0s <= 0.0f ? 0u : min((uint32_t)q0s, pmax);
+          const double sab = La + Llo;
+          const uint32_t pl = pa + lo;
+          for (;;) {
+            bool ok[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ok[u] = qs + u > pmax || sab - Ls[min(pl - min(qs + u, pl), p.N)] > T;
+            if (ok[0] || ok[1] || ok[2] || ok[3]) { qs += ok[0] ? 0u : (ok[1] ? 1u : (ok[2] ? 2u : 3u)); break; }
+            qs += 4;
+          }
+          qs = min(qs, pmax + 1);
+          c_lo = lo; c_hi = hi_; c_T = T; c_strict = true; c_pmin = qs;
+          return qs;
+        }
+#endif
         double t;   // U(pab) >= t  <=>  key bound >= g
         if (m == 1u) t = g;
         else if (m == 4u) t = g > -1.0 ? g * (La + Llo) / (1.0 + g) : -1.0;
@@ -956,7 +997,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           qq += 4;
         }
         qq = min(qq, pmax + 1);
-        c_lo = lo; c_hi = hi_; c_T = T; c_pmin = qq;
+        c_lo = lo; c_hi = hi_; c_T = T; c_strict = false; c_pmin = qq;
         return qq;
       };
       for (uint32_t nt = nt0; nt < nt1; ++nt) {
@@ -965,6 +1006,9 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int acc = (int)(my % kTcAcc);
         const uint32_t aphase = (my / kTcAcc) & 1u;
         BSK_T0(te0);
+#if BSK_TOPK_STRICT
+        const int32_t tmin_t = m == 1u ? __ldg(p.tmin + nt) : 0;   // (consumed after the refresh and metadata wait)
+#endif
         refresh();
         const uint64_t n0 = (uint64_t)nt * TN;
         // this tile's db popcounts / original indices, bulk-loaded by the producer
@@ -977,7 +1021,14 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         { const uint32_t x0 = (uint32_t)tm[nval - 1].x + (uint32_t)tm[0].x; if (x0 == 0xFFFFFFFFu) pmin = 1u; }
         if (lane == 0) BSK_TADD(13, te0);
 #endif
-        if (valid) pmin = tile_pmin(min((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x), max((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x));
+        {
+          const uint32_t tlo = min((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x), thi = max((uint32_t)tm[nval - 1].x, (uint32_t)tm[0].x);
+          bool strict = false;
+#if BSK_TOPK_STRICT
+          if (m == 1u && tlo == thi) strict = tmin_t > Ti;   // (tmin_t: smallest db index of the tile)
+#endif
+          if (valid) pmin = tile_pmin(tlo, thi, strict);
+        }
         const bool direct = __any_sync(0xffffffffu, cnt < K);
 #ifdef BSK_TOPK_STATS
         {
@@ -1730,6 +1781,13 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
     tile_meta_kernel<<<(unsigned)blocks, 256, 0, s>>>(pd, perm, ndb, npad, meta);
     count_launch();
     p.meta = meta;
+#if BSK_TOPK_STRICT
+    int32_t* tmin = reinterpret_cast<int32_t*>(meta + npad);
+    const uint32_t tn = tc_topk_tn(N);
+    tile_min_kernel<<<(unsigned)(npad / tn), tn, 0, s>>>(meta, tmin);
+    count_launch();
+    p.tmin = tmin;
+#endif
   }
   cudaError_t e = atm ? tc_launch<kTcTopkT, 128>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, sc.splits, s)
                       : tc_launch<kTcTopk, 64>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, sc.splits, s);
