@@ -246,28 +246,6 @@ __device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[32]) {
 }
 
 
-// 32 lanes x 32 columns of 32-bit TMEM packed to 16 bits (.pack::16b keeps the low half of
-// each column; register i = column 2i in bits 0-15, column 2i+1 in bits 16-31) -> 16
-// registers, issued without waiting (tmem_ld_wait16x2 waits for both of a pair).
-__device__ __forceinline__ void tmem_ld16p_issue(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld_wait16x2(uint32_t (&a)[16], uint32_t (&b)[16]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-      : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
-        "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]), "+r"(a[13]), "+r"(a[14]), "+r"(a[15]),
-        "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7]),
-        "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]), "+r"(b[12]), "+r"(b[13]), "+r"(b[14]), "+r"(b[15])
-      :
-      : "memory");
-}
-
 }  // namespace tc
 
 #ifndef BSK_PMIN_FAST
@@ -278,9 +256,6 @@ __device__ __forceinline__ void tmem_ld_wait16x2(uint32_t (&a)[16], uint32_t (&b
 #endif
 #ifndef BSK_TOPK_QCAP
 #define BSK_TOPK_QCAP 256 // fused top-k: per-warp survivor queue entries
-#endif
-#ifndef BSK_TOPK_PACK
-#define BSK_TOPK_PACK 0   // fused top-k: 16-bit packed TMEM loads, two per wait (measured slower: DESIGN.md K10)
 #endif
 #ifdef BSK_TOPK_PROF
 #define BSK_T0(v) const long long v = clock64()
@@ -491,16 +466,6 @@ __device__ __forceinline__ uint32_t max32(const uint32_t (&v)[32]) {
   const uint32_t b0 = __vimax3_u32(a[0], a[1], a[2]), b1 = __vimax3_u32(a[3], a[4], a[5]);
   const uint32_t b2 = __vimax3_u32(a[6], a[7], a[8]), b3 = max(a[9], a[10]);
   return max(__vimax3_u32(b0, b1, b2), b3);
-}
-// Max of 32 16-bit values packed two per register (the high and low halves of 16 words):
-// a 3-input tree of paired 16-bit maxima (VIMNMX3 .U16x2), then the larger half.
-__device__ __forceinline__ uint32_t max16p(const uint32_t (&v)[16]) {
-  uint32_t a[6];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) a[i] = __vimax3_u16x2(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
-  a[5] = v[15];
-  const uint32_t m = __vmaxu2(__vimax3_u16x2(a[0], a[1], a[2]), __vimax3_u16x2(a[3], a[4], a[5]));
-  return max(m & 0xffffu, m >> 16);
 }
 // Bit j set iff v[j] >= t, built in four independent partial masks.
 __device__ __forceinline__ uint32_t ge_mask32(const uint32_t (&v)[32], uint32_t t) {
@@ -1163,26 +1128,6 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #else
         if (__any_sync(0xffffffffu, valid && (cnt < K || pmin <= min((uint32_t)pa, tile_hi)))) {
 #endif
-#if BSK_TOPK_PACK
-          // 64 columns per TMEM wait: two 32-column loads packed to 16 bits (pab <= N <= 1024;
-          // LDTM .PACK16BIT, register i = columns 2i | 2i+1 << 16) in flight together, in the
-          // register footprint of one unpacked chunk; one vote rejects both chunks
-          uint32_t pk0[16], pk1[16];
-#pragma unroll 1
-          for (uint32_t c = 0; c < nval; c += 64) {
-            tc::tmem_ld16p_issue(tb + c, pk0);
-            if (c + 32 < nval) tc::tmem_ld16p_issue(tb + c + 32, pk1);   // (warp-uniform)
-            else {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) pk1[i] = 0u;
-            }
-            tc::tmem_ld_wait16x2(pk0, pk1);
-            const uint32_t m0 = max16p(pk0), m1 = max16p(pk1);
-            if (!__any_sync(0xffffffffu, valid && max(m0, m1) >= pmin)) continue;
-            chunk(c, m0, [&](int j) { return (j & 1) ? (pk0[j >> 1] >> 16) : (pk0[j >> 1] & 0xffffu); });
-            chunk(c + 32, m1, [&](int j) { return (j & 1) ? (pk1[j >> 1] >> 16) : (pk1[j >> 1] & 0xffffu); });
-          }
-#else
           uint32_t va[32];
 #pragma unroll 1
           for (uint32_t c = 0; c < nval; c += 32) {   // one 32-column chunk at a time (register budget)
@@ -1194,7 +1139,6 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #endif
             chunk(c, max32(va), [&](int j) { return va[j]; });
           }
-#endif
         }
         release_acc(acc);
         if (lane == 0) BSK_TADD(7, te2);
