@@ -307,6 +307,27 @@ def test_topk_k_sizes_and_ties(k, engine):
     _check_topk(Q, D, N, d, 4, k)
 
 
+@pytest.mark.parametrize("k", [1, 50])
+def test_topk_strict_bound_single_popcount_tiles(k, engine):
+    """The fused IP top-k's strict tile bound (tc.cu, BSK_TOPK_STRICT): on a tile whose db rows all have
+    one popcount and whose db indices all exceed the row's k-th index, only keys ABOVE the threshold are
+    admitted. Whole 128-row tiles of identical sketches (at low and at high indices, so both branches of
+    the index test occur), a block of empty rows (lo = 0), and sparse queries whose k-th key is 0 (T = 0,
+    thousands of ties) — lists and scores bit-identical to the oracle."""
+    N, d = 1024, 500_000
+    D = _sketches(synth.scaled(synth.LARGE, 4000), N)
+    D[40:440] = D[3]                     # ~3 whole tiles of one sketch at low indices
+    D[2500:3100] = D[11]                 # ~5 whole tiles at high indices
+    D[3300:3500] = 0                     # empty db rows
+    Q = np.concatenate([D[:60], D[2490:2520], D[3290:3310]]).copy()
+    sparse = np.zeros_like(D[:8])        # a few bits each: most keys are 0
+    for i in range(8):
+        sparse[i, i] = 1 << (3 * i % 32)
+    Q = np.concatenate([Q, sparse])
+    _check_topk(Q, D, N, d, 1, k)
+    _check_topk(D, D, N, d, 1, k, exclude_self=True)
+
+
 def test_topk_padding_and_empty_db(engine):
     N, d = 64, 1000
     D = _sketches(synth.CSRSpec(n=20, d=d, kind=0, p1=5, p2=20, cap=20, zipf_s=1.1, seed=3), N)
