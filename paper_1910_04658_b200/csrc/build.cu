@@ -297,6 +297,25 @@ struct Tile {
   uint32_t rows;  // rows in the tile
 };
 
+// Checked build (-DBSK_CHECKED; a dev library, never the product): every shared-memory access of
+// K1 is range-checked against the regions it may touch — the block-wide pi table / cache, or the
+// warp's OWN ring / stages / bitmap / mbarriers / zero row (so no warp reads or writes another
+// warp's rows: the inter-warp race a racecheck would look for) — and a violation traps the kernel.
+#ifdef BSK_CHECKED
+#define BSK_CHKE(a, n) (chk_ok((uint32_t)(a), (uint32_t)(n)) ? (void)0 : __trap())
+#define BSK_CHK(a, n) BSK_CHKE(a, n)
+#define lds_u16(a) (BSK_CHKE(a, 2), lds_u16(a))
+#define lds_u32(a) (BSK_CHKE(a, 4), lds_u32(a))
+#define lds_v2(a) (BSK_CHKE(a, 8), lds_v2(a))
+#define lds_v4(a) (BSK_CHKE(a, 16), lds_v4(a))
+#define sts_u16(a, v) (BSK_CHKE(a, 2), sts_u16(a, v))
+#define sts_u32(a, v) (BSK_CHKE(a, 4), sts_u32(a, v))
+#define sts_v4(a, x, y, z, w) (BSK_CHKE(a, 16), sts_v4(a, x, y, z, w))
+#define sts_u16_if(q, a, v) (BSK_CHKE(a, 2), sts_u16_if(q, a, v))
+#define sts_u32_if(q, a, v) (BSK_CHKE(a, 4), sts_u32_if(q, a, v))
+#else
+#define BSK_CHK(a, n) do {} while (0)
+#endif
 template <int MODE, int LOGN, bool XOR>
 __global__ void __launch_bounds__(BuildCfg<MODE>::kThreads, BuildCfg<MODE>::kBlocks)
 build_kernel(const BuildParams p) {
@@ -320,6 +339,18 @@ build_kernel(const BuildParams p) {
   const uint32_t zero_a = mbar_a + 8 * kNS;           // one all-zero sketch row (flush of empty rows)
   const uint64_t seed1 = p.seed + 0x9E3779B97F4A7C15ULL;
   const uint32_t vb = p.vb, vmask = (1u << vb) - 1u;
+#ifdef BSK_CHECKED
+  auto chk_ok = [&](uint32_t a, uint32_t n) -> bool {
+    const bool tab = a >= pi_a && a + n <= pi_a + p.pi_bytes;
+#ifdef BSK_CHECKED_SELFTEST
+    const bool ring = a >= ring_a && a + n <= ring_a + ringB - Wb;   // (the checker's own test: one ring row short)
+#else
+    const bool ring = a >= ring_a && a + n <= ring_a + ringB;
+#endif
+    const bool aux = a >= stage_a && a + n <= stage_a + p.aux_bytes;
+    return (n > 16 || (a & (n - 1)) == 0) && (tab || ring || aux);   // (natural alignment of the access widths)
+  };
+#endif
 
   unsigned bad = 0;
   uint32_t maxj = 0, maxidx = 0;
@@ -393,6 +424,7 @@ build_kernel(const BuildParams p) {
               maxj = max(maxj, jj);
               jj = min(jj, N - 1);
             }
+            BSK_CHK(ring_a + ((jj >> 5) << 2), 4);
             put_bit<XOR>(ring_a + ((jj >> 5) << 2), 1u << (jj & 31u));
           }
         }
@@ -533,6 +565,8 @@ build_kernel(const BuildParams p) {
         // (no proxy fence: the slot's previous contents were read by LDS whose results the
         // warp consumed before this point, and the mbarrier wait orders the copy's writes)
         const uint32_t slot = stage_a + (uint32_t)(k % kNS) * SB, mb = mbar_a + 8u * (uint32_t)(k % kNS);
+        BSK_CHK(mb, 8);
+        BSK_CHK(slot, (uint32_t)SB);
         if (nb > 0) {
           mbar_expect_tx(mb, (uint32_t)nb);
           bulk_load(slot, src0 + s, (uint32_t)nb, mb);
@@ -546,9 +580,9 @@ build_kernel(const BuildParams p) {
         sts_v4(meta_a + 16 * lane, 0u, 0u, 0u, 0u);
         __syncwarp();
         int q = T0.e - b0;
-        if (((T0.ne >> lane) & 1u) && q > 0 && q < kChunk) put_bit<false>(meta_a + 8 * (uint32_t)(q >> 5), 1u << (q & 31));
+        if (((T0.ne >> lane) & 1u) && q > 0 && q < kChunk) { BSK_CHK(meta_a + 8 * (uint32_t)(q >> 5), 4); put_bit<false>(meta_a + 8 * (uint32_t)(q >> 5), 1u << (q & 31)); }
         q = T1.e - b0;
-        if (((T1.ne >> lane) & 1u) && q > 0 && q < kChunk) put_bit<false>(meta_a + 8 * (uint32_t)(q >> 5), 1u << (q & 31));
+        if (((T1.ne >> lane) & 1u) && q > 0 && q < kChunk) { BSK_CHK(meta_a + 8 * (uint32_t)(q >> 5), 4); put_bit<false>(meta_a + 8 * (uint32_t)(q >> 5), 1u << (q & 31)); }
         const uint32_t before = T0.c + __popc(T0.ne & __ballot_sync(kFull, T0.e <= b0)) +
                                 __popc(T1.ne & __ballot_sync(kFull, T1.e <= b0));
         __syncwarp();
@@ -665,10 +699,10 @@ build_kernel(const BuildParams p) {
                          : ring_a + (rowp[u] & (RR - 1u)) * Wb + (j[u] >> 3);
         if (PRED) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) put_bit_if<XOR>(ok[u], addr[u], bit[u]);
+          for (int u = 0; u < 8; ++u) { if (ok[u]) BSK_CHK(addr[u], 4); put_bit_if<XOR>(ok[u], addr[u], bit[u]); }
         } else {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) put_bit<XOR>(addr[u], bit[u]);
+          for (int u = 0; u < 8; ++u) { BSK_CHK(addr[u], 4); put_bit<XOR>(addr[u], bit[u]); }
         }
       };
 
@@ -734,6 +768,20 @@ build_kernel(const BuildParams p) {
   if (maxidx >= d || maxj >= N) bad = 1;
   if (__any_sync(kFull, bad != 0) && lane == 0) latch(p.status, kStatusIndex);
 }
+
+#ifdef BSK_CHECKED
+#undef lds_u16
+#undef lds_u32
+#undef lds_v2
+#undef lds_v4
+#undef sts_u16
+#undef sts_u32
+#undef sts_v4
+#undef sts_u16_if
+#undef sts_u32_if
+#endif
+#undef BSK_CHK
+#undef BSK_CHKE
 
 // Fallback for very wide sketches (one row's W words do not fit the per-warp ring) and for
 // index arrays that are not 16-B aligned (the bulk copies need it): rows zeroed by

@@ -248,6 +248,13 @@ __device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[32]) {
 
 }  // namespace tc
 
+// Checked build (-DBSK_CHECKED, a dev library): index invariants of the top-k epilogue's shared
+// structures (heap slots, survivor queue, owner lanes, metadata columns) trap when violated.
+#ifdef BSK_CHECKED
+#define BSK_ASSERT(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define BSK_ASSERT(c) do {} while (0)
+#endif
 #ifndef BSK_PMIN_FAST
 #define BSK_PMIN_FAST 1   // fused top-k: tile bound start by MUFU exp, IP refinement on the hoisted sum (A/B: DESIGN.md K10)
 #endif
@@ -750,8 +757,8 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     volatile double* Tp = reinterpret_cast<volatile double*>(xp);        xp += kTcM * 8;
     volatile int32_t* Tip = reinterpret_cast<volatile int32_t*>(xp);     xp += kTcM * 4;
     uint32_t* lk = reinterpret_cast<uint32_t*>(xp);
-    auto hkey = [&](uint32_t i) -> double& { return hk[i * kTcM + rt]; };
-    auto hidx = [&](uint32_t i) -> int32_t& { return hi[i * kTcM + rt]; };
+    auto hkey = [&](uint32_t i) -> double& { BSK_ASSERT(i < K); return hk[i * kTcM + rt]; };
+    auto hidx = [&](uint32_t i) -> int32_t& { BSK_ASSERT(i < K); return hi[i * kTcM + rt]; };
     auto epi_bar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpi) : "memory"); };
     uint32_t tcount = 0;   // tiles seen (every group): accumulator, metadata slot and phases
     for (uint32_t ii = 0;; ++ii) {
@@ -1016,6 +1023,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const bool has = b + lane < qn;
             const uint2 e = has ? q[b + lane] : make_uint2(0u, 0u);
             const int owner = (int)(e.y >> 24);
+            BSK_ASSERT(!has || (owner < 32 && e.x < TN));
             const int pa_o = __shfl_sync(0xffffffffu, pa, owner);
             const double T_o = __shfl_sync(0xffffffffu, T, owner);
             const int32_t Ti_o = __shfl_sync(0xffffffffu, Ti, owner);
@@ -1044,6 +1052,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               uint32_t mine = own[lane];
               while (mine) {
                 const uint32_t ee = __ffs(mine) - 1; mine &= mine - 1;
+                BSK_ASSERT(ee < 32u);
                 const uint4 c4 = cq[ee];
                 offer(__hiloint2double((int)c4.w, (int)c4.z), tm[c4.x].y);
               }
@@ -1114,7 +1123,7 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           off += qn;
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if ((sm >> j) & 1u) q[off++] = make_uint2(c + (uint32_t)j, ((uint32_t)lane << 24) | V(j));
+            if ((sm >> j) & 1u) { BSK_ASSERT(off < kQCap && c + (uint32_t)j < TN); q[off++] = make_uint2(c + (uint32_t)j, ((uint32_t)lane << 24) | V(j)); }
           qn += total;
           __syncwarp();
                 };
