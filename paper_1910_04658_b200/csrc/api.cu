@@ -492,10 +492,11 @@ static binsketch_status topk_impl(const uint32_t* queries, uint64_t nq, const ui
     // reached earlier from below (ascending: JS 302 -> 214, COS 260 -> 158, HAM 870 -> 90 ms)
     if (sorted) e = bsk::launch_sort_by_popcount(pd, ndb, N, bins, perm, spb, s, measure_m == BINSKETCH_IP);
     if (qsort && e == cudaSuccess) e = bsk::launch_sort_by_popcount(pq, nq, N, bins, qperm, qspb, s);
-    if (e == cudaSuccess) e = bsk::launch_expand(queries, nq, N, q8, s, qperm);
+    const bool packed_q = bsk::tc_topk_packed_queries(N);   // widened in the kernel, into TMEM
+    if (e == cudaSuccess && !packed_q) e = bsk::launch_expand(queries, nq, N, q8, s, qperm);
     if (e == cudaSuccess) e = bsk::launch_expand(db, ndb, N, d8, s, perm);
     if (e == cudaSuccess)
-      e = bsk::launch_tc_topk(q8, nq, d8, ndb, N, measure_m, k, flags, qspb, qperm, spb, perm,
+      e = bsk::launch_tc_topk(q8, queries, nq, d8, ndb, N, measure_m, k, flags, qspb, qperm, spb, perm,
                               reinterpret_cast<const double*>(w + l.L), cache().convex(N, d),
                               reinterpret_cast<double*>(w + l.pkey), reinterpret_cast<int32_t*>(w + l.pidx),
                               out_idx_m, out_score_m, reinterpret_cast<unsigned long long*>(w + l.ctr),

@@ -125,7 +125,10 @@ cudaError_t launch_sort_by_popcount(const int32_t* pb, uint64_t n, uint32_t N, u
                                     int32_t* spb, cudaStream_t s, bool descending = true);
 // Q8 rows in `qperm` order and D8 rows in `perm` order (nullptr: original order); pq / pd the
 // matching popcounts. Results land at the original query indices.
-cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
+// tc_topk_packed_queries(N): the kernel widens the queries itself from the packed sketches Qsk
+// (original order; Q8 is then not read and may be null); else Q8 holds the widened rows.
+bool tc_topk_packed_queries(uint32_t N);
+cudaError_t launch_tc_topk(const uint8_t* Q8, const uint32_t* Qsk, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
                            uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* qperm,
                            const int32_t* pd, const int32_t* perm, const double* L, bool prefilter, double* part_key,
                            int32_t* part_idx, int32_t* out_idx, float* out_score, unsigned long long* ctr,

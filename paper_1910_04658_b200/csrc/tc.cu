@@ -450,7 +450,8 @@ struct TcParams {
   uint32_t l_topk_smem;   // kTcTopk: table staged after the heaps (bytes, 0 = global)
   double lc;              // log1p(-1/N): closed-form inverse of the table for the tile bound
   const int32_t* qperm;   // kTcTopk: A row (queries sorted by |a_s| descending) -> original query index
-  const uint8_t* a8;      // kTcTopkT: the widened query rows [na][kp] (loaded into TMEM per item)
+  const uint32_t* qsk;    // kTcTopkT: the PACKED query sketches [na][qw] in their original order, widened
+  uint32_t qw;            //   into TMEM per item by the epilogue warps (no widened copy in HBM)
   uint32_t kp;            // kTcTopkT: bytes per widened row (Kp <= 1024)
   unsigned long long* item_ctr;   // dynamic work queue: next item (zeroed before the launch)
   uint32_t* bits;         // kTcJoin: match bitmaps [nthr][na][wpr] (zeroed before the launch)
@@ -770,16 +771,21 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       item_range(it, mt, sp, nt0, nt1);
       const uint64_t r = mt * kTcM + rt;               // row of the (sorted) query matrix
       const bool valid = r < p.na;
+      const uint64_t rq = (valid && p.qperm) ? (uint64_t)__ldg(p.qperm + r) : r;   // original query index
       if (ATM && grp == 0) {
-        // this item's 128 query rows -> TMEM columns [0, kp/4) (lane = row, 4 K-bytes per column).
-        // The previous item's MMAs are complete (this warp waited on its last accumulator).
-        const uint4* src = reinterpret_cast<const uint4*>(p.a8 + (valid ? r : 0) * p.kp);
-        for (uint32_t c0 = 0; c0 < p.kp / 4u; c0 += 32) {
-          uint32_t v[32];
+        // this item's 128 query rows -> TMEM columns [0, kp/4) (lane = row, 4 K-bytes per column),
+        // widened here from the packed sketch (column c = nibble c: bytes {bit 4c, .., bit 4c+3},
+        // the expand_kernel layout of the B operand). The previous item's MMAs are complete (this
+        // warp waited on its last accumulator).
+        const uint32_t* src = p.qsk + (valid ? rq : 0) * p.qw;
+        for (uint32_t c0 = 0; c0 < p.kp / 4u; c0 += 32) {   // 32 columns = 4 sketch words
+          uint32_t wd[4], v[32];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint4 x = valid ? __ldg(src + c0 / 4u + j) : make_uint4(0u, 0u, 0u, 0u);
-            v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
+          for (int j = 0; j < 4; ++j) wd[j] = (valid && c0 / 8u + j < p.qw) ? __ldg(src + c0 / 8u + j) : 0u;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const uint32_t nib = (wd[q >> 3] >> (4 * (q & 7))) & 0xFu;
+            v[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
           }
           tc::tmem_st32(tmem + (lb << 16) + c0, v);
         }
@@ -789,7 +795,6 @@ tc_pairs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (lane == 0) tc::mbar_arrive(aready);
       }
       const int pa = valid ? __ldg(p.pa + r) : 0;
-      const uint64_t rq = (valid && p.qperm) ? (uint64_t)__ldg(p.qperm + r) : r;   // original query index
       const double La = Ls[pa];
       const bool filt = p.prefilter && pa > 0;
       uint32_t cnt = valid ? 0u : K, pmin = 0;   // invalid rows count as full (never insert)
@@ -1551,8 +1556,9 @@ static cudaError_t tc_launch_cg(const uint8_t* A8, const uint8_t* B8, TcParams& 
   if (const char* st = std::getenv("BINSKETCH_TC_STAGES"))   // dev A/B: cap the ring depth
     p.stages = std::max<uint32_t>(2u, std::min<uint32_t>(p.stages, (uint32_t)std::atoi(st)));
   alignas(64) CUtensorMap ma, mb;
-  if (!make_map(&ma, A8, p.na, Kp, kTcM, KC) || !make_map(&mb, B8, p.nb, Kp, ATM ? TN : kTcN / CG, KC))
-    return cudaErrorNotSupported;
+  if (!make_map(&mb, B8, p.nb, Kp, ATM ? TN : kTcN / CG, KC)) return cudaErrorNotSupported;
+  if (ATM) ma = mb;   // (A is not TMA-loaded: the epilogue widens the packed rows into TMEM)
+  else if (!make_map(&ma, A8, p.na, Kp, kTcM, KC)) return cudaErrorNotSupported;
   cudaError_t e = cudaSuccess;
   p.nk = Kp / KC;
   p.tiles_n = (uint32_t)((p.nb + TN - 1) / TN);
@@ -1704,7 +1710,9 @@ uint32_t tc_topk_splits(uint64_t nq, uint64_t ndb, uint32_t N, uint32_t k) {
   return r.chain ? 1u : r.splits;
 }
 
-cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
+bool tc_topk_packed_queries(uint32_t N) { return tc_topk_atm(N); }
+
+cudaError_t launch_tc_topk(const uint8_t* Q8, const uint32_t* Qsk, uint64_t nq, const uint8_t* D8, uint64_t ndb, uint32_t N,
                            uint32_t measure, uint32_t k, uint32_t flags, const int32_t* pq, const int32_t* qperm,
                            const int32_t* pd, const int32_t* perm, const double* L, bool prefilter, double* part_key,
                            int32_t* part_idx, int32_t* out_idx, float* out_score, unsigned long long* ctr,
@@ -1724,8 +1732,10 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, uint64_t nq, const uint8_t* D8, ui
   p.l_topk_smem = lb;
   // splits computed with the device-independent rule (148) so the workspace matches
   const TcSplit sc = tc_split_rule(nq, ndb, N, true, k, tc_topk_tn(N));
-  p.a8 = Q8;
+  p.qsk = Qsk;
+  p.qw = (N + 31) / 32;
   p.kp = tc_kpad(N);
+  if (atm && !Qsk) return cudaErrorInvalidValue;
   p.chain = sc.chain;
   p.done = done;
   {
