@@ -1507,7 +1507,7 @@ cudaError_t launch_expand(const uint32_t* sk, uint64_t n, uint32_t N, uint8_t* o
 struct TcSplit { uint32_t splits, chain; };
 static TcSplit tc_split_rule(uint64_t na, uint64_t nb, uint32_t N, bool topk, uint32_t k = 0, uint32_t tn = kTcN) {
   const uint64_t tiles_n = (nb + tn - 1) / tn, mtiles = (na + kTcM - 1) / kTcM, sms = 148;
-  uint64_t chunk_bytes = 40ull << 20;
+  uint64_t chunk_bytes = (topk ? 48ull : 40ull) << 20;   // top-k, Large: 5 chunks of 41 MB (measured: 6 x 34 MB 39.68, 5 x 41 MB 39.40, 3 x 68 MB 41.12 ms)
   // dev knobs (sanitizer / A-B runs on small shapes): db chunk size in KB, forced heap chaining.
   // Read here only, so workspace sizing and the launch always agree.
   if (const char* e = std::getenv("BINSKETCH_TC_CHUNK_KB")) chunk_bytes = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 10;
