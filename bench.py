@@ -43,9 +43,9 @@ SM_COUNT_B200 = 148
 POPC_PER_CLK_SM = 15.11
 POPC_BASIS = "K9 measured 15.11 POPC/clk/SM (profiles/r02_microbench_k9.jsonl) x 148 SMs x SM clock"
 # ncu --set full of the fused top-k kernel at this workload (one launch).
-TOPK_NCU = {"source": "profiles/r02_packedq/topk_large_summary.txt", "tensor_pipe_active_pct": 45.9,
-            "issue_active_pct": 21.4, "dram_bytes_per_launch": 1.436e9 + 0.575e9, "kernel_share_of_stage": "98.3 %",
-            "launch_list": "profiles/r02_final5/launches_large_summary.txt"}
+TOPK_NCU = {"source": "profiles/r02_final6/topk_large_summary.txt", "tensor_pipe_active_pct": 45.9,
+            "issue_active_pct": 21.4, "dram_bytes_per_launch": 1.464e9 + 0.576e9, "kernel_share_of_stage": "98.4 %",
+            "launch_list": "profiles/r02_final6/launches_large_summary.txt"}
 # Ranking: the dominant kernel of the top-k call is the tensor-core AND-popcount with the integer
 # screen in its epilogue (tc_pairs_kernel<kTcScreen>, K4d). Its share of the call's
 # critical path from the committed launch list (cold-cache, serialised, ms per call): popcounts
