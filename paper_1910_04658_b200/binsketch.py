@@ -460,3 +460,104 @@ def topk_from_host_csr(db_indptr_h: torch.Tensor, db_indices_h: torch.Tensor, pi
     hs.copy_(osc, non_blocking=True)
     d2h = len(ms) * nq * k * 8
     return b["out_h"], h2d, d2h
+
+
+def topk_from_host_csr_batches(batches, pi_h: torch.Tensor, d: int, N: int, measures, k: int,
+                               exclude_self: bool = False, bufs: dict | None = None, on_result=None,
+                               before_batch=None):
+    """Streaming form of `topk_from_host_csr` over a sequence of host (pinned) CSR batches: each batch
+    is (db_indptr, db_indices) — a self-join — or (db_indptr, db_indices, q_indptr, q_indices). Batch
+    i+1's H2D copies run on a copy stream while batch i is built and searched, and batch i's lists are
+    copied back while batch i+1 computes (one device CSR buffer per side, released by an event after
+    each build; two device + two pinned output buffers). Every batch still copies its own inputs in
+    and its own lists out. `before_batch(i)` (optional) is enqueued on the compute stream before batch
+    i's build; `on_result(i, (idx_h, score_h))` is called once batch i's lists are on the host (the
+    pinned buffers are reused two batches later). Returns (h2d_bytes, d2h_bytes) of the last batch."""
+    b = bufs if bufs is not None else {}
+    bits = measures if isinstance(measures, int) else 0
+    if not isinstance(measures, int):
+        for m in measures:
+            bits |= int(m)
+    ms = [m for m in (IP, HAM, JS, COS) if bits & m]
+    mask = 0
+    for m in ms:
+        mask |= m
+    comp = torch.cuda.current_stream()
+    if "copy" not in b:
+        b["copy"] = torch.cuda.Stream()
+    copy = b["copy"]
+    batches = [tuple(x) for x in batches]
+    sep = len(batches[0]) == 4
+    n = batches[0][0].numel() - 1
+    nq = (batches[0][2].numel() - 1) if sep else n
+    if b.get("shape") != (n, nq, sep):
+        b["shape"] = (n, nq, sep)
+        b["dev"] = [None] * 4
+        b["pi"] = torch.empty_like(pi_h, device="cuda")
+        b["sk"] = torch.empty((n, words(N)), dtype=torch.int32, device="cuda")
+        b["qsk"] = torch.empty((nq, words(N)), dtype=torch.int32, device="cuda") if sep else b["sk"]
+        b["ws"] = torch.empty(max(1, workspace_bytes(OP_TOPK, nq, n, N, k)), dtype=torch.uint8, device="cuda")
+        shape = (nq, k) if len(ms) == 1 else (len(ms), nq, k)
+        b["out"] = [(torch.empty(shape, dtype=torch.int32, device="cuda"),
+                     torch.empty(shape, dtype=torch.float32, device="cuda")) for _ in range(2)]
+        b["out_h"] = [(torch.empty(shape, dtype=torch.int32, pin_memory=True),
+                       torch.empty(shape, dtype=torch.float32, pin_memory=True)) for _ in range(2)]
+    for j, t in enumerate(batches[0]):                 # device CSR buffers sized for the largest batch
+        need = max(x[j].numel() for x in batches)
+        if b["dev"][j] is None or b["dev"][j].numel() < need:
+            b["dev"][j] = torch.empty(need, dtype=t.dtype, device="cuda")
+
+    def h2d_batch(i):
+        with torch.cuda.stream(copy):
+            copy.wait_stream(comp) if i == 0 else copy.wait_event(b["built"])   # CSR buffers free
+            nbytes = 0
+            for j, t in enumerate(batches[i]):
+                b["dev"][j][: t.numel()].copy_(t, non_blocking=True)
+                nbytes += t.numel() * t.element_size()
+            b["pi"].copy_(pi_h, non_blocking=True)
+            nbytes += pi_h.numel() * pi_h.element_size()
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        return ev, nbytes
+
+    pend = []
+    h2d = d2h = 0
+    ev_in, nb_in = h2d_batch(0)
+    for i, bt in enumerate(batches):
+        if before_batch is not None:
+            before_batch(i)
+        comp.wait_event(ev_in)
+        h2d = nb_in
+        ni = bt[0].numel() - 1
+        build(b["pi"], d, N, b["dev"][0][: ni + 1], b["dev"][1][: bt[1].numel()], out=b["sk"][:ni])
+        if sep:
+            nqi = bt[2].numel() - 1
+            build(b["pi"], d, N, b["dev"][2][: nqi + 1], b["dev"][3][: bt[3].numel()], out=b["qsk"][:nqi])
+        b["built"] = torch.cuda.Event()
+        b["built"].record(comp)
+        if i + 1 < len(batches):
+            ev_in, nb_in = h2d_batch(i + 1)          # overlaps this batch's top-k
+        oi, osc = b["out"][i % 2]
+        topk(b["qsk"], b["sk"], N, d, mask, k, exclude_self=exclude_self, out_idx=oi, out_score=osc, ws=b["ws"])
+        done = torch.cuda.Event()
+        done.record(comp)
+        hi, hs = b["out_h"][i % 2]
+        with torch.cuda.stream(copy):
+            copy.wait_event(done)
+            hi.copy_(oi, non_blocking=True)
+            hs.copy_(osc, non_blocking=True)
+            ev_out = torch.cuda.Event()
+            ev_out.record(copy)
+        d2h = oi.numel() * 4 + osc.numel() * 4
+        pend.append((i, ev_out))
+        while len(pend) > 1:                         # batch i-1's lists: hand over before its buffers recycle
+            j, ev = pend.pop(0)
+            ev.synchronize()
+            if on_result is not None:
+                on_result(j, b["out_h"][j % 2])
+    comp.wait_stream(copy)                           # the compute stream now orders after the last lists
+    for j, ev in pend:
+        ev.synchronize()
+        if on_result is not None:
+            on_result(j, b["out_h"][j % 2])
+    return h2d, d2h

@@ -617,6 +617,41 @@ def test_topk_from_host_csr_measure_order():
         assert_est_close(gs[t].numpy(), rs)
 
 
+def test_topk_from_host_csr_batches_streaming():
+    """topk_from_host_csr_batches (the bench's e2e leg): several DIFFERENT host batches streamed with
+    overlapped copies — every batch's lists equal the oracle's for that batch (a buffer handed over
+    too early or a copy racing the compute would mix batches). Self-join and separate-query forms."""
+    N, k = 1024, 20
+    got = {}
+    specs = [synth.scaled(synth.LARGE, 700, seed=70 + i) for i in range(4)]
+    d = specs[0].d
+    pi = oracle.make_pi(synth.PI_SEED, d, N)
+    pin = lambda a: torch.from_numpy(a).pin_memory()
+    csr = [synth.make_csr(sp) for sp in specs]
+    batches = [(pin(ip), pin(ix)) for ip, ix in csr]
+    h2d, d2h = bs.topk_from_host_csr_batches(batches, pin(pi.view(np.int32)), d, N, bs.IP, k, exclude_self=True,
+                                             on_result=lambda i, r: got.__setitem__(i, (r[0].clone(), r[1].clone())))
+    assert sorted(got) == [0, 1, 2, 3] and d2h == 700 * k * 8
+    for i, (ip, ix) in enumerate(csr):
+        D, _ = oracle.sketch(pi, d, N, ip, ix)
+        ri, rs = oracle.topk(D, D, N, d, 1, k, exclude_self=True)
+        assert np.array_equal(got[i][0].numpy(), ri)
+        assert_est_close(got[i][1].numpy(), rs)
+    # separate query CSR, two measures
+    got.clear()
+    qcsr = [synth.make_csr(synth.scaled(synth.LARGE, 90, seed=90 + i)) for i in range(3)]
+    batches = [(pin(ip), pin(ix), pin(qp), pin(qx)) for (ip, ix), (qp, qx) in zip(csr[:3], qcsr)]
+    bs.topk_from_host_csr_batches(batches, pin(pi.view(np.int32)), d, N, [bs.COS, bs.JS], k,
+                                  on_result=lambda i, r: got.__setitem__(i, (r[0].clone(), r[1].clone())))
+    for i in range(3):
+        D, _ = oracle.sketch(pi, d, N, *csr[i])
+        Q, _ = oracle.sketch(pi, d, N, *qcsr[i])
+        for t, m in enumerate((4, 8)):
+            ri, rs = oracle.topk(Q, D, N, d, m, k)
+            assert np.array_equal(got[i][0][t].numpy(), ri)
+            assert_est_close(got[i][1][t].numpy(), rs)
+
+
 def test_schedule_independence_stress(monkeypatch):
     """Race / ordering stress in place of compute-sanitizer (closed on this pool,
     profiles/r02_sanitize_memcheck_refused.log): the same inputs through every schedule knob —
