@@ -343,7 +343,7 @@ def run_ours(args):
     # the maximum SM clock with no power cap (clocks below); the sustained figure (measured
     # power-capped at 1342 MHz) is printed beside it. Time basis = the whole top-k call (popcounts,
     # sort, expansion, the kernel, merge), so frac is a lower bound for the kernel itself.
-    engine = os.environ.get("BINSKETCH_ENGINE", "tc")
+    path = bs.topk_path(nq, n, N, d, k)    # the kernel path of this call (binsketch_topk_path)
     f_sm = (clocks["sm_mhz"] or pk.get("sm_max_mhz", 1965.0)) * 1e6
     peak_words = SM_COUNT_B200 * POPC_PER_CLK_SM * f_sm              # word-ops/s at the measured clock
     achieved_words = pairs_per_step * W * args.steps / t_topk
@@ -357,7 +357,7 @@ def run_ours(args):
                  "peak_sustained": sust, "frac_of_sustained": ach / sust,
                  "peak_sustained_basis": "2 x MEASURED_PEAKS bf16_tflops_sustained (power-capped, 1342 MHz)",
                  "traffic": None, "popc_equivalent": popc}
-    if engine != "cuda" and k <= 64 and N <= 6143:
+    if path == "tc_fused":
         roofline = {"bound": "tensor", "kernel": "tc_pairs_kernel (tcgen05.mma kind::i8, query tile in TMEM + fused top-k)",
                     **tc_common,
                     "time_basis": "whole top-k call (popcount + sort + expand + fused kernel + merge); the kernel's "
@@ -366,7 +366,7 @@ def run_ours(args):
             roofline["ncu"] = {k_: v for k_, v in TOPK_NCU.items() if k_ != "dram_bytes_per_launch"}
             roofline["traffic"] = TOPK_NCU["dram_bytes_per_launch"]
             roofline["traffic_unit"] = "DRAM bytes per launch (ncu; operands are L2-resident)"
-    elif engine != "cuda":
+    elif path in ("tc_screen", "tc_pab"):
         # k > 64 or N > 6143: sample thresholds, the tensor-core AND-popcount with the integer screen
         # in its epilogue (survivor lists), the exact list top-k. The screen kernel dominates; its
         # work is the whole contraction (2 * pairs * N int8 ops per measure set), time = the live
@@ -386,6 +386,7 @@ def run_ours(args):
                                    "frac_of_burst": 2.0 * pairs_once * N * args.steps / t_topk / 1e12 / burst,
                                    "time_basis": "whole top-k call (popcounts, sort, expand, sample thresholds, screen, list top-k)"}}
     else:
+        # the CUDA-core kernels (BINSKETCH_ENGINE=cuda, or a small call: binsketch_topk_path)
         roofline = {"bound": "alu", "kernel": "topk_kernel (LOP3+POPC mainloop + fp64 epilogue)",
                     "achieved": popc["achieved"], "peak": popc["peak"], "unit": "Tword-popc/s", "frac": popc["frac"],
                     "peak_basis": popc["peak_basis"], "traffic": None}

@@ -172,13 +172,24 @@ binsketch_status binsketch_estimate(const uint32_t* sketches_a, uint64_t na, con
  * popcount-sorted for the bound); otherwise, for N <= 16383, the fused tensor-core screen
  * (K4d: sample thresholds, the AND-popcount with an integer screen in its epilogue
  * writing survivor lists into the workspace, an exact list top-k), else the tensor-core
- * AND-popcount into a workspace table + the pab-table top-k (K4c / K4b). The screen path runs
+ * AND-popcount into a workspace table + the pab-table top-k (K4c / K4b); small calls (nq * ndb <=
+ * 2^25) run the CUDA-core kernels (binsketch_topk_path names the path). The screen path runs
  * two independent branches on an internal stream forked from and joined back to `stream` with
  * events, so the call stays ordered on `stream` like every other call. */
 binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb,
                                 uint32_t N, uint64_t d, uint32_t measure, uint32_t k, uint32_t flags,
                                 int32_t* out_idx, float* out_score, void* ws, size_t ws_bytes,
                                 binsketch_stream_t stream);
+
+/* Which kernel path binsketch_topk takes for these sizes († reporting / measurement: the bench
+ * names the dominant kernel and its roofline from it; results are identical on every path).
+ * Host-only, no device work. Returns BINSKETCH_PATH_NONE for an empty call,
+ * BINSKETCH_PATH_TC_FUSED (the fused tensor-core top-k, K10), BINSKETCH_PATH_TC_SCREEN
+ * (K4d), BINSKETCH_PATH_TC_PAB (K4c / K4b) or BINSKETCH_PATH_CUDA (the CUDA-core kernels: small
+ * calls, nq * ndb <= 2^25, where the fused kernel has fewer tiles than SMs). */
+enum { BINSKETCH_PATH_NONE = 0, BINSKETCH_PATH_TC_FUSED = 1, BINSKETCH_PATH_TC_SCREEN = 2,
+       BINSKETCH_PATH_TC_PAB = 3, BINSKETCH_PATH_CUDA = 4 };
+int binsketch_topk_path(uint64_t nq, uint64_t ndb, uint32_t N, uint64_t d, uint32_t k);
 
 /* Threshold similarity join — the retrieval step of Experiment 2 (PAPER.md:690-700:
  * "compute the points in the training partition whose similarities are higher than a

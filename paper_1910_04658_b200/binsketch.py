@@ -52,6 +52,7 @@ SIGNATURES = {
     "binsketch_onehot": (_int, [_vp, _u64, _u32, _vp, _vp, _vp, _vp]),
     "binsketch_categorical_estimate": (_int, [_vp, _u64, _vp, _u64, _u32, _u64, _vp, _vp, _sz, _vp]),
     "binsketch_workspace_bytes": (_sz, [_int, _u64, _u64, _u32, _u32]),
+    "binsketch_topk_path": (_int, [_u64, _u64, _u32, _u64, _u32]),
     "binsketch_card_table": (_int, [_u32, _u64, _vp]),
     "binsketch_device_status": (_int, [_vp]),
     "binsketch_launch_count": (_u64, []),
@@ -205,6 +206,14 @@ def popcount(sk: torch.Tensor, N: int, out: torch.Tensor | None = None) -> torch
 
 def workspace_bytes(op: int, na: int, nb: int, N: int, k: int = 0) -> int:
     return int(_lib().binsketch_workspace_bytes(op, na, nb, N, k))
+
+
+PATH_NAMES = {0: "none", 1: "tc_fused", 2: "tc_screen", 3: "tc_pab", 4: "cuda"}
+
+
+def topk_path(nq: int, ndb: int, N: int, d: int, k: int) -> str:
+    """The kernel path binsketch_topk takes for these sizes (host-only query)."""
+    return PATH_NAMES[int(_lib().binsketch_topk_path(nq, ndb, N, d, k))]
 
 
 def _workspace(op, na, nb, N, k, ws):

@@ -116,9 +116,22 @@ bool engine_tc() {
   const char* e = std::getenv("BINSKETCH_ENGINE");
   return e && !std::strcmp(e, "tc");
 }
-bool use_tc(int op, uint32_t N, uint32_t k = 0) {
+bool fused_topk_ok(uint32_t N, uint32_t k) {
+  return k <= bsk::tc_topk_max_k() && N <= bsk::tc_topk_max_n() && bsk::tc_topk_fits(N, k);
+}
+// Small top-k calls (nq * ndb <= 2^25 pairs) go to the CUDA-core kernels: the fused tensor-core
+// kernel then has fewer tiles than SMs and every tile is a heap-filling one (measured, self-joins:
+// 1000 rows JS k = 10 0.158 vs 0.336 ms, 4000 rows IP k = 50 1.19 vs 1.78 ms; 16000 rows IP
+// 7.1 vs 5.1 ms; profiles/r02_topk_engine_sweep.jsonl). BINSKETCH_ENGINE=tc forces the fused kernel.
+constexpr uint64_t kSmallTopkPairs = uint64_t(1) << 25;
+bool small_topk(uint64_t nq, uint64_t ndb) {
+  if (const char* e = std::getenv("BINSKETCH_TOPK_SMALL"))   // "0": no small-call rule (test / A-B knob)
+    if (!std::strcmp(e, "0")) return false;
+  return !engine_tc() && nq <= kSmallTopkPairs && ndb <= kSmallTopkPairs && nq * ndb <= kSmallTopkPairs;
+}
+bool use_tc(int op, uint32_t N, uint32_t k = 0, uint64_t nq = ~uint64_t(0), uint64_t ndb = ~uint64_t(0)) {
   if (engine_cuda()) return false;
-  if (op == BINSKETCH_OP_TOPK) return k <= bsk::tc_topk_max_k() && N <= bsk::tc_topk_max_n() && bsk::tc_topk_fits(N, k);
+  if (op == BINSKETCH_OP_TOPK) return fused_topk_ok(N, k) && !small_topk(nq, ndb);
   // all-pairs estimate: the epilogue (fp64 recipe, 16 B of planes per pair) dominates; at W <= 32
   // the CUDA-core kernel's 32 POPCs per pair are cheaper than the tensor-core pipeline around it
   // (Medium, 1e8 pairs x 4 planes: N = 1000 1.28 vs 1.49 ms; N = 2000 1.87 vs 1.56 ms)
@@ -130,7 +143,7 @@ bool use_tc(int op, uint32_t N, uint32_t k = 0) {
 // fits the budget; otherwise the CUDA-core kernels end to end.
 constexpr size_t kPabBudget = size_t(4) << 30;
 bool use_tc_pab(uint32_t N, uint64_t nq, uint64_t ndb, uint32_t k) {
-  return !engine_cuda() && !use_tc(BINSKETCH_OP_TOPK, N, k) && nq * ndb * 4 <= kPabBudget;
+  return !engine_cuda() && !fused_topk_ok(N, k) && nq * ndb * 4 <= kPabBudget;
 }
 
 // Top-k through the fused tensor-core screen (K4d): sample thresholds and minimum-pab
@@ -227,7 +240,7 @@ Layout layout(int op, uint64_t na, uint64_t nb, uint32_t N, uint32_t k) {
     return l;
   }
   const bool ep = op == BINSKETCH_OP_ESTIMATE && use_est_pab(na, nb);
-  const bool tc = !ep && use_tc(op, N, k);
+  const bool tc = !ep && use_tc(op, N, k, na, nb);
   const bool tcp = (op == BINSKETCH_OP_TOPK && use_tc_pab(N, na, nb, k)) || ep;
   if (tcp) {
     l.ctr = off; off += kAlign;
@@ -466,7 +479,7 @@ static binsketch_status topk_impl(const uint32_t* queries, uint64_t nq, const ui
   if (e == cudaSuccess) e = self ? cudaMemcpyAsync(pd, pq, nq * 4, cudaMemcpyDeviceToDevice, s)
                                  : bsk::launch_popcount(db, ndb, W, pd, s);
   if (e != cudaSuccess) return cuda_status(e);
-  if (ndb > 0 && use_tc(BINSKETCH_OP_TOPK, N, k)) {
+  if (ndb > 0 && use_tc(BINSKETCH_OP_TOPK, N, k, nq, ndb)) {
    for (uint32_t mi = 0; mi < nm; ++mi) {   // fused top-k: one pass per measure
     const uint32_t measure_m = mlist[mi];
     int32_t* out_idx_m = out_idx + (size_t)mi * nq * k;
@@ -611,6 +624,14 @@ bool graphs_enabled() {
   return !(e && !std::strcmp(e, "0"));
 }
 }  // namespace
+
+int binsketch_topk_path(uint64_t nq, uint64_t ndb, uint32_t N, uint64_t d, uint32_t k) {
+  if (nq == 0 || ndb == 0 || k == 0 || N < 2) return BINSKETCH_PATH_NONE;
+  if (use_tc(BINSKETCH_OP_TOPK, N, k, nq, ndb)) return BINSKETCH_PATH_TC_FUSED;
+  if (use_tc_pab(N, nq, ndb, k))
+    return (screen_size_ok(N, nq, ndb, k) && cache().monotone(N, d)) ? BINSKETCH_PATH_TC_SCREEN : BINSKETCH_PATH_TC_PAB;
+  return BINSKETCH_PATH_CUDA;
+}
 
 binsketch_status binsketch_topk(const uint32_t* queries, uint64_t nq, const uint32_t* db, uint64_t ndb, uint32_t N,
                                 uint64_t d, uint32_t measure, uint32_t k, uint32_t flags, int32_t* out_idx,

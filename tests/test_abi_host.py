@@ -34,11 +34,28 @@ def _declared():
 
 def test_exports_every_declared_symbol(lib):
     names = _declared()
-    assert len(names) == 24
+    assert len(names) == 25
     for name in names:
         assert hasattr(lib, name), name
     from paper_1910_04658_b200.binsketch import SIGNATURES
     assert sorted(SIGNATURES) == names      # the binding wraps exactly the ABI
+
+
+def test_topk_path_host(lib, monkeypatch):
+    """binsketch_topk_path (host-only): the kernel path a top-k call takes — the fused tensor-core
+    kernel for the Large shape, the tensor-core screen for Ranking (k = 100), the CUDA-core kernels
+    for small calls (nq * ndb <= 2^25), none for empty calls; the engine override wins."""
+    from paper_1910_04658_b200 import binsketch as bs
+    monkeypatch.setenv("BINSKETCH_TOPK_SMALL", "1")
+    monkeypatch.delenv("BINSKETCH_ENGINE", raising=False)
+    assert bs.topk_path(200_000, 200_000, 1024, 500_000, 50) == "tc_fused"
+    assert bs.topk_path(1000, 100_000, 4096, 102_660, 100) == "tc_screen"
+    assert bs.topk_path(1000, 1000, 1224, 5000, 10) == "cuda"
+    assert bs.topk_path(0, 1000, 1224, 5000, 10) == "none" and bs.topk_path(10, 10, 1224, 5000, 0) == "none"
+    monkeypatch.setenv("BINSKETCH_ENGINE", "tc")
+    assert bs.topk_path(1000, 1000, 1224, 5000, 10) == "tc_fused"
+    monkeypatch.setenv("BINSKETCH_ENGINE", "cuda")
+    assert bs.topk_path(200_000, 200_000, 1024, 500_000, 50) == "cuda"
 
 
 def test_host_entry_points(lib):

@@ -617,6 +617,24 @@ def test_topk_from_host_csr_measure_order():
         assert_est_close(gs[t].numpy(), rs)
 
 
+@pytest.mark.parametrize("measure,k", [(1, 50), (4, 10)])
+def test_topk_small_call_routing(measure, k, monkeypatch):
+    """The product rule: calls with nq * ndb <= 2^25 pairs take the CUDA-core kernels
+    (binsketch_topk_path), larger ones the fused tensor-core kernel; lists identical to the oracle
+    on both sides of the boundary."""
+    monkeypatch.setenv("BINSKETCH_TOPK_SMALL", "1")
+    monkeypatch.delenv("BINSKETCH_ENGINE", raising=False)
+    N, d = 1024, 500_000
+    assert bs.topk_path(1000, 1000, N, d, k) == "cuda"
+    assert bs.topk_path(5792, 5793, N, d, k) == "cuda" and bs.topk_path(5793, 5793, N, d, k) == "tc_fused"
+    assert bs.topk_path(200_000, 200_000, N, d, 50) == "tc_fused"
+    D = _sketches(synth.scaled(synth.LARGE, 1500), N)
+    _check_topk(D, D, N, d, measure, k, exclude_self=True)       # CUDA-core
+    monkeypatch.setenv("BINSKETCH_TOPK_SMALL", "0")
+    assert bs.topk_path(1500, 1500, N, d, k) == "tc_fused"
+    _check_topk(D, D, N, d, measure, k, exclude_self=True)       # fused tensor-core
+
+
 def test_topk_from_host_csr_batches_streaming():
     """topk_from_host_csr_batches (the bench's e2e leg): several DIFFERENT host batches streamed with
     overlapped copies — every batch's lists equal the oracle's for that batch (a buffer handed over
