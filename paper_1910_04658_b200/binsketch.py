@@ -518,7 +518,10 @@ def topk_from_host_csr_batches(batches, pi_h: torch.Tensor, d: int, N: int, meas
 
     def h2d_batch(i):
         with torch.cuda.stream(copy):
-            copy.wait_stream(comp) if i == 0 else copy.wait_event(b["built"])   # CSR buffers free
+            if i == 0:
+                copy.wait_stream(comp)                 # after everything already queued on the caller's stream
+            else:
+                copy.wait_event(b["built"])            # batch i-1's builds no longer read the CSR buffers
             nbytes = 0
             for j, t in enumerate(batches[i]):
                 b["dev"][j][: t.numel()].copy_(t, non_blocking=True)
