@@ -199,6 +199,18 @@ def max_over_ranks(x: float, ws: int, device: str = "cuda") -> float:
     return float(t.item())
 
 
+def csr_sha256(ip_h, ix_h, qp_h=None, qx_h=None) -> str:
+    """sha256(indptr || indices [|| query indptr || query indices]) of the workload's synthetic CSR
+    (the inputs are identified by hash in every bench line)."""
+    import hashlib
+    h = hashlib.sha256(ip_h.tobytes())
+    h.update(ix_h.tobytes())
+    if qp_h is not None:
+        h.update(qp_h.tobytes())
+        h.update(qx_h.tobytes())
+    return h.hexdigest()
+
+
 def aggregate_value(ws: int, units_per_rank_step: int, steps: int, t_max: float) -> float:
     """Whole-job throughput: all ranks' units over the slowest rank's time (weak scaling)."""
     return ws * units_per_rank_step * steps / t_max
@@ -403,7 +415,8 @@ def run_ours(args):
         "config": {"workload": args.workload, "desc": w["desc"], "n": n, "nq": nq, "d": d, "N": N, "k": k,
                    "nnz": nnz, "measure": measure, "pairs_per_step": pairs_per_step,
                    "l2": "flushed between timed steps (256 MB write outside the events)",
-                   "parallelism": f"independent instances x{ws} (no data-path collective)"},
+                   "parallelism": f"independent instances x{ws} (no data-path collective)",
+                   "input_sha256": csr_sha256(ip_h, ix_h, qp_h, qx_h)},
         "stages_ms_per_step": {"build": t_build / args.steps * 1e3, "topk": t_topk / args.steps * 1e3},
         "build_rows_per_s": (n + (nq if qp is not None else 0)) * args.steps / t_build,
         "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,

@@ -1745,11 +1745,13 @@ cudaError_t launch_tc_topk(const uint8_t* Q8, const uint32_t* Qsk, uint64_t nq, 
     count_launch();
     p.meta = meta;
 #if BSK_TOPK_STRICT
+    if (measure == 1u) {   // (the strict bound is IP-only)
     int32_t* tmin = reinterpret_cast<int32_t*>(meta + npad);
     const uint32_t tn = tc_topk_tn(N);
     tile_min_kernel<<<(unsigned)(npad / tn), tn, 0, s>>>(meta, tmin);
     count_launch();
     p.tmin = tmin;
+    }
 #endif
   }
   cudaError_t e = atm ? tc_launch<kTcTopkT, 128>(Q8, D8, p, N, p.heap_smem + p.l_topk_smem, sc.splits, s)
